@@ -1,0 +1,145 @@
+/*
+ * edpc_b200.h -- C ABI of the B200-native EDPC compression hot path.
+ *
+ * Plain C: opaque handles, raw pointers, sizes and int status codes; no torch
+ * or C++ types cross this boundary.  Every call returns EDPC_OK (0) or a
+ * nonzero edpc_status; edpc_last_error() gives the thread's last message.
+ *
+ * Each entry point replaces one reference interface (pkg/src/edpc/...):
+ *
+ *   edpc_quantize_rows     <- coder.py:83-106  quantize_rows / _quantize_kernel :58-80
+ *   edpc_encode_rows       <- coder.py:264-271 ArithmeticEncoder.encode_rows / _encode_kernel :126-165
+ *   edpc_encode_finish     <- coder.py:290-306 ArithmeticEncoder.finish
+ *   edpc_decoder_init      <- coder.py:317-333 ArithmeticDecoder.__init__ (code-register priming)
+ *   edpc_decode_rows       <- coder.py:335-340 ArithmeticDecoder.decode_rows / _decode_kernel :177-229
+ *   edpc_ctx_create        <- pipeline.py:120-137 geometry + EdpcModel(cfg) construction (model.py:187-199)
+ *   edpc_load_params       <- model.py:201-221 flat parameter buffers (parameters() order)
+ *   edpc_get_params        <- model.py:294-300 state_checksum's byte source
+ *   edpc_set_input         <- pipeline.py:44-56 split_lanes (on device)
+ *   edpc_compress_steps    <- pipeline.py:137,194-211 bootstrap + predict/encode/train loop
+ *   edpc_compress_finish   <- pipeline.py:221-227 ArithmeticEncoder.finish per segment
+ *   edpc_set_payloads      <- pipeline.py:258-261 ArithmeticDecoder per segment
+ *   edpc_decompress_steps  <- pipeline.py:261,278-290 bootstrap + predict/decode/train loop
+ *   edpc_get_output        <- pipeline.py:295 join_lanes
+ *   edpc_predict           <- model.py:241-263 EdpcModel.predict
+ *   edpc_train_step        <- model.py:265-281 EdpcModel.train_step
+ *
+ * Threading: calls on one edpc_ctx must be serialised by the caller (the
+ * reference's "one owner thread" rule).  Distinct contexts may
+ * be driven from distinct host threads.
+ */
+#ifndef EDPC_B200_H
+#define EDPC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EDPC_ABI_VERSION 1
+
+typedef enum {
+  EDPC_OK = 0,
+  EDPC_ERR_INVALID = 1,   /* bad argument / geometry (reference: ValueError) */
+  EDPC_ERR_CUDA = 2,      /* CUDA runtime failure or no usable device */
+  EDPC_ERR_CODER = 3,     /* bitstream exhausted (reference: CoderError) */
+  EDPC_ERR_STATE = 4,     /* call out of order: stale cache, finished coder */
+  EDPC_ERR_NOMEM = 5      /* device allocation failed */
+} edpc_status;
+
+typedef struct {
+  int32_t context_len;
+  int32_t embed_dim;
+  int32_t hidden_local;
+  int32_t hidden_global;
+  int32_t lte_ratio;
+  int32_t branches;
+  int32_t lanes;          /* global lane count B (the container's) */
+  int32_t _pad;
+  double lr;
+  double beta1;
+  double beta2;
+  double adam_eps;
+  uint64_t seed;
+} edpc_config;
+
+typedef struct edpc_ctx edpc_ctx;
+
+const char* edpc_last_error(void);
+int edpc_abi_version(void);
+int edpc_device_count(int* count);
+/* 1 if the library was built with the tcgen05 (sm_100a) GEMM path compiled in */
+int edpc_has_tcgen05(void);
+
+/* ---------------------------------------------------------------- coder parity
+ * Stateless w.r.t. the library: the caller owns the coder registers.
+ * dtype: 0 = float32 rows, 1 = float64 rows.  cums rows are 257 x uint32. */
+int edpc_quantize_rows(int device, const void* probs, int64_t n, int dtype, uint32_t* cums);
+
+/* enc_state = {low, high, pending, bitpos}; buf holds cap bytes, zero beyond bitpos. */
+int edpc_encode_rows(int device, int64_t* enc_state, uint8_t* buf, int64_t cap,
+                     const uint32_t* cums, const int32_t* symbols, int64_t n);
+int edpc_encode_finish(int device, int64_t* enc_state, uint8_t* buf, int64_t cap,
+                       int64_t* bit_length);
+
+/* dec_state = {low, high, code, bitpos}; decoded symbols into out (int32);
+ * *done = rows decoded (< n means exhausted: EDPC_ERR_CODER). */
+int edpc_decoder_init(int device, int64_t* dec_state, const uint8_t* data, int64_t nbytes,
+                      int64_t bit_length);
+int edpc_decode_rows(int device, int64_t* dec_state, const uint8_t* data, int64_t nbytes,
+                     int64_t bit_length, const uint32_t* cums, int64_t n, int32_t* out,
+                     int64_t* done);
+
+/* ------------------------------------------------------------ context (stream)
+ * One context = one container being (de)compressed on one device.
+ * lane_begin/lane_count select this device's contiguous share of the B lanes
+ * (whole segments); single-GPU callers pass 0 and cfg->lanes.
+ * original_len is the full stream length n (L = ceil(n / B)). */
+int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_len,
+                    int32_t device, int32_t lane_begin, int32_t lane_count, edpc_ctx** out);
+int edpc_ctx_destroy(edpc_ctx* ctx);
+int edpc_ctx_info(edpc_ctx* ctx, int64_t* lane_len, int64_t* n_params, int64_t* n_shared);
+
+/* fp32 parameters in the reference parameters() order (model.py:237-239),
+ * full lane_mats for all B lanes (the context keeps its own lanes' slice). */
+int edpc_load_params(edpc_ctx* ctx, const float* params, int64_t count);
+int edpc_get_params(edpc_ctx* ctx, float* params, int64_t count);
+
+/* compress side: stream bytes (host or device pointer) -> device lane matrix */
+int edpc_set_input(edpc_ctx* ctx, const uint8_t* data, int64_t n, int on_device);
+/* runs lane columns [i0, i1) (bootstrap for i < context_len, model steps after) */
+int edpc_compress_steps(edpc_ctx* ctx, int64_t i0, int64_t i1);
+/* finishes every local segment; bit_lengths[S_local], payload bytes total */
+int edpc_compress_finish(edpc_ctx* ctx, int64_t* bit_lengths, int64_t* total_bytes);
+/* concatenated local payloads (ceil(bits/8) bytes each, in segment order) */
+int edpc_get_payloads(edpc_ctx* ctx, uint8_t* out, int64_t cap);
+
+/* decompress side */
+int edpc_set_payloads(edpc_ctx* ctx, const uint8_t* data, const int64_t* bit_lengths);
+int edpc_decompress_steps(edpc_ctx* ctx, int64_t i0, int64_t i1);
+int edpc_get_output(edpc_ctx* ctx, uint8_t* out, int64_t n_local);
+
+/* model-level seam: one predict / train_step on caller contexts (host memory).
+ * contexts: lane_count x context_len bytes; probs: lane_count x 256 fp32
+ * (may be NULL); targets: lane_count bytes; loss: mean NLL in nats over the
+ * local lanes' share (sum_local / B). */
+int edpc_predict(edpc_ctx* ctx, const uint8_t* contexts, float* probs);
+int edpc_train_step(edpc_ctx* ctx, const uint8_t* targets, float* loss);
+/* probs of the last model step run by compress/decompress_steps (debug taps) */
+int edpc_last_probs(edpc_ctx* ctx, float* probs);
+
+/* --------------------------------------------------- multi-GPU step phases
+ * For G > 1 the host drives each model step as: phase 0 (forward, coder,
+ * backward, per-lane FDM update; shared-parameter gradients left as 8 fixed
+ * lane-group partials) -> exchange of the partials -> phase 1 (canonical
+ * tree reduction + Adam).  edpc_grad_partials exposes the device buffer. */
+int edpc_step_phase(edpc_ctx* ctx, int64_t i, int32_t phase, int32_t decompress);
+int edpc_grad_partials(edpc_ctx* ctx, float** dev_ptr, int64_t* n_shared);
+
+int edpc_sync(edpc_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EDPC_B200_H */

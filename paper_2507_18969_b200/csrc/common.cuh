@@ -1,0 +1,73 @@
+// Shared helpers for the EDPC B200 kernels: status plumbing, warp reductions.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/edpc_b200.h"
+
+namespace edpc {
+
+void set_error(const std::string& msg);
+
+struct Status {
+  int code;
+};
+
+#define EDPC_CUDA_TRY(expr)                                                          \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess) {                                                         \
+      ::edpc::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e) + " @" +  \
+                        __FILE__ + ":" + std::to_string(__LINE__));                  \
+      return EDPC_ERR_CUDA;                                                          \
+    }                                                                                \
+  } while (0)
+
+#define EDPC_CHECK_ARG(cond, msg)       \
+  do {                                  \
+    if (!(cond)) {                      \
+      ::edpc::set_error(msg);           \
+      return EDPC_ERR_INVALID;          \
+    }                                   \
+  } while (0)
+
+#define EDPC_TRY(expr)         \
+  do {                         \
+    int _s = (expr);           \
+    if (_s != EDPC_OK) return _s; \
+  } while (0)
+
+constexpr int kVocab = 256;
+constexpr int kTotal = 1 << 16;
+constexpr int kNumGroups = 8;  // fixed lane groups of the G-invariant reduction
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+__device__ __forceinline__ double warp_sum_d(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Lane-group boundaries of the canonical gradient reduction: group g covers
+// global lanes [g*B/8, (g+1)*B/8) (floor division; groups may be empty when B<8).
+__host__ __device__ __forceinline__ int group_begin(int g, int B) {
+  return (int)(((int64_t)g * B) / kNumGroups);
+}
+
+inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+}  // namespace edpc

@@ -1,0 +1,178 @@
+// Generic fp32 SIMT GEMM with fused epilogues: the any-shape path.
+//
+// C[z](m, n) = sum_{s < nsum} sum_{k in K-range} A_s(m, k) * B_s(k, n)
+//   A(m,k) = TA ? A[k*lda + m] : A[m*lda + k]
+//   B(k,n) = TB ? B[n*ldb + k] : B[k*ldb + n]
+// blockIdx.z = zb + nzb * zg: zb selects a batch (pointer strides sA/sB), zg a
+// lane group of the canonical gradient reduction (the K range is that
+// group's lanes; used by the weight-gradient GEMMs whose K dim is lanes).
+//
+// The accumulation order is fixed by the tile loop (k ascending in BK
+// chunks, s ascending), so results are bitwise reproducible run to run and
+// identical between compress and decompress.  This path serves every model
+// shape (the reference test-suite's tiny configs included); tc_gemm.cuh is
+// the tcgen05 fast path for the paper dims.
+#pragma once
+
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace edpc {
+
+struct GemmShape {
+  int M, N, K;
+  const float* A;
+  int64_t lda, sA, sA_sum;
+  const float* B;
+  int64_t ldb, sB, sB_sum;
+  int nzb;        // batches
+  int nsum;       // summed sub-problems
+  // lane-group K split (wgrad): groups [g0, g0 + ngroups) of B_global lanes,
+  // local lanes start at global lane `lane0`.  ngroups == 0: K range [0, K).
+  int ngroups, g0, B_global, lane0;
+};
+
+constexpr int kSimtBM = 64, kSimtBN = 64, kSimtBK = 16;
+
+template <bool TA, bool TB, class Epi>
+__global__ void __launch_bounds__(256) k_gemm_simt(GemmShape g, Epi epi) {
+  __shared__ float As[kSimtBK][kSimtBM + 4];
+  __shared__ float Bs[kSimtBK][kSimtBN + 4];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  const int m0 = blockIdx.y * kSimtBM, n0 = blockIdx.x * kSimtBN;
+  const int zb = blockIdx.z % g.nzb, zg = blockIdx.z / g.nzb;
+  int k_begin = 0, k_end = g.K;
+  if (g.ngroups > 0) {
+    int gg = g.g0 + zg;
+    k_begin = group_begin(gg, g.B_global) - g.lane0;
+    k_end = group_begin(gg + 1, g.B_global) - g.lane0;
+  }
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+
+  for (int s = 0; s < g.nsum; ++s) {
+    const float* A = g.A + zb * g.sA + s * g.sA_sum;
+    const float* B = g.B + zb * g.sB + s * g.sB_sum;
+    for (int k0 = k_begin; k0 < k_end; k0 += kSimtBK) {
+      // A tile: BM x BK (1024 elements, 4 per thread)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        int e = tid + r * 256;
+        int mm, kk;
+        if (TA) {
+          mm = e & (kSimtBM - 1);
+          kk = e / kSimtBM;
+        } else {
+          kk = e & (kSimtBK - 1);
+          mm = e / kSimtBK;
+        }
+        int gm = m0 + mm, gk = k0 + kk;
+        float v = 0.f;
+        if (gm < g.M && gk < k_end) v = TA ? A[(int64_t)gk * g.lda + gm] : A[(int64_t)gm * g.lda + gk];
+        As[kk][mm] = v;
+      }
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        int e = tid + r * 256;
+        int nn, kk;
+        if (TB) {
+          kk = e & (kSimtBK - 1);
+          nn = e / kSimtBK;
+        } else {
+          nn = e & (kSimtBN - 1);
+          kk = e / kSimtBN;
+        }
+        int gn = n0 + nn, gk = k0 + kk;
+        float v = 0.f;
+        if (gn < g.N && gk < k_end) v = TB ? B[(int64_t)gn * g.ldb + gk] : B[(int64_t)gk * g.ldb + gn];
+        Bs[kk][nn] = v;
+      }
+      __syncthreads();
+#pragma unroll
+      for (int kk = 0; kk < kSimtBK; ++kk) {
+        float a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+      __syncthreads();
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int m = m0 + ty + 16 * i;
+    if (m >= g.M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = n0 + tx + 16 * j;
+      if (n < g.N) epi(zb, zg, m, n, acc[i][j]);
+    }
+  }
+}
+
+template <bool TA, bool TB, class Epi>
+inline cudaError_t gemm_simt(const GemmShape& g, const Epi& epi, cudaStream_t st) {
+  int nz = g.nzb * (g.ngroups > 0 ? g.ngroups : 1);
+  dim3 grid((unsigned)cdiv(g.N, kSimtBN), (unsigned)cdiv(g.M, kSimtBM), (unsigned)nz);
+  if (g.M <= 0 || g.N <= 0 || nz <= 0) return cudaSuccess;
+  k_gemm_simt<TA, TB, Epi><<<grid, 256, 0, st>>>(g, epi);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- epilogues
+
+// C[zb] = acc + bias[zb] (row-broadcast); ldc row stride, sC batch stride
+struct EpiBias {
+  float* C;
+  int64_t ldc, sC;
+  const float* bias;
+  int64_t sBias;
+  __device__ void operator()(int zb, int, int m, int n, float acc) const {
+    C[zb * sC + (int64_t)m * ldc + n] = acc + bias[zb * sBias + n];
+  }
+};
+
+// C = acc + bias + resid (MBRB out-projection + residual, model.py:102)
+struct EpiBiasResid {
+  float* C;
+  int64_t ldc;
+  const float* bias;
+  const float* resid;
+  int64_t ldr;
+  __device__ void operator()(int, int, int m, int n, float acc) const {
+    C[(int64_t)m * ldc + n] = (acc + bias[n]) + resid[(int64_t)m * ldr + n];
+  }
+};
+
+// plain store (dgrad outputs)
+struct EpiStore {
+  float* C;
+  int64_t ldc;
+  __device__ void operator()(int, int, int m, int n, float acc) const {
+    C[(int64_t)m * ldc + n] = acc;
+  }
+};
+
+// weight-gradient partial of lane group (g0 + zg) at param offset (+ zb*sOff)
+struct EpiPartial {
+  float* partials;     // [8][n_shared]
+  int64_t n_shared;
+  int64_t off, sOff;   // parameter offset in the shared flat layout, batch stride
+  int64_t ldw;         // row stride of the weight (its N)
+  int g0;
+  __device__ void operator()(int zb, int zg, int m, int n, float acc) const {
+    partials[(int64_t)(g0 + zg) * n_shared + off + zb * sOff + (int64_t)m * ldw + n] = acc;
+  }
+};
+
+}  // namespace edpc

@@ -1,0 +1,522 @@
+// Per-step elementwise / per-lane kernels of the EDPC predictor and its online
+// update.  Every reduction has a fixed order (warp butterflies, sequential
+// lane loops, the 8-group tree), so a step is bitwise reproducible and the
+// decoder replays the encoder's trajectory exactly (pkg/src/edpc/__init__.py:1-7).
+#pragma once
+
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "coder.cuh"
+#include "common.cuh"
+
+namespace edpc {
+
+// where a step's context bytes live: row b of the lane matrix, columns
+// [i - T, i) are the context (model.py:252-255) and column i the target
+struct ByteCols {
+  const uint8_t* base;
+  int64_t ld;
+};
+
+struct StepIdx {
+  const int64_t* i;  // current lane column (device)
+  const int64_t* t;  // Adam step count (device), model.py:230
+};
+
+__device__ __forceinline__ float gelu_cdf(float x) {
+  return 0.5f * (1.0f + erff(x * 0.70710678118654752440f));
+}
+
+// ------------------------------------------------------ gather + layer norm
+
+// x = E[ctx] (model.py:255), then LN (nn.py:103-113, population variance,
+// eps 1e-5 under the sqrt).  One warp per lane.  gather=false: x is input.
+template <bool kGather>
+__global__ void __launch_bounds__(256)
+k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE, int F, int Bl,
+           float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
+           float* __restrict__ xhat, float* __restrict__ rstd, float* __restrict__ x0) {
+  const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= Bl) return;
+  float* xr = x + (int64_t)b * F;
+  float s = 0.f;
+  if (kGather) {
+    const int64_t col0 = *si.i - T;
+    const uint8_t* row = src.base + (int64_t)b * src.ld + col0;
+    for (int f = lane; f < F; f += 32) {
+      int p = f / DE, d = f - p * DE;
+      float v = E[(int)row[p] * DE + d];
+      xr[f] = v;
+      s += v;
+    }
+  } else {
+    for (int f = lane; f < F; f += 32) s += xr[f];
+  }
+  const float mean = warp_sum(s) / (float)F;
+  float q = 0.f;
+  for (int f = lane; f < F; f += 32) {
+    float d = xr[f] - mean;
+    q += d * d;
+  }
+  const float var = warp_sum(q) / (float)F;
+  const float r = 1.0f / sqrtf(var + 1e-5f);
+  for (int f = lane; f < F; f += 32) {
+    float h = (xr[f] - mean) * r;
+    xhat[(int64_t)b * F + f] = h;
+    x0[(int64_t)b * F + f] = h * gain[f] + bias[f];
+  }
+  if (lane == 0) rstd[b] = r;
+}
+
+// ff = GeLU(prod_i H_i) (model.py:98-101, _kernels.py:35-42)
+__global__ void k_mbrb_act(const float* __restrict__ H, int K, int64_t plane, float* __restrict__ ff) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= plane) return;
+  float p = H[e];
+  for (int z = 1; z < K; ++z) p = p * H[z * plane + e];
+  ff[e] = p * gelu_cdf(p);
+}
+
+// MBRB backward epilogue of the out-projection dgrad (model.py:107-119):
+// g_prod = g_ff * GeLU'(prod); g_H_z = g_prod * prod_{j != z} H_j
+struct EpiBwdAct {
+  const float* H;
+  float* GH;
+  int K;
+  int64_t plane, ld;
+  __device__ void operator()(int, int, int m, int n, float acc) const {
+    const int64_t e = (int64_t)m * ld + n;
+    float p = H[e];
+    for (int z = 1; z < K; ++z) p = p * H[z * plane + e];
+    const float cdf = gelu_cdf(p);
+    const float pdf = 0.39894228040143267794f * expf(-0.5f * p * p);
+    const float gp = acc * (cdf + p * pdf);
+    for (int z = 0; z < K; ++z) {
+      float g = gp;
+      for (int j = 0; j < K; ++j)
+        if (j != z) g = g * H[j * plane + e];
+      GH[z * plane + e] = g;
+    }
+  }
+};
+
+// LN backward + residual (nn.py:116-125, model.py:120-121); one warp per lane
+__global__ void __launch_bounds__(256)
+k_ln_bwd(const float* __restrict__ gx0, const float* __restrict__ xhat,
+         const float* __restrict__ rstd, const float* __restrict__ gain,
+         const float* __restrict__ up, float* __restrict__ out, int F, int Bl) {
+  const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= Bl) return;
+  const int64_t o = (int64_t)b * F;
+  float s1 = 0.f, s2 = 0.f;
+  for (int f = lane; f < F; f += 32) {
+    float g = gx0[o + f] * gain[f];
+    s1 += g;
+    s2 += g * xhat[o + f];
+  }
+  const float gm = warp_sum(s1) / (float)F;
+  const float gxm = warp_sum(s2) / (float)F;
+  const float r = rstd[b];
+  for (int f = lane; f < F; f += 32) {
+    float g = gx0[o + f] * gain[f];
+    out[o + f] = (g - gm - xhat[o + f] * gxm) * r + up[o + f];
+  }
+}
+
+// ------------------------------------------- lane-group column reductions
+
+// partials[g0+zg][off + z*sOff + n] = sum over the group's lanes (ascending)
+// of src[z*sz + b*ld + n] (* mul[b*ld + n] when mul != null): bias and LN
+// gradients (nn.py:94, :118-119) as 8 fixed lane-group partials.
+__global__ void k_colsum_groups(const float* __restrict__ src, int64_t ld, int64_t sz,
+                                const float* __restrict__ mul, int N, float* __restrict__ partials,
+                                int64_t n_shared, int64_t off, int64_t sOff, int g0, int B_global,
+                                int lane0) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  const int z = blockIdx.y;
+  const int gg = g0 + blockIdx.z;
+  if (n >= N) return;
+  const int b0 = group_begin(gg, B_global) - lane0, b1 = group_begin(gg + 1, B_global) - lane0;
+  const float* s = src + z * sz + n;
+  float acc = 0.f;
+  if (mul) {
+    for (int b = b0; b < b1; ++b) acc += s[(int64_t)b * ld] * mul[(int64_t)b * ld + n];
+  } else {
+    for (int b = b0; b < b1; ++b) acc += s[(int64_t)b * ld];
+  }
+  partials[(int64_t)gg * n_shared + off + z * sOff + n] = acc;
+}
+
+// ---------------------------------------------------- LTE per-lane matrix
+
+// mixed_b = down_b . U_b (nn.py:168-174); one warp per lane
+__global__ void __launch_bounds__(256)
+k_fdm_fwd(const float* __restrict__ down, const float* __restrict__ U, float* __restrict__ mixed,
+          int FP, int Bl) {
+  const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= Bl) return;
+  const float* d = down + (int64_t)b * FP;
+  const float* u = U + (int64_t)b * FP * FP;
+  for (int j = lane; j < FP; j += 32) {
+    float acc = 0.f;
+    for (int i = 0; i < FP; ++i) acc = fmaf(d[i], u[(int64_t)i * FP + j], acc);
+    mixed[(int64_t)b * FP + j] = acc;
+  }
+}
+
+struct AdamConsts {
+  float lr, b1, b2, k1, k2, eps;
+};
+
+__device__ __forceinline__ double ipow(double a, int64_t e) {
+  double r = 1.0;
+  while (e) {
+    if (e & 1) r *= a;
+    e >>= 1;
+    a *= a;
+  }
+  return r;
+}
+
+__device__ __forceinline__ void adam_bc(const AdamConsts& c, double b1d, double b2d, int64_t t,
+                                        float& bc1, float& bc2) {
+  bc1 = (float)(1.0 - ipow(b1d, t));
+  bc2 = (float)(1.0 - ipow(b2d, t));
+}
+
+// _kernels.py:26-31 in fp32
+__device__ __forceinline__ void adam_elem(float& w, float& m, float& v, float g,
+                                          const AdamConsts& c, float bc1, float bc2) {
+  float mi = c.b1 * m + c.k1 * g;
+  float vi = c.b2 * v + c.k2 * (g * g);
+  m = mi;
+  v = vi;
+  w -= (c.lr * (mi / bc1)) / (sqrtf(vi / bc2) + c.eps);
+}
+
+// Fused FDM backward + per-lane Adam (nn.py:177-179 then _kernels.py:18-32 on
+// lane_mats): g_down_b = g_mixed_b . U_b^T with the pre-update U, then
+// U_b -= Adam(down_b (x) g_mixed_b).  U, m, v are read and written once.
+__global__ void __launch_bounds__(256)
+k_fdm_bwd_adam(const float* __restrict__ down, const float* __restrict__ gmix,
+               float* __restrict__ U, float* __restrict__ Um, float* __restrict__ Uv,
+               float* __restrict__ gdown, int FP, int Bl, StepIdx si, AdamConsts c, double b1d,
+               double b2d) {
+  const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= Bl) return;
+  float bc1, bc2;
+  adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
+  const float* d = down + (int64_t)b * FP;
+  const float* gm = gmix + (int64_t)b * FP;
+  const int64_t base = (int64_t)b * FP * FP;
+  for (int i = 0; i < FP; ++i) {
+    float acc = 0.f;
+    const float di = d[i];
+    for (int j = lane; j < FP; j += 32) {
+      const int64_t e = base + (int64_t)i * FP + j;
+      float w = U[e], m = Um[e], v = Uv[e];
+      const float gj = gm[j];
+      acc = fmaf(gj, w, acc);
+      adam_elem(w, m, v, di * gj, c, bc1, bc2);
+      U[e] = w;
+      Um[e] = m;
+      Uv[e] = v;
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) gdown[(int64_t)b * FP + i] = acc;
+  }
+}
+
+// ------------------------------------------------ embedding scatter-add
+
+// Deterministic replacement of np.add.at (model.py:276-278).  Each chunk is
+// <= 64 consecutive lanes of one lane group; thread c owns byte value c and
+// walks the chunk's (lane, position) entries in order.  chunk_tab[k] =
+// {group, local lane begin, local lane end}.
+__global__ void __launch_bounds__(256)
+k_embed_grad_chunks(ByteCols src, StepIdx si, int T, int DE, int F,
+                    const float* __restrict__ gx, const int* __restrict__ chunk_tab,
+                    float* __restrict__ sub) {
+  __shared__ uint8_t cbytes[64 * 64];
+  const int k = blockIdx.x;
+  const int lb = chunk_tab[3 * k + 1], le = chunk_tab[3 * k + 2];
+  const int nl = le - lb;
+  const int64_t col0 = *si.i - T;
+  for (int e = threadIdx.x; e < nl * T; e += blockDim.x) {
+    int bl = e / T, p = e - bl * T;
+    cbytes[e] = src.base[(int64_t)(lb + bl) * src.ld + col0 + p];
+  }
+  __syncthreads();
+  const int c = threadIdx.x;
+  for (int d0 = 0; d0 < DE; d0 += 16) {
+    float acc[16];
+#pragma unroll
+    for (int d = 0; d < 16; ++d) acc[d] = 0.f;
+    for (int e = 0; e < nl * T; ++e) {
+      if (cbytes[e] != c) continue;
+      int bl = e / T, p = e - bl * T;
+      const float* g = gx + (int64_t)(lb + bl) * F + p * DE + d0;
+#pragma unroll
+      for (int d = 0; d < 16; ++d)
+        if (d0 + d < DE) acc[d] += g[d];
+    }
+#pragma unroll
+    for (int d = 0; d < 16; ++d)
+      if (d0 + d < DE) sub[((int64_t)k * 256 + c) * DE + d0 + d] = acc[d];
+  }
+}
+
+// group partial = sum of its chunks, in chunk order
+__global__ void k_embed_grad_reduce(const float* __restrict__ sub, const int* __restrict__ grp_chunks,
+                                    int DE, float* __restrict__ partials, int64_t n_shared,
+                                    int64_t off) {
+  const int gl = blockIdx.y;  // local group slot
+  const int gg = grp_chunks[3 * gl], k0 = grp_chunks[3 * gl + 1], k1 = grp_chunks[3 * gl + 2];
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 256 * DE) return;
+  float acc = 0.f;
+  for (int k = k0; k < k1; ++k) acc += sub[(int64_t)k * 256 * DE + e];
+  partials[(int64_t)gg * n_shared + off + e] = acc;
+}
+
+// ------------------------------------------------------- Adam (shared)
+
+// grad = ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)) -- the canonical G-invariant
+// tree over the 8 lane groups -- then fused Adam (_kernels.py:18-32).
+__global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, float* __restrict__ V,
+                              const float* __restrict__ P, int64_t n, StepIdx si, AdamConsts c,
+                              double b1d, double b2d) {
+  float bc1, bc2;
+  adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float q[8];
+#pragma unroll
+    for (int g = 0; g < 8; ++g) q[g] = P[g * n + e];
+    const float grad = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+    float w = W[e], m = M[e], v = V[e];
+    adam_elem(w, m, v, grad, c, bc1, bc2);
+    W[e] = w;
+    M[e] = m;
+    V[e] = v;
+  }
+}
+
+// --------------------------------------------------- softmax + quantizer
+
+enum QuantMode { kProbsOnly = 0, kEncode = 1, kDecode = 2 };
+
+// nn.py:186-190 softmax in fp32, then the quantizer on the exact doubles of
+// the fp32 probabilities (coder.py:58-80).  kEncode writes the target
+// symbol's (cum_lo | freq << 16) into intervals[i][b]; kDecode writes the
+// row's cumulative table (cum[0..255] as u16; cum[256] = 65536 implied).
+template <int kMode>
+__global__ void __launch_bounds__(256)
+k_softmax_quant(const float* __restrict__ logits, float* __restrict__ probs, int Bl,
+                ByteCols src, StepIdx si, uint32_t* __restrict__ intervals,
+                uint16_t* __restrict__ cdf16) {
+  const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= Bl) return;
+  const float* lg = logits + (int64_t)b * 256 + lane * 8;
+  float x[8];
+  float4 v0 = *reinterpret_cast<const float4*>(lg);
+  float4 v1 = *reinterpret_cast<const float4*>(lg + 4);
+  x[0] = v0.x; x[1] = v0.y; x[2] = v0.z; x[3] = v0.w;
+  x[4] = v1.x; x[5] = v1.y; x[6] = v1.z; x[7] = v1.w;
+  float mx = x[0];
+#pragma unroll
+  for (int j = 1; j < 8; ++j) mx = fmaxf(mx, x[j]);
+  mx = warp_max(mx);
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    x[j] = expf(x[j] - mx);
+    s += x[j];
+  }
+  s = warp_sum(s);
+  double p[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    x[j] = x[j] / s;
+    p[j] = (double)x[j];
+  }
+  float* pr = probs + (int64_t)b * 256 + lane * 8;
+  *reinterpret_cast<float4*>(pr) = make_float4(x[0], x[1], x[2], x[3]);
+  *reinterpret_cast<float4*>(pr + 4) = make_float4(x[4], x[5], x[6], x[7]);
+  if (kMode == kProbsOnly) return;
+  int freq[8];
+  warp_quantize<false>(p, freq);
+  uint32_t cum[8];
+  warp_cdf(freq, cum);
+  const int64_t i = *si.i;
+  if (kMode == kEncode) {
+    const int tgt = src.base[(int64_t)b * src.ld + i];
+    if ((tgt >> 3) == lane) {
+      uint32_t lo = 0, fr = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if ((tgt & 7) == j) {
+          lo = cum[j];
+          fr = (uint32_t)freq[j];
+        }
+      intervals[i * Bl + b] = lo | (fr << 16);
+    }
+  } else {
+    uint16_t* dst = cdf16 + (int64_t)b * 256 + lane * 8;
+    uint4 pk;
+    pk.x = cum[0] | (cum[1] << 16);
+    pk.y = cum[2] | (cum[3] << 16);
+    pk.z = cum[4] | (cum[5] << 16);
+    pk.w = cum[6] | (cum[7] << 16);
+    *reinterpret_cast<uint4*>(dst) = pk;
+  }
+}
+
+// dlogits = (probs - onehot(target)) / B (nn.py:204-210); nll for the loss
+__global__ void k_dlogits(const float* __restrict__ probs, ByteCols src, StepIdx si, int Bl,
+                          float Bf, float* __restrict__ g, float* __restrict__ nll) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)Bl * 256) return;
+  const int b = (int)(e >> 8), v = (int)(e & 255);
+  const int tgt = src.base[(int64_t)b * src.ld + *si.i];
+  float p = probs[e];
+  if (v == tgt) {
+    if (nll) nll[b] = -logf(p);
+    p = p - 1.0f;
+  }
+  g[e] = p / Bf;
+}
+
+// --------------------------------------------------------------- coder
+
+// bootstrap intervals: the first min(t, L) columns under the uniform table
+// (pipeline.py:84-90, coder.py:118-123)
+__global__ void k_boot_intervals(const uint8_t* __restrict__ mat, int64_t L, int Bl, int64_t ncols,
+                                 uint32_t* __restrict__ intervals) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= ncols * Bl) return;
+  const int64_t i = e / Bl;
+  const int b = (int)(e - i * Bl);
+  const uint32_t s = mat[(int64_t)b * L + i];
+  intervals[e] = (s * 256u) | (256u << 16);
+}
+
+// Stage B of DPCA on the device: one thread per segment walks lane columns
+// [i0, i1) and its lanes in order (pipeline.py:152-153, 182-184).
+__global__ void k_encode_columns(const uint32_t* __restrict__ intervals, int Bl, int spl, int Sl,
+                                 int64_t i0, int64_t i1, int64_t* __restrict__ enc_state,
+                                 uint32_t* __restrict__ words, int64_t cap_words) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= Sl) return;
+  int64_t* stp = enc_state + 4 * s;
+  EncState st{(uint64_t)stp[0], (uint64_t)stp[1], (uint64_t)stp[2], (uint64_t)stp[3]};
+  BitWriter w;
+  w.open(words + (int64_t)s * cap_words, st.bitpos);
+  const int b0 = s * spl;
+  for (int64_t i = i0; i < i1; ++i) {
+    const uint32_t* row = intervals + i * Bl + b0;
+    for (int b = 0; b < spl; ++b) {
+      const uint32_t iv = row[b];
+      const uint32_t lo = iv & 0xffffu;
+      enc_symbol(st, w, lo, lo + (iv >> 16));
+    }
+  }
+  w.close();
+  stp[0] = (int64_t)st.low;
+  stp[1] = (int64_t)st.high;
+  stp[2] = (int64_t)st.pending;
+  stp[3] = (int64_t)w.bitpos;
+}
+
+__global__ void k_encode_finish_all(int64_t* __restrict__ enc_state, uint32_t* __restrict__ words,
+                                    int64_t cap_words, int Sl) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= Sl) return;
+  int64_t* stp = enc_state + 4 * s;
+  EncState st{(uint64_t)stp[0], (uint64_t)stp[1], (uint64_t)stp[2], (uint64_t)stp[3]};
+  BitWriter w;
+  w.open(words + (int64_t)s * cap_words, st.bitpos);
+  enc_finish(st, w);
+  w.close();
+  stp[2] = 0;
+  stp[3] = (int64_t)w.bitpos;
+}
+
+__global__ void k_decoder_init_all(int64_t* __restrict__ dec_state, const uint8_t* __restrict__ pay,
+                                   const int64_t* __restrict__ pay_off,
+                                   const int64_t* __restrict__ bits, int Sl) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= Sl) return;
+  const uint8_t* d = pay + pay_off[s];
+  uint64_t code = 0;
+  for (int k = 0; k < 32; ++k) code = (code << 1) | read_bit(d, bits[s], k);
+  int64_t* stp = dec_state + 4 * s;
+  stp[0] = 0;
+  stp[1] = (int64_t)kMask32;
+  stp[2] = (int64_t)code;
+  stp[3] = 32;
+}
+
+// One warp per segment decodes lane column i for its lanes (pipeline.py:272-275);
+// uniform=true is the bootstrap table.  On exhaustion the segment's error
+// flag is set and its remaining symbols decode as 0 (host raises CoderError).
+__global__ void k_decode_column(uint8_t* __restrict__ mat, int64_t L, StepIdx si, int spl, int Sl,
+                                const uint16_t* __restrict__ cdf16, bool uniform,
+                                int64_t* __restrict__ dec_state, const uint8_t* __restrict__ pay,
+                                const int64_t* __restrict__ pay_off,
+                                const int64_t* __restrict__ bits, int* __restrict__ err) {
+  const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (s >= Sl) return;
+  const int64_t i = *si.i;
+  int64_t* stp = dec_state + 4 * s;
+  const bool dead = err[s] != 0;
+  DecState st{(uint64_t)stp[0], (uint64_t)stp[1], (uint64_t)stp[2], stp[3]};
+  const uint8_t* data = pay + pay_off[s];
+  const int64_t nbits = bits[s];
+  bool ok = !dead;
+  for (int bl = 0; bl < spl; ++bl) {
+    const int b = s * spl + bl;
+    int sym = 0;
+    if (ok) {
+      uint32_t cum[8];
+      if (uniform) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) cum[j] = (uint32_t)(lane * 8 + j) * 256u;
+      } else {
+        uint4 pk = *reinterpret_cast<const uint4*>(cdf16 + (int64_t)b * 256 + lane * 8);
+        cum[0] = pk.x & 0xffffu; cum[1] = pk.x >> 16;
+        cum[2] = pk.y & 0xffffu; cum[3] = pk.y >> 16;
+        cum[4] = pk.z & 0xffffu; cum[5] = pk.z >> 16;
+        cum[6] = pk.w & 0xffffu; cum[7] = pk.w >> 16;
+      }
+      const uint64_t span = st.high - st.low + 1;
+      const uint64_t value = dec_value(st, span);
+      uint32_t c_lo, c_hi;
+      sym = warp_find_symbol(cum, value, c_lo, c_hi);
+      ok = dec_advance(st, data, nbits, span, c_lo, c_hi);
+      if (!ok) sym = 0;
+    }
+    if (lane == 0) mat[(int64_t)b * L + i] = (uint8_t)sym;
+  }
+  if (lane == 0) {
+    if (!ok && !dead) err[s] = 1;
+    stp[0] = (int64_t)st.low;
+    stp[1] = (int64_t)st.high;
+    stp[2] = (int64_t)st.code;
+    stp[3] = st.bitpos;
+  }
+}
+
+__global__ void k_step_advance(int64_t* i, int64_t* t) {
+  *i += 1;
+  *t += 1;
+}
+
+}  // namespace edpc

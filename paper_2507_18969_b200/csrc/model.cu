@@ -1,0 +1,913 @@
+// EDPC context: device-resident model, lane matrix, coders and the per-step
+// schedule (predict -> quantize -> code -> backward -> Adam) behind the C ABI.
+//
+// Reference mapping: EdpcModel (pkg/src/edpc/model.py:184-300) and the
+// compress/decompress loops (pipeline.py:109-298).  Layout, roofline and the
+// determinism rules are in DESIGN.md.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "gemm_simt.cuh"
+#include "kernels.cuh"
+#include "tc_gemm.cuh"
+
+namespace edpc {
+
+struct MbrbOffs {
+  int64_t ln_g, ln_b, w0, b0, wstride, out_w, out_b;
+  int H;
+};
+
+// Offsets in the *shared* flat layout = the reference parameters() order with
+// lte.lane_mats taken out (the per-lane FDM lives in its own buffers).
+struct Layout {
+  int T, DE, F, FP, HL, HG, K, B;
+  int64_t emb, down_w, down_b, up_w, up_b, head_w, head_b;
+  MbrbOffs loc, glo;
+  int64_t n_shared, ref_lane_mats, n_ref, fdm;
+
+  void build(const edpc_config& c) {
+    T = c.context_len;
+    DE = c.embed_dim;
+    F = T * DE;
+    FP = F / c.lte_ratio;
+    HL = c.hidden_local;
+    HG = c.hidden_global;
+    K = c.branches;
+    B = c.lanes;
+    fdm = (int64_t)FP * FP;
+    int64_t o = 0;
+    emb = o;
+    o += 256 * (int64_t)DE;
+    auto mbrb = [&](MbrbOffs& m, int H) {
+      m.H = H;
+      m.ln_g = o;
+      o += F;
+      m.ln_b = o;
+      o += F;
+      m.w0 = o;
+      m.b0 = o + (int64_t)F * H;
+      m.wstride = (int64_t)F * H + H;
+      o += K * m.wstride;
+      m.out_w = o;
+      o += (int64_t)H * F;
+      m.out_b = o;
+      o += F;
+    };
+    mbrb(loc, HL);
+    down_w = o;
+    o += (int64_t)F * FP;
+    down_b = o;
+    o += FP;
+    ref_lane_mats = o;  // lane_mats sit here in the reference order
+    up_w = o;
+    o += (int64_t)FP * F;
+    up_b = o;
+    o += F;
+    mbrb(glo, HG);
+    head_w = o;
+    o += (int64_t)F * 256;
+    head_b = o;
+    o += 256;
+    n_shared = o;
+    n_ref = o + (int64_t)B * fdm;
+  }
+};
+
+}  // namespace edpc
+
+using namespace edpc;
+
+struct edpc_ctx {
+  edpc_config cfg;
+  Layout lay;
+  int device = 0;
+  int Bl = 0, lane0 = 0, S = 0, Sl = 0, spl = 0, seg0 = 0;
+  int64_t n = 0, L = 0;
+  int g_first = 0, g_count = 0;  // local lane groups
+  bool use_tc = false;
+  cudaStream_t st = nullptr, st_enc = nullptr;
+  cudaEvent_t ev = nullptr;
+  AdamConsts adam{};
+
+  std::vector<void*> allocs;
+  float *W = nullptr, *M = nullptr, *V = nullptr, *Gp = nullptr;
+  float *U = nullptr, *Um = nullptr, *Uv = nullptr;
+  uint8_t* mat = nullptr;
+  uint8_t* scratch = nullptr;  // [Bl][T+1] for the predict/train_step seam
+  int64_t *d_i = nullptr, *d_t = nullptr;
+  // activations
+  float *x_emb, *l_xhat, *l_rstd, *l_x0, *l_H, *l_ff, *x_local;
+  float *down, *mixed, *x_lte;
+  float *g_xhat, *g_rstd, *g_x0, *g_H, *g_ff, *x_global;
+  float *logits, *probs, *nll;
+  // backward temporaries
+  float *gl, *gA, *gB, *GH, *gx0, *gmix, *gdown, *emb_sub;
+  int *chunk_tab = nullptr, *grp_chunks = nullptr;
+  int n_chunks = 0;
+  // coder
+  uint32_t* intervals = nullptr;
+  uint16_t* cdf16 = nullptr;
+  int64_t *enc_state = nullptr, *dec_state = nullptr;
+  uint32_t* enc_words = nullptr;
+  int64_t enc_cap_words = 0;
+  uint8_t* payload = nullptr;
+  int64_t *pay_off = nullptr, *bit_len = nullptr;
+  int* dec_err = nullptr;
+  // host bookkeeping
+  int64_t enc_upto = 0;  // intervals columns [0, enc_upto) handed to the encoder
+  bool finished = false, have_input = false, have_payload = false, have_cache = false;
+  int64_t version = 0;   // model updates done (seam)
+  int64_t seam_t = 0;
+
+  ~edpc_ctx() {
+    if (st) cudaStreamSynchronize(st);
+    if (st_enc) cudaStreamSynchronize(st_enc);
+    for (void* p : allocs) cudaFree(p);
+    if (ev) cudaEventDestroy(ev);
+    if (st) cudaStreamDestroy(st);
+    if (st_enc) cudaStreamDestroy(st_enc);
+  }
+
+  template <typename T>
+  int alloc(T** p, int64_t count) {
+    size_t bytes = (size_t)std::max<int64_t>(count, 1) * sizeof(T);
+    bytes = (bytes + 255) & ~(size_t)255;
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, bytes);
+    if (e != cudaSuccess) {
+      set_error("cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+      return EDPC_ERR_NOMEM;
+    }
+    allocs.push_back(q);
+    *p = reinterpret_cast<T*>(q);
+    return EDPC_OK;
+  }
+
+  StepIdx si() const { return StepIdx{d_i, d_t}; }
+  ByteCols lanes_src() const { return ByteCols{mat, L}; }
+  ByteCols seam_src() const { return ByteCols{scratch, (int64_t)lay.T + 1}; }
+};
+
+namespace edpc {
+
+static int check_cfg(const edpc_config* c) {
+  EDPC_CHECK_ARG(c, "null config");
+  EDPC_CHECK_ARG(c->context_len >= 1, "context_len must be >= 1");
+  EDPC_CHECK_ARG(c->embed_dim >= 1, "embed_dim must be >= 1");
+  EDPC_CHECK_ARG(c->branches >= 1, "branches must be >= 1");
+  EDPC_CHECK_ARG(c->lanes >= 1, "lanes must be >= 1");
+  EDPC_CHECK_ARG(c->hidden_local >= 1 && c->hidden_global >= 1, "hidden dims must be >= 1");
+  int64_t f = (int64_t)c->context_len * c->embed_dim;
+  EDPC_CHECK_ARG(c->lte_ratio >= 1 && f % c->lte_ratio == 0,
+                 "lte_ratio must divide context_len * embed_dim");
+  EDPC_CHECK_ARG(c->context_len <= 4096, "context_len > 4096 unsupported");
+  return EDPC_OK;
+}
+
+// ------------------------------------------------------------ GEMM dispatch
+
+// out[Bl][N] = A[Bl][Kd] . W[Kd][N] (+ bias) over nzb batches (weights at
+// w + z*sW, bias at bias + z*sW, out at out + z*sOut)
+static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, const float* w,
+                              int N, int nzb, int64_t sW, float* out, int64_t sOut,
+                              const float* bias, const float* resid, int M) {
+  GemmShape g{};
+  g.M = M;
+  g.N = N;
+  g.K = Kd;
+  g.A = A;
+  g.lda = lda;
+  g.B = w;
+  g.ldb = N;
+  g.sB = sW;
+  g.nzb = nzb;
+  g.nsum = 1;
+  if (c->use_tc && tc_supported(M, N, Kd)) {
+    if (resid) return tc_linear_fwd(A, lda, w, N, Kd, M, bias, resid, out, nzb, sW, sOut, c->st);
+    return tc_linear_fwd(A, lda, w, N, Kd, M, bias, nullptr, out, nzb, sW, sOut, c->st);
+  }
+  if (resid) return gemm_simt<false, false>(g, EpiBiasResid{out, N, bias, resid, N}, c->st);
+  return gemm_simt<false, false>(g, EpiBias{out, N, sOut, bias, sW}, c->st);
+}
+
+// weight-gradient partials: Gp[g][off + z*sOff + m*N + n] = sum over group
+// g's lanes of X[b][m] * G[z][b][n]
+static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, int N, int nzb,
+                         int64_t sG, int64_t off, int64_t sOff) {
+  GemmShape g{};
+  g.M = Mw;
+  g.N = N;
+  g.K = c->Bl;
+  g.A = X;
+  g.lda = Mw;
+  g.B = G;
+  g.ldb = N;
+  g.sB = sG;
+  g.nzb = nzb;
+  g.nsum = 1;
+  g.ngroups = c->g_count;
+  g.g0 = c->g_first;
+  g.B_global = c->lay.B;
+  g.lane0 = c->lane0;
+  EpiPartial e{c->Gp, c->lay.n_shared, off, sOff, N, c->g_first};
+  return gemm_simt<true, false>(g, e, c->st);
+}
+
+// bias-gradient partials (column sums per lane group)
+static cudaError_t colsum(edpc_ctx* c, const float* src, int N, int nz, int64_t sz,
+                          const float* mul, int64_t off, int64_t sOff) {
+  if (c->g_count == 0) return cudaSuccess;
+  dim3 grid((unsigned)cdiv(N, 256), (unsigned)nz, (unsigned)c->g_count);
+  k_colsum_groups<<<grid, 256, 0, c->st>>>(src, N, sz, mul, N, c->Gp, c->lay.n_shared, off, sOff,
+                                           c->g_first, c->lay.B, c->lane0);
+  return cudaGetLastError();
+}
+
+// dgrad: out[Bl][N] = sum_s G_s[Bl][Kd] . W_s^T where W_s is [N][Kd] row-major
+template <class Epi>
+static cudaError_t dgrad(edpc_ctx* c, const float* G, int Kd, int nsum, int64_t sG_sum,
+                         const float* w, int64_t sW_sum, int N, const Epi& epi) {
+  GemmShape g{};
+  g.M = c->Bl;
+  g.N = N;
+  g.K = Kd;
+  g.A = G;
+  g.lda = Kd;
+  g.sA_sum = sG_sum;
+  g.B = w;
+  g.ldb = Kd;
+  g.sB_sum = sW_sum;
+  g.nzb = 1;
+  g.nsum = nsum;
+  return gemm_simt<false, true>(g, epi, c->st);
+}
+
+#define CK(expr)                                                        \
+  do {                                                                  \
+    cudaError_t _e = (expr);                                            \
+    if (_e != cudaSuccess) {                                            \
+      set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));    \
+      return EDPC_ERR_CUDA;                                             \
+    }                                                                   \
+  } while (0)
+
+// --------------------------------------------------------------- forward
+
+struct MbrbBufs {
+  float *x, *xhat, *rstd, *x0, *H, *ff, *out;
+};
+
+static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool gather,
+                        ByteCols src) {
+  const Layout& L = c->lay;
+  const int Bl = c->Bl, F = L.F, H = o.H;
+  dim3 g8((unsigned)cdiv(Bl, 8));
+  if (gather)
+    k_embed_ln<true><<<g8, 256, 0, c->st>>>(src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
+                                            c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0);
+  else
+    k_embed_ln<false><<<g8, 256, 0, c->st>>>(src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
+                                             c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0);
+  CK(cudaGetLastError());
+  const int64_t plane = (int64_t)Bl * H;
+  CK(fwd_linear(c, b.x0, F, F, c->W + o.w0, H, L.K, o.wstride, b.H, plane, c->W + o.b0, nullptr,
+                Bl));
+  k_mbrb_act<<<(unsigned)cdiv(plane, 256), 256, 0, c->st>>>(b.H, L.K, plane, b.ff);
+  CK(cudaGetLastError());
+  CK(fwd_linear(c, b.ff, H, H, c->W + o.out_w, F, 1, 0, b.out, 0, c->W + o.out_b, b.x, Bl));
+  return EDPC_OK;
+}
+
+static int forward(edpc_ctx* c, ByteCols src) {
+  const Layout& L = c->lay;
+  const int Bl = c->Bl;
+  MbrbBufs lb{c->x_emb, c->l_xhat, c->l_rstd, c->l_x0, c->l_H, c->l_ff, c->x_local};
+  EDPC_TRY(mbrb_forward(c, L.loc, lb, true, src));
+  CK(fwd_linear(c, c->x_local, L.F, L.F, c->W + L.down_w, L.FP, 1, 0, c->down, 0,
+                c->W + L.down_b, nullptr, Bl));
+  k_fdm_fwd<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(c->down, c->U, c->mixed, L.FP, Bl);
+  CK(cudaGetLastError());
+  CK(fwd_linear(c, c->mixed, L.FP, L.FP, c->W + L.up_w, L.F, 1, 0, c->x_lte, 0, c->W + L.up_b,
+                nullptr, Bl));
+  MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
+  EDPC_TRY(mbrb_forward(c, L.glo, gb, false, src));
+  CK(fwd_linear(c, c->x_global, L.F, L.F, c->W + L.head_w, 256, 1, 0, c->logits, 0,
+                c->W + L.head_b, nullptr, Bl));
+  return EDPC_OK;
+}
+
+static int softmax_quant(edpc_ctx* c, int mode, ByteCols src) {
+  dim3 g8((unsigned)cdiv(c->Bl, 8));
+  if (mode == kProbsOnly)
+    k_softmax_quant<kProbsOnly><<<g8, 256, 0, c->st>>>(c->logits, c->probs, c->Bl, src, c->si(),
+                                                       c->intervals, c->cdf16);
+  else if (mode == kEncode)
+    k_softmax_quant<kEncode><<<g8, 256, 0, c->st>>>(c->logits, c->probs, c->Bl, src, c->si(),
+                                                    c->intervals, c->cdf16);
+  else
+    k_softmax_quant<kDecode><<<g8, 256, 0, c->st>>>(c->logits, c->probs, c->Bl, src, c->si(),
+                                                    c->intervals, c->cdf16);
+  CK(cudaGetLastError());
+  return EDPC_OK;
+}
+
+// -------------------------------------------------------------- backward
+
+// g_up: gradient w.r.t. the block output [Bl][F]; writes the gradient w.r.t.
+// the block input into g_in
+static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, const float* g_up,
+                         float* g_in) {
+  const Layout& L = c->lay;
+  const int Bl = c->Bl, F = L.F, H = o.H, K = L.K;
+  const int64_t plane = (int64_t)Bl * H;
+  // g_ff = g_up . out_w^T, epilogue -> GH[z] (product rule + GeLU')
+  CK(dgrad(c, g_up, F, 1, 0, c->W + o.out_w, 0, H, EpiBwdAct{b.H, c->GH, K, plane, H}));
+  // out_w / out_b gradients
+  CK(wgrad(c, b.ff, H, g_up, F, 1, 0, o.out_w, 0));
+  CK(colsum(c, g_up, F, 1, 0, nullptr, o.out_b, 0));
+  // branch weights / biases
+  CK(wgrad(c, b.x0, F, c->GH, H, K, plane, o.w0, o.wstride));
+  CK(colsum(c, c->GH, H, K, plane, nullptr, o.b0, o.wstride));
+  // g_x0 = sum_z GH[z] . W_z^T
+  CK(dgrad(c, c->GH, H, K, plane, c->W + o.w0, o.wstride, F, EpiStore{c->gx0, F}));
+  // LN gain / bias gradients, then LN backward + residual
+  CK(colsum(c, c->gx0, F, 1, 0, b.xhat, o.ln_g, 0));
+  CK(colsum(c, c->gx0, F, 1, 0, nullptr, o.ln_b, 0));
+  k_ln_bwd<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(c->gx0, b.xhat, b.rstd, c->W + o.ln_g, g_up,
+                                                     g_in, F, Bl);
+  CK(cudaGetLastError());
+  return EDPC_OK;
+}
+
+static int backward(edpc_ctx* c, ByteCols src, float* nll) {
+  const Layout& L = c->lay;
+  const int Bl = c->Bl, F = L.F, FP = L.FP;
+  k_dlogits<<<(unsigned)cdiv((int64_t)Bl * 256, 256), 256, 0, c->st>>>(
+      c->probs, src, c->si(), Bl, (float)L.B, c->gl, nll);
+  CK(cudaGetLastError());
+  // head
+  CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0));
+  CK(colsum(c, c->gl, 256, 1, 0, nullptr, L.head_b, 0));
+  CK(dgrad(c, c->gl, 256, 1, 0, c->W + L.head_w, 0, F, EpiStore{c->gA, F}));
+  // global MBRB: gA -> gB
+  MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
+  EDPC_TRY(mbrb_backward(c, L.glo, gb, c->gA, c->gB));
+  // LTE up
+  CK(wgrad(c, c->mixed, FP, c->gB, F, 1, 0, L.up_w, 0));
+  CK(colsum(c, c->gB, F, 1, 0, nullptr, L.up_b, 0));
+  CK(dgrad(c, c->gB, F, 1, 0, c->W + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
+  // per-lane FDM: g_down with the old U, then U's Adam step (fused)
+  k_fdm_bwd_adam<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(
+      c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, FP, Bl, c->si(), c->adam, c->cfg.beta1,
+      c->cfg.beta2);
+  CK(cudaGetLastError());
+  // LTE down
+  CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0));
+  CK(colsum(c, c->gdown, FP, 1, 0, nullptr, L.down_b, 0));
+  CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore{c->gA, F}));
+  // local MBRB: gA -> gB (gradient w.r.t. the embedded context)
+  MbrbBufs lb{c->x_emb, c->l_xhat, c->l_rstd, c->l_x0, c->l_H, c->l_ff, c->x_local};
+  EDPC_TRY(mbrb_backward(c, L.loc, lb, c->gA, c->gB));
+  // embedding scatter-add as per-group partials
+  if (c->n_chunks > 0) {
+    k_embed_grad_chunks<<<(unsigned)c->n_chunks, 256, 0, c->st>>>(src, c->si(), L.T, L.DE, F,
+                                                                  c->gB, c->chunk_tab, c->emb_sub);
+    CK(cudaGetLastError());
+    dim3 gr((unsigned)cdiv(256 * L.DE, 256), (unsigned)c->g_count);
+    k_embed_grad_reduce<<<gr, 256, 0, c->st>>>(c->emb_sub, c->grp_chunks, L.DE, c->Gp,
+                                               L.n_shared, L.emb);
+    CK(cudaGetLastError());
+  }
+  return EDPC_OK;
+}
+
+static int adam_shared(edpc_ctx* c) {
+  int blocks = (int)std::min<int64_t>(cdiv(c->lay.n_shared, 256), 148 * 8);
+  k_adam_shared<<<blocks, 256, 0, c->st>>>(c->W, c->M, c->V, c->Gp, c->lay.n_shared, c->si(),
+                                           c->adam, c->cfg.beta1, c->cfg.beta2);
+  CK(cudaGetLastError());
+  return EDPC_OK;
+}
+
+// One model step at lane column i (already in d_i / d_t).
+static int model_step(edpc_ctx* c, int mode) {
+  ByteCols src = c->lanes_src();
+  EDPC_TRY(forward(c, src));
+  EDPC_TRY(softmax_quant(c, mode, src));
+  if (mode == kDecode) {
+    k_decode_column<<<(unsigned)cdiv(c->Sl, 4), 128, 0, c->st>>>(
+        c->mat, c->L, c->si(), c->spl, c->Sl, c->cdf16, false, c->dec_state, c->payload,
+        c->pay_off, c->bit_len, c->dec_err);
+    CK(cudaGetLastError());
+  }
+  EDPC_TRY(backward(c, src, nullptr));
+  EDPC_TRY(adam_shared(c));
+  k_step_advance<<<1, 1, 0, c->st>>>(c->d_i, c->d_t);
+  CK(cudaGetLastError());
+  return EDPC_OK;
+}
+
+static int set_step(edpc_ctx* c, int64_t i, int64_t t) {
+  int64_t h[2] = {i, t};
+  CK(cudaMemcpyAsync(c->d_i, &h[0], 8, cudaMemcpyHostToDevice, c->st));
+  CK(cudaMemcpyAsync(c->d_t, &h[1], 8, cudaMemcpyHostToDevice, c->st));
+  return EDPC_OK;
+}
+
+static int launch_encoder(edpc_ctx* c, int64_t upto) {
+  if (upto <= c->enc_upto) return EDPC_OK;
+  CK(cudaEventRecord(c->ev, c->st));
+  CK(cudaStreamWaitEvent(c->st_enc, c->ev, 0));
+  k_encode_columns<<<(unsigned)cdiv(c->Sl, 64), 64, 0, c->st_enc>>>(
+      c->intervals, c->Bl, c->spl, c->Sl, c->enc_upto, upto, c->enc_state, c->enc_words,
+      c->enc_cap_words);
+  CK(cudaGetLastError());
+  c->enc_upto = upto;
+  return EDPC_OK;
+}
+
+}  // namespace edpc
+
+// ================================================================== C ABI
+
+extern "C" {
+
+int edpc_has_tcgen05(void) { return tc_compiled() ? 1 : 0; }
+
+int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_len,
+                    int32_t device, int32_t lane_begin, int32_t lane_count, edpc_ctx** out) {
+  EDPC_CHECK_ARG(out, "null out");
+  *out = nullptr;
+  EDPC_TRY(check_cfg(cfg));
+  EDPC_CHECK_ARG(segments >= 1 && cfg->lanes % segments == 0,
+                 "segments must divide lanes");
+  EDPC_CHECK_ARG(original_len >= 0, "negative length");
+  EDPC_CHECK_ARG(lane_begin >= 0 && lane_count >= 1 && lane_begin + lane_count <= cfg->lanes,
+                 "bad lane range");
+  const int spl = cfg->lanes / segments;
+  EDPC_CHECK_ARG(lane_begin % spl == 0 && lane_count % spl == 0,
+                 "lane range must cover whole segments");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    set_error("no CUDA device available (the B200 path has no CPU fallback)");
+    return EDPC_ERR_CUDA;
+  }
+  EDPC_CHECK_ARG(device >= 0 && device < ndev, "device ordinal out of range");
+  EDPC_CUDA_TRY(cudaSetDevice(device));
+
+  edpc_ctx* c = new edpc_ctx();
+  c->cfg = *cfg;
+  c->lay.build(*cfg);
+  c->device = device;
+  c->Bl = lane_count;
+  c->lane0 = lane_begin;
+  c->S = segments;
+  c->spl = spl;
+  c->Sl = lane_count / spl;
+  c->seg0 = lane_begin / spl;
+  c->n = original_len;
+  c->L = original_len ? (original_len + cfg->lanes - 1) / cfg->lanes : 0;
+  // local lane groups: group g belongs to the device holding its first lane
+  // (multi-device callers split B on group boundaries, see dist.py)
+  c->g_first = -1;
+  c->g_count = 0;
+  for (int g = 0; g < kNumGroups; ++g) {
+    int b0 = group_begin(g, cfg->lanes);
+    if (b0 >= lane_begin && b0 < lane_begin + lane_count) {
+      if (c->g_first < 0) c->g_first = g;
+      c->g_count++;
+    }
+  }
+  if (c->g_first < 0) c->g_first = 0;
+  {
+    double b1 = cfg->beta1, b2 = cfg->beta2;
+    c->adam.lr = (float)cfg->lr;
+    c->adam.b1 = (float)b1;
+    c->adam.b2 = (float)b2;
+    c->adam.k1 = (float)(1.0 - b1);
+    c->adam.k2 = (float)(1.0 - b2);
+    c->adam.eps = (float)cfg->adam_eps;
+  }
+  c->use_tc = tc_compiled() && tc_enabled_env();
+
+  auto fail = [&](int code) {
+    delete c;
+    return code;
+  };
+  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->st_enc, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming) != cudaSuccess) {
+    set_error("stream/event creation failed");
+    return fail(EDPC_ERR_CUDA);
+  }
+  const Layout& L = c->lay;
+  const int Bl = c->Bl;
+  const int64_t F = L.F, FP = L.FP;
+  const int Hm = std::max(L.HL, L.HG);
+#define A_(p, n)                        \
+  do {                                  \
+    int _r = c->alloc(&(p), (n));       \
+    if (_r != EDPC_OK) return fail(_r); \
+  } while (0)
+  A_(c->W, L.n_shared);
+  A_(c->M, L.n_shared);
+  A_(c->V, L.n_shared);
+  A_(c->Gp, (int64_t)kNumGroups * L.n_shared);
+  A_(c->U, (int64_t)Bl * L.fdm);
+  A_(c->Um, (int64_t)Bl * L.fdm);
+  A_(c->Uv, (int64_t)Bl * L.fdm);
+  A_(c->mat, (int64_t)Bl * std::max<int64_t>(c->L, 1));
+  A_(c->scratch, (int64_t)Bl * (L.T + 1));
+  A_(c->d_i, 2);
+  A_(c->d_t, 2);
+  A_(c->x_emb, Bl * F);
+  A_(c->l_xhat, Bl * F);
+  A_(c->l_rstd, Bl);
+  A_(c->l_x0, Bl * F);
+  A_(c->l_H, (int64_t)L.K * Bl * L.HL);
+  A_(c->l_ff, (int64_t)Bl * L.HL);
+  A_(c->x_local, Bl * F);
+  A_(c->down, Bl * FP);
+  A_(c->mixed, Bl * FP);
+  A_(c->x_lte, Bl * F);
+  A_(c->g_xhat, Bl * F);
+  A_(c->g_rstd, Bl);
+  A_(c->g_x0, Bl * F);
+  A_(c->g_H, (int64_t)L.K * Bl * L.HG);
+  A_(c->g_ff, (int64_t)Bl * L.HG);
+  A_(c->x_global, Bl * F);
+  A_(c->logits, (int64_t)Bl * 256);
+  A_(c->probs, (int64_t)Bl * 256);
+  A_(c->nll, Bl);
+  A_(c->gl, (int64_t)Bl * 256);
+  A_(c->gA, Bl * F);
+  A_(c->gB, Bl * F);
+  A_(c->GH, (int64_t)L.K * Bl * Hm);
+  A_(c->gx0, Bl * F);
+  A_(c->gmix, Bl * FP);
+  A_(c->gdown, Bl * FP);
+  // embedding-gradient chunks: <= 64 lanes (and <= 4096 context bytes) each,
+  // never straddling a lane group
+  {
+    const int chunk = std::max(1, std::min(64, 4096 / L.T));
+    std::vector<int> tab, grp;
+    int k = 0;
+    for (int g = c->g_first; g < c->g_first + c->g_count; ++g) {
+      int b0 = group_begin(g, L.B) - c->lane0, b1 = group_begin(g + 1, L.B) - c->lane0;
+      int k0 = k;
+      for (int b = b0; b < b1; b += chunk) {
+        tab.push_back(g);
+        tab.push_back(b);
+        tab.push_back(std::min(b + chunk, b1));
+        ++k;
+      }
+      grp.push_back(g);
+      grp.push_back(k0);
+      grp.push_back(k);
+    }
+    c->n_chunks = k;
+    A_(c->chunk_tab, (int64_t)std::max<size_t>(tab.size(), 3));
+    A_(c->grp_chunks, (int64_t)std::max<size_t>(grp.size(), 3));
+    A_(c->emb_sub, (int64_t)std::max(k, 1) * 256 * L.DE);
+    if (!tab.empty() &&
+        cudaMemcpy(c->chunk_tab, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(EDPC_ERR_CUDA);
+    if (!grp.empty() &&
+        cudaMemcpy(c->grp_chunks, grp.data(), grp.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(EDPC_ERR_CUDA);
+  }
+  // coder buffers: 18 bits per symbol worst case (coder.py:269-270) + slack
+  A_(c->intervals, std::max<int64_t>(c->L, 1) * Bl);
+  A_(c->cdf16, (int64_t)Bl * 256);
+  A_(c->enc_state, 4 * (int64_t)c->Sl);
+  A_(c->dec_state, 4 * (int64_t)c->Sl);
+  c->enc_cap_words = (18 * (int64_t)c->spl * std::max<int64_t>(c->L, 1) + 128) / 32 + 2;
+  A_(c->enc_words, c->enc_cap_words * c->Sl);
+  A_(c->pay_off, c->Sl + 1);
+  A_(c->bit_len, c->Sl);
+  A_(c->dec_err, c->Sl);
+#undef A_
+  // zero state: Adam moments, encoders (low=0, high=2^32-1), error flags
+  cudaMemsetAsync(c->M, 0, L.n_shared * 4, c->st);
+  cudaMemsetAsync(c->V, 0, L.n_shared * 4, c->st);
+  cudaMemsetAsync(c->Um, 0, (int64_t)Bl * L.fdm * 4, c->st);
+  cudaMemsetAsync(c->Uv, 0, (int64_t)Bl * L.fdm * 4, c->st);
+  cudaMemsetAsync(c->Gp, 0, (int64_t)kNumGroups * L.n_shared * 4, c->st);
+  cudaMemsetAsync(c->enc_words, 0, c->enc_cap_words * c->Sl * 4, c->st);
+  cudaMemsetAsync(c->dec_err, 0, c->Sl * 4, c->st);
+  {
+    std::vector<int64_t> es(4 * (size_t)c->Sl);
+    for (int s = 0; s < c->Sl; ++s) {
+      es[4 * s + 0] = 0;
+      es[4 * s + 1] = (int64_t)kMask32;
+      es[4 * s + 2] = 0;
+      es[4 * s + 3] = 0;
+    }
+    cudaMemcpy(c->enc_state, es.data(), es.size() * 8, cudaMemcpyHostToDevice);
+  }
+  if (cudaStreamSynchronize(c->st) != cudaSuccess) {
+    set_error("context init failed");
+    return fail(EDPC_ERR_CUDA);
+  }
+  *out = c;
+  return EDPC_OK;
+}
+
+int edpc_ctx_destroy(edpc_ctx* ctx) {
+  if (ctx) {
+    cudaSetDevice(ctx->device);
+    delete ctx;
+  }
+  return EDPC_OK;
+}
+
+int edpc_ctx_info(edpc_ctx* c, int64_t* lane_len, int64_t* n_params, int64_t* n_shared) {
+  EDPC_CHECK_ARG(c, "null ctx");
+  if (lane_len) *lane_len = c->L;
+  if (n_params) *n_params = c->lay.n_ref;
+  if (n_shared) *n_shared = c->lay.n_shared;
+  return EDPC_OK;
+}
+
+int edpc_load_params(edpc_ctx* c, const float* params, int64_t count) {
+  EDPC_CHECK_ARG(c && params, "null argument");
+  EDPC_CHECK_ARG(count == c->lay.n_ref, "parameter count mismatch");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  const Layout& L = c->lay;
+  const int64_t fdm_all = (int64_t)L.B * L.fdm;
+  // shared = ref[0, lane_mats) ++ ref[lane_mats + B*fdm, end)
+  EDPC_CUDA_TRY(cudaMemcpy(c->W, params, L.ref_lane_mats * 4, cudaMemcpyHostToDevice));
+  EDPC_CUDA_TRY(cudaMemcpy(c->W + L.ref_lane_mats, params + L.ref_lane_mats + fdm_all,
+                           (L.n_shared - L.ref_lane_mats) * 4, cudaMemcpyHostToDevice));
+  EDPC_CUDA_TRY(cudaMemcpy(c->U, params + L.ref_lane_mats + (int64_t)c->lane0 * L.fdm,
+                           (int64_t)c->Bl * L.fdm * 4, cudaMemcpyHostToDevice));
+  return EDPC_OK;
+}
+
+int edpc_get_params(edpc_ctx* c, float* params, int64_t count) {
+  EDPC_CHECK_ARG(c && params, "null argument");
+  EDPC_CHECK_ARG(count == c->lay.n_ref, "parameter count mismatch");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  const Layout& L = c->lay;
+  const int64_t fdm_all = (int64_t)L.B * L.fdm;
+  EDPC_CUDA_TRY(cudaMemcpy(params, c->W, L.ref_lane_mats * 4, cudaMemcpyDeviceToHost));
+  EDPC_CUDA_TRY(cudaMemcpy(params + L.ref_lane_mats + fdm_all, c->W + L.ref_lane_mats,
+                           (L.n_shared - L.ref_lane_mats) * 4, cudaMemcpyDeviceToHost));
+  EDPC_CUDA_TRY(cudaMemcpy(params + L.ref_lane_mats + (int64_t)c->lane0 * L.fdm, c->U,
+                           (int64_t)c->Bl * L.fdm * 4, cudaMemcpyDeviceToHost));
+  return EDPC_OK;
+}
+
+int edpc_set_input(edpc_ctx* c, const uint8_t* data, int64_t n, int on_device) {
+  EDPC_CHECK_ARG(c, "null ctx");
+  EDPC_CHECK_ARG(n == c->n, "input length differs from the context's original_len");
+  EDPC_CHECK_ARG(n == 0 || data, "null data");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  // local lanes [lane0, lane0+Bl) = stream bytes [lane0*L, (lane0+Bl)*L) (zero padded)
+  const int64_t start = (int64_t)c->lane0 * c->L;
+  const int64_t want = (int64_t)c->Bl * c->L;
+  const int64_t have = std::max<int64_t>(0, std::min<int64_t>(want, n - start));
+  if (want > have)
+    EDPC_CUDA_TRY(cudaMemsetAsync(c->mat + have, 0, want - have, c->st));
+  if (have > 0)
+    EDPC_CUDA_TRY(cudaMemcpyAsync(c->mat, data + start, have,
+                                  on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                  c->st));
+  c->have_input = true;
+  return EDPC_OK;
+}
+
+int edpc_compress_steps(edpc_ctx* c, int64_t i0, int64_t i1) {
+  EDPC_CHECK_ARG(c, "null ctx");
+  EDPC_CHECK_ARG(c->have_input, "set_input first");
+  if (c->finished) {
+    set_error("encoder already finished");
+    return EDPC_ERR_STATE;
+  }
+  EDPC_CHECK_ARG(0 <= i0 && i0 <= i1 && i1 <= c->L, "bad column range");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  const int T = c->lay.T;
+  const int64_t boot = std::min<int64_t>(T, c->L);
+  if (i0 < boot) {
+    const int64_t a = i0, e = std::min(i1, boot);
+    k_boot_intervals<<<(unsigned)cdiv((e) * (int64_t)c->Bl, 256), 256, 0, c->st>>>(
+        c->mat, c->L, c->Bl, e, c->intervals);
+    EDPC_CUDA_TRY(cudaGetLastError());
+    (void)a;
+  }
+  const int64_t s0 = std::max<int64_t>(i0, T);
+  if (s0 < i1) {
+    EDPC_TRY(set_step(c, s0, s0 - T + 1));
+    for (int64_t i = s0; i < i1; ++i) EDPC_TRY(model_step(c, kEncode));
+  }
+  // DPCA: hand the finished columns to the encoder stream
+  EDPC_TRY(launch_encoder(c, i1));
+  return EDPC_OK;
+}
+
+int edpc_compress_finish(edpc_ctx* c, int64_t* bit_lengths, int64_t* total_bytes) {
+  EDPC_CHECK_ARG(c && bit_lengths, "null argument");
+  if (c->finished) {
+    set_error("encoder already finished");
+    return EDPC_ERR_STATE;
+  }
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  EDPC_TRY(launch_encoder(c, c->L));
+  k_encode_finish_all<<<(unsigned)cdiv(c->Sl, 64), 64, 0, c->st_enc>>>(
+      c->enc_state, c->enc_words, c->enc_cap_words, c->Sl);
+  EDPC_CUDA_TRY(cudaGetLastError());
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st_enc));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  std::vector<int64_t> es(4 * (size_t)c->Sl);
+  EDPC_CUDA_TRY(cudaMemcpy(es.data(), c->enc_state, es.size() * 8, cudaMemcpyDeviceToHost));
+  int64_t tot = 0;
+  for (int s = 0; s < c->Sl; ++s) {
+    bit_lengths[s] = es[4 * s + 3];
+    tot += (es[4 * s + 3] + 7) / 8;
+  }
+  if (total_bytes) *total_bytes = tot;
+  c->finished = true;
+  return EDPC_OK;
+}
+
+int edpc_get_payloads(edpc_ctx* c, uint8_t* out, int64_t cap) {
+  EDPC_CHECK_ARG(c && out, "null argument");
+  if (!c->finished) {
+    set_error("compress_finish first");
+    return EDPC_ERR_STATE;
+  }
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  std::vector<int64_t> es(4 * (size_t)c->Sl);
+  EDPC_CUDA_TRY(cudaMemcpy(es.data(), c->enc_state, es.size() * 8, cudaMemcpyDeviceToHost));
+  int64_t pos = 0;
+  for (int s = 0; s < c->Sl; ++s) {
+    int64_t nb = (es[4 * s + 3] + 7) / 8;
+    EDPC_CHECK_ARG(pos + nb <= cap, "payload buffer too small");
+    if (nb)
+      EDPC_CUDA_TRY(cudaMemcpy(out + pos, c->enc_words + (int64_t)s * c->enc_cap_words, nb,
+                               cudaMemcpyDeviceToHost));
+    pos += nb;
+  }
+  return EDPC_OK;
+}
+
+int edpc_set_payloads(edpc_ctx* c, const uint8_t* data, const int64_t* bit_lengths) {
+  EDPC_CHECK_ARG(c && bit_lengths, "null argument");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  std::vector<int64_t> off(c->Sl + 1, 0);
+  for (int s = 0; s < c->Sl; ++s) {
+    EDPC_CHECK_ARG(bit_lengths[s] >= 0, "negative bit length");
+    off[s + 1] = off[s] + (bit_lengths[s] + 7) / 8;
+  }
+  const int64_t total = off[c->Sl];
+  int r = c->alloc(&c->payload, total + 64);
+  if (r != EDPC_OK) return r;
+  EDPC_CUDA_TRY(cudaMemset(c->payload, 0, total + 64));
+  if (total) {
+    EDPC_CHECK_ARG(data, "null payload");
+    EDPC_CUDA_TRY(cudaMemcpy(c->payload, data, total, cudaMemcpyHostToDevice));
+  }
+  EDPC_CUDA_TRY(cudaMemcpy(c->pay_off, off.data(), (c->Sl + 1) * 8, cudaMemcpyHostToDevice));
+  EDPC_CUDA_TRY(cudaMemcpy(c->bit_len, bit_lengths, c->Sl * 8, cudaMemcpyHostToDevice));
+  k_decoder_init_all<<<(unsigned)cdiv(c->Sl, 64), 64, 0, c->st>>>(c->dec_state, c->payload,
+                                                                 c->pay_off, c->bit_len, c->Sl);
+  EDPC_CUDA_TRY(cudaGetLastError());
+  EDPC_CUDA_TRY(cudaMemsetAsync(c->mat, 0, (int64_t)c->Bl * std::max<int64_t>(c->L, 1), c->st));
+  c->have_payload = true;
+  return EDPC_OK;
+}
+
+int edpc_decompress_steps(edpc_ctx* c, int64_t i0, int64_t i1) {
+  EDPC_CHECK_ARG(c, "null ctx");
+  EDPC_CHECK_ARG(c->have_payload, "set_payloads first");
+  EDPC_CHECK_ARG(0 <= i0 && i0 <= i1 && i1 <= c->L, "bad column range");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  const int T = c->lay.T;
+  const int64_t boot = std::min<int64_t>(T, c->L);
+  for (int64_t i = i0; i < std::min(i1, boot); ++i) {
+    EDPC_TRY(set_step(c, i, 0));
+    k_decode_column<<<(unsigned)cdiv(c->Sl, 4), 128, 0, c->st>>>(
+        c->mat, c->L, c->si(), c->spl, c->Sl, c->cdf16, true, c->dec_state, c->payload,
+        c->pay_off, c->bit_len, c->dec_err);
+    EDPC_CUDA_TRY(cudaGetLastError());
+  }
+  const int64_t s0 = std::max<int64_t>(i0, T);
+  if (s0 < i1) {
+    EDPC_TRY(set_step(c, s0, s0 - T + 1));
+    for (int64_t i = s0; i < i1; ++i) EDPC_TRY(model_step(c, kDecode));
+  }
+  return EDPC_OK;
+}
+
+int edpc_get_output(edpc_ctx* c, uint8_t* out, int64_t n_local) {
+  EDPC_CHECK_ARG(c && (out || n_local == 0), "null argument");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  std::vector<int> err(c->Sl);
+  EDPC_CUDA_TRY(cudaMemcpy(err.data(), c->dec_err, c->Sl * 4, cudaMemcpyDeviceToHost));
+  for (int s = 0; s < c->Sl; ++s)
+    if (err[s]) {
+      set_error("bitstream exhausted in segment " + std::to_string(c->seg0 + s));
+      return EDPC_ERR_CODER;
+    }
+  EDPC_CHECK_ARG(n_local <= (int64_t)c->Bl * c->L, "output larger than local lanes");
+  if (n_local) EDPC_CUDA_TRY(cudaMemcpy(out, c->mat, n_local, cudaMemcpyDeviceToHost));
+  return EDPC_OK;
+}
+
+int edpc_predict(edpc_ctx* c, const uint8_t* contexts, float* probs) {
+  EDPC_CHECK_ARG(c && contexts, "null argument");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  const int T = c->lay.T;
+  // contexts row b -> scratch[b][0..T)
+  EDPC_CUDA_TRY(cudaMemcpy2DAsync(c->scratch, T + 1, contexts, T, T, c->Bl,
+                                  cudaMemcpyHostToDevice, c->st));
+  EDPC_TRY(set_step(c, T, c->version + 1));
+  EDPC_TRY(forward(c, c->seam_src()));
+  EDPC_TRY(softmax_quant(c, kProbsOnly, c->seam_src()));
+  if (probs)
+    EDPC_CUDA_TRY(cudaMemcpyAsync(probs, c->probs, (size_t)c->Bl * 256 * 4,
+                                  cudaMemcpyDeviceToHost, c->st));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  c->have_cache = true;
+  return EDPC_OK;
+}
+
+int edpc_train_step(edpc_ctx* c, const uint8_t* targets, float* loss) {
+  EDPC_CHECK_ARG(c && targets, "null argument");
+  if (!c->have_cache) {
+    set_error("stale cache: model was updated since this predict");
+    return EDPC_ERR_STATE;
+  }
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  const int T = c->lay.T;
+  EDPC_CUDA_TRY(cudaMemcpy2DAsync(c->scratch + T, T + 1, targets, 1, 1, c->Bl,
+                                  cudaMemcpyHostToDevice, c->st));
+  EDPC_TRY(backward(c, c->seam_src(), c->nll));
+  EDPC_TRY(adam_shared(c));
+  std::vector<float> nll(c->Bl);
+  EDPC_CUDA_TRY(cudaMemcpyAsync(nll.data(), c->nll, c->Bl * 4, cudaMemcpyDeviceToHost, c->st));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  double s = 0;
+  for (float v : nll) s += v;
+  if (loss) *loss = (float)(s / c->lay.B);
+  c->version++;
+  c->have_cache = false;
+  return EDPC_OK;
+}
+
+int edpc_last_probs(edpc_ctx* c, float* probs) {
+  EDPC_CHECK_ARG(c && probs, "null argument");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  EDPC_CUDA_TRY(cudaMemcpy(probs, c->probs, (size_t)c->Bl * 256 * 4, cudaMemcpyDeviceToHost));
+  return EDPC_OK;
+}
+
+int edpc_step_phase(edpc_ctx* c, int64_t i, int32_t phase, int32_t decompress) {
+  EDPC_CHECK_ARG(c, "null ctx");
+  EDPC_CHECK_ARG(i >= c->lay.T && i < c->L, "step index out of range");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  ByteCols src = c->lanes_src();
+  if (phase == 0) {
+    EDPC_TRY(set_step(c, i, i - c->lay.T + 1));
+    EDPC_TRY(forward(c, src));
+    EDPC_TRY(softmax_quant(c, decompress ? kDecode : kEncode, src));
+    if (decompress) {
+      k_decode_column<<<(unsigned)cdiv(c->Sl, 4), 128, 0, c->st>>>(
+          c->mat, c->L, c->si(), c->spl, c->Sl, c->cdf16, false, c->dec_state, c->payload,
+          c->pay_off, c->bit_len, c->dec_err);
+      EDPC_CUDA_TRY(cudaGetLastError());
+    }
+    EDPC_TRY(backward(c, src, nullptr));
+    return EDPC_OK;
+  }
+  EDPC_CHECK_ARG(phase == 1, "phase must be 0 or 1");
+  EDPC_TRY(adam_shared(c));
+  return EDPC_OK;
+}
+
+int edpc_grad_partials(edpc_ctx* c, float** dev_ptr, int64_t* n_shared) {
+  EDPC_CHECK_ARG(c && dev_ptr && n_shared, "null argument");
+  *dev_ptr = c->Gp;
+  *n_shared = c->lay.n_shared;
+  return EDPC_OK;
+}
+
+int edpc_sync(edpc_ctx* c) {
+  EDPC_CHECK_ARG(c, "null ctx");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st_enc));
+  return EDPC_OK;
+}
+
+}  // extern "C"

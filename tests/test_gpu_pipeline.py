@@ -1,0 +1,174 @@
+"""End-to-end compress/decompress on the GPU (the reference pipeline suite,
+pkg/tests/test_pipeline.py, re-pointed at the B200 path) plus cross-checks
+against the CPU oracle: coder bit-identity from logged probabilities and the
+compression-ratio bound (|ratio_gpu / ratio_oracle - 1| <= 0.5%)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import coder as oc
+from oracle import pipeline as op
+from paper_2507_18969_b200 import (ArithmeticEncoder, CoderError, ContainerError, ModelConfig,
+                                   compress, decompress, quantize_rows, read_container,
+                                   split_lanes, write_container)
+from paper_2507_18969_b200 import synth
+from helpers import DESK, TINY, tiny_cfg
+
+pytestmark = pytest.mark.gpu
+RATIO_TOL = 0.005
+
+
+def roundtrip(data, cfg, segments=4, **kw):
+    blob = write_container(compress(data, cfg, segments, **kw))
+    return decompress(read_container(blob))
+
+
+@pytest.mark.parametrize("data", [b"", b"\x7f", b"abcdef", b"\x00" * 3000, b"\xff" * 3000,
+                                  bytes(range(256)) * 12,
+                                  b"the quick brown fox jumps over the lazy dog. " * 70])
+def test_roundtrips(data):
+    assert roundtrip(data, TINY) == data
+
+
+def test_random_and_precompressed_roundtrip():
+    rng = np.random.default_rng(1)
+    data = rng.integers(0, 256, size=4096, dtype=np.uint8).tobytes()
+    blob = write_container(compress(data, TINY, 4))
+    assert len(blob) >= int(len(data) * 0.99)
+    assert decompress(read_container(blob)) == data
+    assert roundtrip(blob, TINY) == blob
+
+
+def test_random_geometry_roundtrips():
+    rng = np.random.default_rng(3)
+    for trial in range(10):
+        lanes = int(rng.choice([1, 2, 4, 8, 16]))
+        segments = int(rng.choice([s for s in (1, 2, 4, 8, 16) if lanes % s == 0]))
+        n = int(rng.integers(0, 3000))
+        cfg = tiny_cfg(lanes=lanes, seed=int(rng.integers(0, 1 << 32)))
+        data = rng.integers(0, 256, size=n, dtype=np.uint8).tobytes()
+        assert roundtrip(data, cfg, segments) == data, (lanes, segments, n)
+
+
+def test_repeated_byte_compresses_hard():
+    data = b"a" * 65536
+    cfg = tiny_cfg(lanes=16, context_len=8)
+    blob = write_container(compress(data, cfg, 4))
+    assert len(blob) < 2048
+    assert decompress(read_container(blob)) == data
+
+
+def test_geometry_errors():
+    with pytest.raises(ValueError):
+        compress(b"x" * 100, tiny_cfg(lanes=8), segments=3)
+    with pytest.raises(ValueError):
+        compress(b"x" * 100, tiny_cfg(lanes=8), segments=0)
+
+
+def test_output_invariant_to_scheduling_and_deterministic():
+    rng = np.random.default_rng(5)
+    data = (b"schedule invariance probe " * 120) + rng.integers(0, 256, 500, dtype=np.uint8).tobytes()
+    cfg = tiny_cfg(lanes=16)
+    for segments in (1, 2, 8):
+        blobs = {write_container(compress(data, cfg, segments, threads=t, queue_capacity=q,
+                                          serial=s, chunk=ch))
+                 for t, q, s, ch in ((1, 1, True, 512), (2, 4, False, 7), (8, 64, False, 1))}
+        assert len(blobs) == 1
+        assert decompress(read_container(blobs.pop())) == data
+
+
+def test_encoder_decoder_parameter_lockstep():
+    data = b"lockstep parameter trajectories must match exactly. " * 60
+    cfg = tiny_cfg(lanes=8)
+    enc, dec = [], []
+    c = compress(data, cfg, 2, param_probe=lambda i, m: enc.append((i, m.state_checksum())),
+                 probe_every=100)
+    out = decompress(read_container(write_container(c)),
+                     param_probe=lambda i, m: dec.append((i, m.state_checksum())), probe_every=100)
+    assert out == data and len(enc) >= 3 and enc == dec
+
+
+def test_segment_reencode_from_logged_probs_gpu_and_oracle():
+    """coder.py parity: given the logged probabilities, the GPU quantizer+coder
+    AND the C oracle coder both reproduce the container's segment bit-exactly."""
+    data = b"segment independence: re-encode one segment from the log. " * 40
+    cfg = tiny_cfg(lanes=8)
+    segments = 4
+    log = []
+    c = compress(data, cfg, segments, step_hook=lambda i, p, t: log.append((p.copy(), t.copy())))
+    chunk = cfg.lanes // segments
+    split, mat = split_lanes(data, cfg.lanes)
+    boot = min(cfg.context_len, split.lane_len)
+    for s in range(segments):
+        lo, hi = s * chunk, (s + 1) * chunk
+        eg, eo = ArithmeticEncoder(), oc.ArithmeticEncoder()
+        for i in range(boot):
+            eg.encode_rows(oc.uniform_cums(chunk), mat[lo:hi, i])
+            eo.encode_rows(oc.uniform_cums(chunk), mat[lo:hi, i])
+        for probs, tg in log:
+            _, cg = quantize_rows(probs[lo:hi])
+            _, co = oc.quantize_rows(probs[lo:hi])
+            assert np.array_equal(cg, co)
+            eg.encode_rows(cg, tg[lo:hi])
+            eo.encode_rows(co, tg[lo:hi])
+        assert eg.finish() == eo.finish() == (c.segments[s], c.header.bit_lengths[s])
+
+
+def test_payload_bit_flip_changes_output_or_errors():
+    data = b"corruption does not crash the decoder " * 50
+    cfg = tiny_cfg(lanes=8)
+    blob = bytearray(write_container(compress(data, cfg, 2)))
+    hsize = 89 + 16
+    rng = np.random.default_rng(7)
+    changed = 0
+    for _ in range(12):
+        pos = int(rng.integers(hsize, len(blob)))
+        m = bytearray(blob)
+        m[pos] ^= 1 << int(rng.integers(0, 8))
+        try:
+            changed += decompress(read_container(bytes(m))) != data
+        except (ContainerError, CoderError):
+            changed += 1
+    assert changed >= 10
+
+
+def test_stats_reporting():
+    stats = {}
+    compress(b"stats " * 500, tiny_cfg(lanes=8), 2, stats=stats)
+    assert stats["steps"] > 0 and stats["wall_s"] > 0 and "peak_queue_depth" in stats
+
+
+def _ratio(n, blob_len):
+    return n / blob_len
+
+
+def test_ratio_within_half_percent_of_oracle_desk_dims():
+    """Same data, B, S, dims: GPU (fp32) vs the fp64 oracle pinned to the reference."""
+    data = synth.text_like(48 << 10, 1)
+    cfg = ModelConfig(**DESK, lanes=16)
+    blob = write_container(compress(data, cfg, 4))
+    assert decompress(read_container(blob)) == data
+    payloads, _ = op.compress(data, cfg, 4)
+    ref_len = 89 + 8 * 4 + sum(len(p) for p in payloads)
+    r_gpu, r_ref = _ratio(len(data), len(blob)), _ratio(len(data), ref_len)
+    assert abs(r_gpu / r_ref - 1) <= RATIO_TOL, (r_gpu, r_ref)
+
+
+@pytest.mark.parametrize("name", ["desk_text_256k", "c1_text_1m"])
+def test_ratio_within_half_percent_of_reference_run(name):
+    """Anchored on a run of the unmodified reference (tests/golden/ref_ratio_*.json)."""
+    path = os.path.join(os.path.dirname(__file__), "golden", f"ref_ratio_{name}.json")
+    if not os.path.exists(path):
+        pytest.skip("reference run not recorded")
+    ref = json.load(open(path))
+    data = synth.generate(ref["kind"], ref["nbytes"], ref["seed"])
+    assert synth.sha256(data) == ref["sha256"]
+    prof = DESK if ref["profile"] == "desk" else dict(context_len=16, embed_dim=16,
+                                                      hidden_local=2048, hidden_global=4096,
+                                                      lte_ratio=4, branches=2)
+    cfg = ModelConfig(**prof, lanes=ref["lanes"])
+    blob = write_container(compress(data, cfg, ref["segments"]))
+    assert abs((len(data) / len(blob)) / ref["ratio"] - 1) <= RATIO_TOL
+    assert decompress(read_container(blob)) == data
