@@ -108,6 +108,15 @@ int edpc_get_params(edpc_ctx* ctx, float* params, int64_t count);
 
 /* compress side: stream bytes (host or device pointer) -> device lane matrix */
 int edpc_set_input(edpc_ctx* ctx, const uint8_t* data, int64_t n, int on_device);
+/* streaming ingestion: lane columns [col0, col1) of the local lanes copied
+ * from the host stream (pitch L; zero padding past n) -- pipeline.py:44-56
+ * done column-block by column-block so H2D overlaps the model steps */
+int edpc_set_input_columns(edpc_ctx* ctx, const uint8_t* stream, int64_t n, int64_t col0,
+                           int64_t col1);
+/* coded intervals (cum_lo | freq << 16) of lane columns [col0, col1), [col][lane] */
+int edpc_get_intervals(edpc_ctx* ctx, int64_t col0, int64_t col1, uint32_t* out);
+/* lane-matrix columns [col0, col1) as [lane][col] (decoded bytes on the decode side) */
+int edpc_get_columns(edpc_ctx* ctx, int64_t col0, int64_t col1, uint8_t* out);
 /* runs lane columns [i0, i1) (bootstrap for i < context_len, model steps after) */
 int edpc_compress_steps(edpc_ctx* ctx, int64_t i0, int64_t i1);
 /* finishes every local segment; bit_lengths[S_local], payload bytes total */
@@ -138,6 +147,19 @@ int edpc_step_phase(edpc_ctx* ctx, int64_t i, int32_t phase, int32_t decompress)
 int edpc_grad_partials(edpc_ctx* ctx, float** dev_ptr, int64_t* n_shared);
 
 int edpc_sync(edpc_ctx* ctx);
+
+/* ------------------------------------------------------------ measurement
+ * CUDA-event timing of kernel regions on the stream each kernel runs on
+ * (used by bench.py for the live roofline).  Regions: 0 GEMM, 1 FDM fwd,
+ * 2 FDM bwd+Adam, 3 shared Adam, 4 softmax+quantize, 5 encoder, 6 decoder,
+ * 7 bias/LN column sums, 8 elementwise/LN, 9 embedding grad.
+ * edpc_prof_read(region = -1) returns the number of kernel launches since
+ * the last edpc_prof() call (profiling on or off). */
+int edpc_prof(edpc_ctx* ctx, int enable);
+/* device timer on the context's stream: op 0 start, op 1 stop (joins the
+ * encoder stream), op 2 wait + elapsed milliseconds into *ms */
+int edpc_timer(edpc_ctx* ctx, int32_t op, double* ms);
+int edpc_prof_read(edpc_ctx* ctx, int32_t region, double* ms, int64_t* count);
 
 #ifdef __cplusplus
 }

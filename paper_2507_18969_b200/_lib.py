@@ -16,6 +16,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "_edpc_b200.so")
 
 OK, ERR_INVALID, ERR_CUDA, ERR_CODER, ERR_STATE, ERR_NOMEM = range(6)
+REGIONS = ["gemm", "fdm_fwd", "fdm_bwd_adam", "adam_shared", "softmax_quant", "encode",
+           "decode", "colsum", "elementwise", "embed_grad"]
 
 
 class EdpcNativeError(RuntimeError):
@@ -62,6 +64,9 @@ _SIGS = {
     "edpc_load_params": ([_P, _P, _I64], ctypes.c_int),
     "edpc_get_params": ([_P, _P, _I64], ctypes.c_int),
     "edpc_set_input": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
+    "edpc_set_input_columns": ([_P, _P, _I64, _I64, _I64], ctypes.c_int),
+    "edpc_get_intervals": ([_P, _I64, _I64, _P], ctypes.c_int),
+    "edpc_get_columns": ([_P, _I64, _I64, _P], ctypes.c_int),
     "edpc_compress_steps": ([_P, _I64, _I64], ctypes.c_int),
     "edpc_compress_finish": ([_P, _P, _P], ctypes.c_int),
     "edpc_get_payloads": ([_P, _P, _I64], ctypes.c_int),
@@ -74,6 +79,9 @@ _SIGS = {
     "edpc_step_phase": ([_P, _I64, _I32, _I32], ctypes.c_int),
     "edpc_grad_partials": ([_P, _P, _P], ctypes.c_int),
     "edpc_sync": ([_P], ctypes.c_int),
+    "edpc_prof": ([_P, ctypes.c_int], ctypes.c_int),
+    "edpc_timer": ([_P, _I32, _P], ctypes.c_int),
+    "edpc_prof_read": ([_P, _I32, _P, _P], ctypes.c_int),
 }
 
 

@@ -80,11 +80,79 @@ struct Layout {
   }
 };
 
+// Per-region CUDA-event timing (bench.py's live roofline) and launch count.
+enum ProfRegion {
+  kRegGemm = 0, kRegFdmFwd, kRegFdmBwd, kRegAdam, kRegSoftmax, kRegEncode, kRegDecode,
+  kRegColsum, kRegElem, kRegEmbed, kNumRegions
+};
+
+struct Prof {
+  bool on = false;
+  int64_t launches = 0;
+  double ms[kNumRegions] = {};
+  int64_t n[kNumRegions] = {};
+  std::vector<cudaEvent_t> pool;
+  struct Pair {
+    cudaEvent_t a, b;
+    int r;
+  };
+  std::vector<Pair> pending;
+  cudaEvent_t open[kNumRegions] = {};
+
+  cudaEvent_t get() {
+    if (pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = pool.back();
+    pool.pop_back();
+    return e;
+  }
+  void begin(int r, cudaStream_t s) {
+    ++launches;
+    if (!on) return;
+    open[r] = get();
+    cudaEventRecord(open[r], s);
+  }
+  void end(int r, cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t b = get();
+    cudaEventRecord(b, s);
+    pending.push_back({open[r], b, r});
+  }
+  void flush() {
+    for (auto& p : pending) {
+      cudaEventSynchronize(p.b);
+      float t = 0.f;
+      cudaEventElapsedTime(&t, p.a, p.b);
+      ms[p.r] += t;
+      n[p.r] += 1;
+      pool.push_back(p.a);
+      pool.push_back(p.b);
+    }
+    pending.clear();
+  }
+  void reset() {
+    flush();
+    launches = 0;
+    for (int r = 0; r < kNumRegions; ++r) ms[r] = 0, n[r] = 0;
+  }
+  ~Prof() {
+    for (auto& p : pending) {
+      cudaEventDestroy(p.a);
+      cudaEventDestroy(p.b);
+    }
+    for (auto e : pool) cudaEventDestroy(e);
+  }
+};
+
 }  // namespace edpc
 
 using namespace edpc;
 
 struct edpc_ctx {
+  Prof prof;
   edpc_config cfg;
   Layout lay;
   int device = 0;
@@ -94,6 +162,7 @@ struct edpc_ctx {
   bool use_tc = false;
   cudaStream_t st = nullptr, st_enc = nullptr;
   cudaEvent_t ev = nullptr;
+  cudaEvent_t t0 = nullptr, t1 = nullptr, tj = nullptr;
   AdamConsts adam{};
 
   std::vector<void*> allocs;
@@ -131,6 +200,9 @@ struct edpc_ctx {
     if (st_enc) cudaStreamSynchronize(st_enc);
     for (void* p : allocs) cudaFree(p);
     if (ev) cudaEventDestroy(ev);
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
+    if (tj) cudaEventDestroy(tj);
     if (st) cudaStreamDestroy(st);
     if (st_enc) cudaStreamDestroy(st_enc);
   }
@@ -156,6 +228,14 @@ struct edpc_ctx {
 };
 
 namespace edpc {
+
+struct Scope {
+  edpc_ctx* c;
+  int r;
+  cudaStream_t s;
+  Scope(edpc_ctx* c_, int r_, cudaStream_t s_) : c(c_), r(r_), s(s_) { c->prof.begin(r, s); }
+  ~Scope() { c->prof.end(r, s); }
+};
 
 static int check_cfg(const edpc_config* c) {
   EDPC_CHECK_ARG(c, "null config");
@@ -189,6 +269,7 @@ static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, cons
   g.sB = sW;
   g.nzb = nzb;
   g.nsum = 1;
+  Scope sc(c, kRegGemm, c->st);
   if (c->use_tc && tc_supported(M, N, Kd)) {
     if (resid) return tc_linear_fwd(A, lda, w, N, Kd, M, bias, resid, out, nzb, sW, sOut, c->st);
     return tc_linear_fwd(A, lda, w, N, Kd, M, bias, nullptr, out, nzb, sW, sOut, c->st);
@@ -217,6 +298,7 @@ static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, in
   g.B_global = c->lay.B;
   g.lane0 = c->lane0;
   EpiPartial e{c->Gp, c->lay.n_shared, off, sOff, N, c->g_first};
+  Scope sc(c, kRegGemm, c->st);
   return gemm_simt<true, false>(g, e, c->st);
 }
 
@@ -225,6 +307,7 @@ static cudaError_t colsum(edpc_ctx* c, const float* src, int N, int nz, int64_t 
                           const float* mul, int64_t off, int64_t sOff) {
   if (c->g_count == 0) return cudaSuccess;
   dim3 grid((unsigned)cdiv(N, 256), (unsigned)nz, (unsigned)c->g_count);
+  Scope sc(c, kRegColsum, c->st);
   k_colsum_groups<<<grid, 256, 0, c->st>>>(src, N, sz, mul, N, c->Gp, c->lay.n_shared, off, sOff,
                                            c->g_first, c->lay.B, c->lane0);
   return cudaGetLastError();
@@ -246,6 +329,7 @@ static cudaError_t dgrad(edpc_ctx* c, const float* G, int Kd, int nsum, int64_t 
   g.sB_sum = sW_sum;
   g.nzb = 1;
   g.nsum = nsum;
+  Scope sc(c, kRegGemm, c->st);
   return gemm_simt<false, true>(g, epi, c->st);
 }
 
@@ -269,6 +353,7 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
   const Layout& L = c->lay;
   const int Bl = c->Bl, F = L.F, H = o.H;
   dim3 g8((unsigned)cdiv(Bl, 8));
+  Scope sc_ln(c, kRegElem, c->st);
   if (gather)
     k_embed_ln<true><<<g8, 256, 0, c->st>>>(src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
                                             c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0);
@@ -279,7 +364,10 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
   const int64_t plane = (int64_t)Bl * H;
   CK(fwd_linear(c, b.x0, F, F, c->W + o.w0, H, L.K, o.wstride, b.H, plane, c->W + o.b0, nullptr,
                 Bl));
-  k_mbrb_act<<<(unsigned)cdiv(plane, 256), 256, 0, c->st>>>(b.H, L.K, plane, b.ff);
+  {
+    Scope sc_(c, kRegElem, c->st);
+    k_mbrb_act<<<(unsigned)cdiv(plane, 256), 256, 0, c->st>>>(b.H, L.K, plane, b.ff);
+  }
   CK(cudaGetLastError());
   CK(fwd_linear(c, b.ff, H, H, c->W + o.out_w, F, 1, 0, b.out, 0, c->W + o.out_b, b.x, Bl));
   return EDPC_OK;
@@ -292,7 +380,10 @@ static int forward(edpc_ctx* c, ByteCols src) {
   EDPC_TRY(mbrb_forward(c, L.loc, lb, true, src));
   CK(fwd_linear(c, c->x_local, L.F, L.F, c->W + L.down_w, L.FP, 1, 0, c->down, 0,
                 c->W + L.down_b, nullptr, Bl));
-  k_fdm_fwd<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(c->down, c->U, c->mixed, L.FP, Bl);
+  {
+    Scope sc_(c, kRegFdmFwd, c->st);
+    k_fdm_fwd<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(c->down, c->U, c->mixed, L.FP, Bl);
+  }
   CK(cudaGetLastError());
   CK(fwd_linear(c, c->mixed, L.FP, L.FP, c->W + L.up_w, L.F, 1, 0, c->x_lte, 0, c->W + L.up_b,
                 nullptr, Bl));
@@ -305,6 +396,7 @@ static int forward(edpc_ctx* c, ByteCols src) {
 
 static int softmax_quant(edpc_ctx* c, int mode, ByteCols src) {
   dim3 g8((unsigned)cdiv(c->Bl, 8));
+  Scope sc(c, kRegSoftmax, c->st);
   if (mode == kProbsOnly)
     k_softmax_quant<kProbsOnly><<<g8, 256, 0, c->st>>>(c->logits, c->probs, c->Bl, src, c->si(),
                                                        c->intervals, c->cdf16);
@@ -340,8 +432,11 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
   // LN gain / bias gradients, then LN backward + residual
   CK(colsum(c, c->gx0, F, 1, 0, b.xhat, o.ln_g, 0));
   CK(colsum(c, c->gx0, F, 1, 0, nullptr, o.ln_b, 0));
-  k_ln_bwd<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(c->gx0, b.xhat, b.rstd, c->W + o.ln_g, g_up,
-                                                     g_in, F, Bl);
+  {
+    Scope sc_(c, kRegElem, c->st);
+    k_ln_bwd<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(c->gx0, b.xhat, b.rstd, c->W + o.ln_g, g_up,
+                                                       g_in, F, Bl);
+  }
   CK(cudaGetLastError());
   return EDPC_OK;
 }
@@ -349,8 +444,11 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
 static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   const Layout& L = c->lay;
   const int Bl = c->Bl, F = L.F, FP = L.FP;
-  k_dlogits<<<(unsigned)cdiv((int64_t)Bl * 256, 256), 256, 0, c->st>>>(
-      c->probs, src, c->si(), Bl, (float)L.B, c->gl, nll);
+  {
+    Scope sc_(c, kRegElem, c->st);
+    k_dlogits<<<(unsigned)cdiv((int64_t)Bl * 256, 256), 256, 0, c->st>>>(
+        c->probs, src, c->si(), Bl, (float)L.B, c->gl, nll);
+  }
   CK(cudaGetLastError());
   // head
   CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0));
@@ -364,9 +462,12 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   CK(colsum(c, c->gB, F, 1, 0, nullptr, L.up_b, 0));
   CK(dgrad(c, c->gB, F, 1, 0, c->W + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
   // per-lane FDM: g_down with the old U, then U's Adam step (fused)
-  k_fdm_bwd_adam<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(
-      c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, FP, Bl, c->si(), c->adam, c->cfg.beta1,
-      c->cfg.beta2);
+  {
+    Scope sc_(c, kRegFdmBwd, c->st);
+    k_fdm_bwd_adam<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(
+        c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, FP, Bl, c->si(), c->adam, c->cfg.beta1,
+        c->cfg.beta2);
+  }
   CK(cudaGetLastError());
   // LTE down
   CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0));
@@ -377,12 +478,18 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   EDPC_TRY(mbrb_backward(c, L.loc, lb, c->gA, c->gB));
   // embedding scatter-add as per-group partials
   if (c->n_chunks > 0) {
-    k_embed_grad_chunks<<<(unsigned)c->n_chunks, 256, 0, c->st>>>(src, c->si(), L.T, L.DE, F,
-                                                                  c->gB, c->chunk_tab, c->emb_sub);
+    {
+      Scope sc_(c, kRegEmbed, c->st);
+      k_embed_grad_chunks<<<(unsigned)c->n_chunks, 256, 0, c->st>>>(src, c->si(), L.T, L.DE, F,
+                                                                    c->gB, c->chunk_tab, c->emb_sub);
+    }
     CK(cudaGetLastError());
     dim3 gr((unsigned)cdiv(256 * L.DE, 256), (unsigned)c->g_count);
-    k_embed_grad_reduce<<<gr, 256, 0, c->st>>>(c->emb_sub, c->grp_chunks, L.DE, c->Gp,
-                                               L.n_shared, L.emb);
+    {
+      Scope sc_(c, kRegEmbed, c->st);
+      k_embed_grad_reduce<<<gr, 256, 0, c->st>>>(c->emb_sub, c->grp_chunks, L.DE, c->Gp,
+                                                 L.n_shared, L.emb);
+    }
     CK(cudaGetLastError());
   }
   return EDPC_OK;
@@ -390,8 +497,11 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
 
 static int adam_shared(edpc_ctx* c) {
   int blocks = (int)std::min<int64_t>(cdiv(c->lay.n_shared, 256), 148 * 8);
-  k_adam_shared<<<blocks, 256, 0, c->st>>>(c->W, c->M, c->V, c->Gp, c->lay.n_shared, c->si(),
-                                           c->adam, c->cfg.beta1, c->cfg.beta2);
+  {
+    Scope sc_(c, kRegAdam, c->st);
+    k_adam_shared<<<blocks, 256, 0, c->st>>>(c->W, c->M, c->V, c->Gp, c->lay.n_shared, c->si(),
+                                             c->adam, c->cfg.beta1, c->cfg.beta2);
+  }
   CK(cudaGetLastError());
   return EDPC_OK;
 }
@@ -402,6 +512,7 @@ static int model_step(edpc_ctx* c, int mode) {
   EDPC_TRY(forward(c, src));
   EDPC_TRY(softmax_quant(c, mode, src));
   if (mode == kDecode) {
+    Scope sc(c, kRegDecode, c->st);
     k_decode_column<<<(unsigned)cdiv(c->Sl, 4), 128, 0, c->st>>>(
         c->mat, c->L, c->si(), c->spl, c->Sl, c->cdf16, false, c->dec_state, c->payload,
         c->pay_off, c->bit_len, c->dec_err);
@@ -409,7 +520,10 @@ static int model_step(edpc_ctx* c, int mode) {
   }
   EDPC_TRY(backward(c, src, nullptr));
   EDPC_TRY(adam_shared(c));
-  k_step_advance<<<1, 1, 0, c->st>>>(c->d_i, c->d_t);
+  {
+    Scope sc_(c, kRegElem, c->st);
+    k_step_advance<<<1, 1, 0, c->st>>>(c->d_i, c->d_t);
+  }
   CK(cudaGetLastError());
   return EDPC_OK;
 }
@@ -425,6 +539,7 @@ static int launch_encoder(edpc_ctx* c, int64_t upto) {
   if (upto <= c->enc_upto) return EDPC_OK;
   CK(cudaEventRecord(c->ev, c->st));
   CK(cudaStreamWaitEvent(c->st_enc, c->ev, 0));
+  Scope sc(c, kRegEncode, c->st_enc);
   k_encode_columns<<<(unsigned)cdiv(c->Sl, 64), 64, 0, c->st_enc>>>(
       c->intervals, c->Bl, c->spl, c->Sl, c->enc_upto, upto, c->enc_state, c->enc_words,
       c->enc_cap_words);
@@ -685,6 +800,55 @@ int edpc_set_input(edpc_ctx* c, const uint8_t* data, int64_t n, int on_device) {
   return EDPC_OK;
 }
 
+int edpc_set_input_columns(edpc_ctx* c, const uint8_t* stream, int64_t n, int64_t col0,
+                           int64_t col1) {
+  EDPC_CHECK_ARG(c && (stream || n == 0), "null argument");
+  EDPC_CHECK_ARG(n == c->n, "input length differs from the context's original_len");
+  EDPC_CHECK_ARG(0 <= col0 && col0 <= col1 && col1 <= c->L, "bad column range");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  if (!c->have_input) {
+    EDPC_CUDA_TRY(cudaMemsetAsync(c->mat, 0, (int64_t)c->Bl * std::max<int64_t>(c->L, 1), c->st));
+    c->have_input = true;
+  }
+  const int64_t w = col1 - col0;
+  if (w == 0) return EDPC_OK;
+  // rows fully inside the stream go as one strided copy; at most one row is partial
+  int64_t full = 0;
+  while (full < c->Bl && ((int64_t)(c->lane0 + full)) * c->L + col1 <= n) ++full;
+  if (full)
+    EDPC_CUDA_TRY(cudaMemcpy2DAsync(c->mat + col0, c->L, stream + (int64_t)c->lane0 * c->L + col0,
+                                    c->L, w, full, cudaMemcpyHostToDevice, c->st));
+  if (full < c->Bl) {
+    const int64_t start = (int64_t)(c->lane0 + full) * c->L + col0;
+    const int64_t have = std::max<int64_t>(0, std::min<int64_t>(w, n - start));
+    if (have)
+      EDPC_CUDA_TRY(cudaMemcpyAsync(c->mat + full * c->L + col0, stream + start, have,
+                                    cudaMemcpyHostToDevice, c->st));
+  }
+  return EDPC_OK;
+}
+
+int edpc_get_intervals(edpc_ctx* c, int64_t col0, int64_t col1, uint32_t* out) {
+  EDPC_CHECK_ARG(c && out, "null argument");
+  EDPC_CHECK_ARG(0 <= col0 && col0 <= col1 && col1 <= c->L, "bad column range");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  EDPC_CUDA_TRY(cudaMemcpyAsync(out, c->intervals + col0 * c->Bl, (col1 - col0) * c->Bl * 4,
+                                cudaMemcpyDeviceToHost, c->st));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return EDPC_OK;
+}
+
+int edpc_get_columns(edpc_ctx* c, int64_t col0, int64_t col1, uint8_t* out) {
+  EDPC_CHECK_ARG(c && out, "null argument");
+  EDPC_CHECK_ARG(0 <= col0 && col0 <= col1 && col1 <= c->L, "bad column range");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  if (col1 > col0)
+    EDPC_CUDA_TRY(cudaMemcpy2DAsync(out, col1 - col0, c->mat + col0, c->L, col1 - col0, c->Bl,
+                                    cudaMemcpyDeviceToHost, c->st));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return EDPC_OK;
+}
+
 int edpc_compress_steps(edpc_ctx* c, int64_t i0, int64_t i1) {
   EDPC_CHECK_ARG(c, "null ctx");
   EDPC_CHECK_ARG(c->have_input, "set_input first");
@@ -899,6 +1063,59 @@ int edpc_grad_partials(edpc_ctx* c, float** dev_ptr, int64_t* n_shared) {
   EDPC_CHECK_ARG(c && dev_ptr && n_shared, "null argument");
   *dev_ptr = c->Gp;
   *n_shared = c->lay.n_shared;
+  return EDPC_OK;
+}
+
+int edpc_prof(edpc_ctx* c, int enable) {
+  EDPC_CHECK_ARG(c, "null ctx");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  cudaStreamSynchronize(c->st);
+  cudaStreamSynchronize(c->st_enc);
+  c->prof.reset();
+  c->prof.on = enable != 0;
+  return EDPC_OK;
+}
+
+int edpc_prof_read(edpc_ctx* c, int32_t region, double* ms, int64_t* count) {
+  EDPC_CHECK_ARG(c && ms && count, "null argument");
+  EDPC_CHECK_ARG(region >= -1 && region < kNumRegions, "bad region");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  cudaStreamSynchronize(c->st);
+  cudaStreamSynchronize(c->st_enc);
+  c->prof.flush();
+  if (region < 0) {
+    *ms = 0;
+    *count = c->prof.launches;
+  } else {
+    *ms = c->prof.ms[region];
+    *count = c->prof.n[region];
+  }
+  return EDPC_OK;
+}
+
+int edpc_timer(edpc_ctx* c, int32_t op, double* ms) {
+  EDPC_CHECK_ARG(c, "null ctx");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  if (!c->t0) {
+    EDPC_CUDA_TRY(cudaEventCreate(&c->t0));
+    EDPC_CUDA_TRY(cudaEventCreate(&c->t1));
+    EDPC_CUDA_TRY(cudaEventCreateWithFlags(&c->tj, cudaEventDisableTiming));
+  }
+  if (op == 0) {  // start: after everything queued on both streams so far
+    EDPC_CUDA_TRY(cudaEventRecord(c->tj, c->st_enc));
+    EDPC_CUDA_TRY(cudaStreamWaitEvent(c->st, c->tj, 0));
+    EDPC_CUDA_TRY(cudaEventRecord(c->t0, c->st));
+  } else if (op == 1) {  // stop: joins the encoder stream first (DPCA stage B)
+    EDPC_CUDA_TRY(cudaEventRecord(c->tj, c->st_enc));
+    EDPC_CUDA_TRY(cudaStreamWaitEvent(c->st, c->tj, 0));
+    EDPC_CUDA_TRY(cudaEventRecord(c->t1, c->st));
+  } else {
+    EDPC_CHECK_ARG(ms, "null ms");
+    EDPC_CUDA_TRY(cudaEventSynchronize(c->t1));
+    float t = 0.f;
+    EDPC_CUDA_TRY(cudaEventElapsedTime(&t, c->t0, c->t1));
+    *ms = t;
+  }
   return EDPC_OK;
 }
 
