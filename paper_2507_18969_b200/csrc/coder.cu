@@ -83,11 +83,12 @@ __global__ void k_quantize_rows(const void* __restrict__ probs, int64_t n,
   if (lane == 31) dst[256] = cum[7] + (uint32_t)freq[7];
 }
 
-__global__ void k_encode_rows(int64_t* st_io, uint32_t* words, const uint32_t* __restrict__ cums,
-                              const int32_t* __restrict__ sym, int64_t n) {
+__global__ void k_encode_rows(int64_t* st_io, uint32_t* words, int64_t cap_words,
+                              const uint32_t* __restrict__ cums, const int32_t* __restrict__ sym,
+                              int64_t n) {
   EncState st{(uint64_t)st_io[0], (uint64_t)st_io[1], (uint64_t)st_io[2], (uint64_t)st_io[3]};
   BitWriter w;
-  w.open(words, st.bitpos);
+  w.open(words, st.bitpos, (uint64_t)cap_words);
   for (int64_t r = 0; r < n; ++r) {
     int s = sym[r];
     enc_symbol(st, w, cums[r * 257 + s], cums[r * 257 + s + 1]);
@@ -99,10 +100,10 @@ __global__ void k_encode_rows(int64_t* st_io, uint32_t* words, const uint32_t* _
   st_io[3] = (int64_t)w.bitpos;
 }
 
-__global__ void k_encode_finish(int64_t* st_io, uint32_t* words) {
+__global__ void k_encode_finish(int64_t* st_io, uint32_t* words, int64_t cap_words) {
   EncState st{(uint64_t)st_io[0], (uint64_t)st_io[1], (uint64_t)st_io[2], (uint64_t)st_io[3]};
   BitWriter w;
-  w.open(words, st.bitpos);
+  w.open(words, st.bitpos, (uint64_t)cap_words);
   enc_finish(st, w);
   w.close();
   st_io[2] = 0;
@@ -212,7 +213,7 @@ int edpc_encode_rows(int device, int64_t* enc_state, uint8_t* buf, int64_t cap,
   EDPC_CUDA_TRY(cudaMemcpy(dst.p, enc_state, 32, cudaMemcpyHostToDevice));
   EDPC_CUDA_TRY(cudaMemcpy(dc.p, cums, (size_t)n * 257 * 4, cudaMemcpyHostToDevice));
   EDPC_CUDA_TRY(cudaMemcpy(ds.p, symbols, (size_t)n * 4, cudaMemcpyHostToDevice));
-  k_encode_rows<<<1, 1>>>(dst.as<int64_t>(), dbuf.as<uint32_t>(), dc.as<uint32_t>(),
+  k_encode_rows<<<1, 1>>>(dst.as<int64_t>(), dbuf.as<uint32_t>(), wbytes / 4, dc.as<uint32_t>(),
                           ds.as<int32_t>(), n);
   EDPC_CUDA_TRY(cudaGetLastError());
   EDPC_CUDA_TRY(cudaMemcpy(enc_state, dst.p, 32, cudaMemcpyDeviceToHost));
@@ -232,7 +233,7 @@ int edpc_encode_finish(int device, int64_t* enc_state, uint8_t* buf, int64_t cap
   EDPC_CUDA_TRY(cudaMemset(dbuf.p, 0, wbytes));
   EDPC_CUDA_TRY(cudaMemcpy(dbuf.p, buf, cap, cudaMemcpyHostToDevice));
   EDPC_CUDA_TRY(cudaMemcpy(dst.p, enc_state, 32, cudaMemcpyHostToDevice));
-  k_encode_finish<<<1, 1>>>(dst.as<int64_t>(), dbuf.as<uint32_t>());
+  k_encode_finish<<<1, 1>>>(dst.as<int64_t>(), dbuf.as<uint32_t>(), wbytes / 4);
   EDPC_CUDA_TRY(cudaGetLastError());
   EDPC_CUDA_TRY(cudaMemcpy(enc_state, dst.p, 32, cudaMemcpyDeviceToHost));
   EDPC_CUDA_TRY(cudaMemcpy(buf, dbuf.p, cap, cudaMemcpyDeviceToHost));

@@ -139,21 +139,28 @@ __device__ __forceinline__ void warp_cdf(const int (&freq)[8], uint32_t (&cum)[8
 __device__ __forceinline__ uint32_t bswap32(uint32_t x) { return __byte_perm(x, 0, 0x0123); }
 
 // MSB-first bit writer over 32-bit words stored big-endian (byte 0 = bits 0..7).
+// Writes past `cap` words are dropped (never out of bounds); the owner
+// sizes buffers for the worst case (18 bits/symbol, coder.py:269-270).
 struct BitWriter {
   uint32_t* words;
   uint64_t bitpos;
+  uint64_t cap;
   uint32_t acc;  // pending bits of word bitpos>>5, MSB-aligned
 
-  __device__ void open(uint32_t* w, uint64_t bp) {
+  __device__ void open(uint32_t* w, uint64_t bp, uint64_t cap_words) {
     words = w;
     bitpos = bp;
-    acc = (bp & 31) ? bswap32(w[bp >> 5]) : 0u;
+    cap = cap_words;
+    acc = ((bp & 31) && (bp >> 5) < cap) ? bswap32(w[bp >> 5]) : 0u;
+  }
+  __device__ __forceinline__ void store(uint64_t wi, uint32_t v) {
+    if (wi < cap) words[wi] = bswap32(v);
   }
   __device__ __forceinline__ void put(uint32_t bit) {
     acc |= bit << (31 - (uint32_t)(bitpos & 31));
     ++bitpos;
     if ((bitpos & 31) == 0) {
-      words[(bitpos >> 5) - 1] = bswap32(acc);
+      store((bitpos >> 5) - 1, acc);
       acc = 0;
     }
   }
@@ -169,13 +176,13 @@ struct BitWriter {
       bitpos += k;
       n -= k;
       if ((bitpos & 31) == 0) {
-        words[(bitpos >> 5) - 1] = bswap32(acc);
+        store((bitpos >> 5) - 1, acc);
         acc = 0;
       }
     }
   }
   __device__ void close() {
-    if (bitpos & 31) words[bitpos >> 5] = bswap32(acc);
+    if (bitpos & 31) store(bitpos >> 5, acc);
   }
 };
 

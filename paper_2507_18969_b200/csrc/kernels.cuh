@@ -417,7 +417,7 @@ __global__ void k_encode_columns(const uint32_t* __restrict__ intervals, int Bl,
   int64_t* stp = enc_state + 4 * s;
   EncState st{(uint64_t)stp[0], (uint64_t)stp[1], (uint64_t)stp[2], (uint64_t)stp[3]};
   BitWriter w;
-  w.open(words + (int64_t)s * cap_words, st.bitpos);
+  w.open(words + (int64_t)s * cap_words, st.bitpos, (uint64_t)cap_words);
   const int b0 = s * spl;
   for (int64_t i = i0; i < i1; ++i) {
     const uint32_t* row = intervals + i * Bl + b0;
@@ -441,7 +441,7 @@ __global__ void k_encode_finish_all(int64_t* __restrict__ enc_state, uint32_t* _
   int64_t* stp = enc_state + 4 * s;
   EncState st{(uint64_t)stp[0], (uint64_t)stp[1], (uint64_t)stp[2], (uint64_t)stp[3]};
   BitWriter w;
-  w.open(words + (int64_t)s * cap_words, st.bitpos);
+  w.open(words + (int64_t)s * cap_words, st.bitpos, (uint64_t)cap_words);
   enc_finish(st, w);
   w.close();
   stp[2] = 0;

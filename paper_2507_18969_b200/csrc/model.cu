@@ -190,7 +190,8 @@ struct edpc_ctx {
   int64_t *pay_off = nullptr, *bit_len = nullptr;
   int* dec_err = nullptr;
   // host bookkeeping
-  int64_t enc_upto = 0;  // intervals columns [0, enc_upto) handed to the encoder
+  int64_t enc_upto = 0;   // intervals columns [0, enc_upto) handed to the encoder
+  int64_t cols_done = 0;  // lane columns whose intervals have been produced
   bool finished = false, have_input = false, have_payload = false, have_cache = false;
   int64_t version = 0;   // model updates done (seam)
   int64_t seam_t = 0;
@@ -873,6 +874,7 @@ int edpc_compress_steps(edpc_ctx* c, int64_t i0, int64_t i1) {
     for (int64_t i = s0; i < i1; ++i) EDPC_TRY(model_step(c, kEncode));
   }
   // DPCA: hand the finished columns to the encoder stream
+  c->cols_done = std::max(c->cols_done, i1);
   EDPC_TRY(launch_encoder(c, i1));
   return EDPC_OK;
 }
@@ -884,7 +886,8 @@ int edpc_compress_finish(edpc_ctx* c, int64_t* bit_lengths, int64_t* total_bytes
     return EDPC_ERR_STATE;
   }
   EDPC_CUDA_TRY(cudaSetDevice(c->device));
-  EDPC_TRY(launch_encoder(c, c->L));
+  // a stream is finished after the columns actually produced (normally all L)
+  EDPC_TRY(launch_encoder(c, c->cols_done));
   k_encode_finish_all<<<(unsigned)cdiv(c->Sl, 64), 64, 0, c->st_enc>>>(
       c->enc_state, c->enc_words, c->enc_cap_words, c->Sl);
   EDPC_CUDA_TRY(cudaGetLastError());
