@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdio>
+#include <cstdlib>
 #include <algorithm>
 #include <cmath>
 #include <string>
@@ -230,12 +232,38 @@ struct edpc_ctx {
 
 namespace edpc {
 
+static bool sync_debug() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EDPC_SYNC_DEBUG");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// Brackets one kernel launch: launch count, optional CUDA-event timing, and
+// (EDPC_SYNC_DEBUG=1) a synchronous error check naming the region.
 struct Scope {
   edpc_ctx* c;
   int r;
   cudaStream_t s;
-  Scope(edpc_ctx* c_, int r_, cudaStream_t s_) : c(c_), r(r_), s(s_) { c->prof.begin(r, s); }
-  ~Scope() { c->prof.end(r, s); }
+  const char* where;
+  Scope(edpc_ctx* c_, int r_, cudaStream_t s_, const char* w = "")
+      : c(c_), r(r_), s(s_), where(w) {
+    c->prof.begin(r, s);
+  }
+  ~Scope() {
+    c->prof.end(r, s);
+    if (sync_debug()) {
+      cudaError_t e = cudaStreamSynchronize(s);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess) {
+        fprintf(stderr, "[edpc debug] region %d (%s) launch #%lld failed: %s\n", r, where,
+                (long long)c->prof.launches, cudaGetErrorString(e));
+        abort();
+      }
+    }
+  }
 };
 
 static int check_cfg(const edpc_config* c) {
@@ -888,6 +916,7 @@ int edpc_compress_finish(edpc_ctx* c, int64_t* bit_lengths, int64_t* total_bytes
   EDPC_CUDA_TRY(cudaSetDevice(c->device));
   // a stream is finished after the columns actually produced (normally all L)
   EDPC_TRY(launch_encoder(c, c->cols_done));
+  Scope sc(c, kRegEncode, c->st_enc, "encode_finish");
   k_encode_finish_all<<<(unsigned)cdiv(c->Sl, 64), 64, 0, c->st_enc>>>(
       c->enc_state, c->enc_words, c->enc_cap_words, c->Sl);
   EDPC_CUDA_TRY(cudaGetLastError());
