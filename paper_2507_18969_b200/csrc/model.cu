@@ -101,10 +101,13 @@ struct Prof {
   std::vector<Pair> pending;
   cudaEvent_t open[kNumRegions] = {};
 
+  static void chk(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fprintf(stderr, "[edpc prof] %s: %s\n", what, cudaGetErrorString(e));
+  }
   cudaEvent_t get() {
     if (pool.empty()) {
-      cudaEvent_t e;
-      cudaEventCreate(&e);
+      cudaEvent_t e = nullptr;
+      chk(cudaEventCreate(&e), "cudaEventCreate");
       return e;
     }
     cudaEvent_t e = pool.back();
@@ -115,19 +118,20 @@ struct Prof {
     ++launches;
     if (!on) return;
     open[r] = get();
-    cudaEventRecord(open[r], s);
+    chk(cudaEventRecord(open[r], s), "record(begin)");
   }
   void end(int r, cudaStream_t s) {
-    if (!on) return;
+    if (!on || !open[r]) return;
     cudaEvent_t b = get();
-    cudaEventRecord(b, s);
+    chk(cudaEventRecord(b, s), "record(end)");
     pending.push_back({open[r], b, r});
+    open[r] = nullptr;
   }
   void flush() {
     for (auto& p : pending) {
-      cudaEventSynchronize(p.b);
+      chk(cudaEventSynchronize(p.b), "sync");
       float t = 0.f;
-      cudaEventElapsedTime(&t, p.a, p.b);
+      chk(cudaEventElapsedTime(&t, p.a, p.b), "elapsed");
       ms[p.r] += t;
       n[p.r] += 1;
       pool.push_back(p.a);
@@ -140,12 +144,14 @@ struct Prof {
     launches = 0;
     for (int r = 0; r < kNumRegions; ++r) ms[r] = 0, n[r] = 0;
   }
-  ~Prof() {
+  void release() {
     for (auto& p : pending) {
-      cudaEventDestroy(p.a);
-      cudaEventDestroy(p.b);
+      chk(cudaEventDestroy(p.a), "destroy");
+      chk(cudaEventDestroy(p.b), "destroy");
     }
-    for (auto e : pool) cudaEventDestroy(e);
+    pending.clear();
+    for (auto e : pool) chk(cudaEventDestroy(e), "destroy");
+    pool.clear();
   }
 };
 
@@ -201,6 +207,8 @@ struct edpc_ctx {
   ~edpc_ctx() {
     if (st) cudaStreamSynchronize(st);
     if (st_enc) cudaStreamSynchronize(st_enc);
+    prof.flush();
+    prof.release();
     for (void* p : allocs) cudaFree(p);
     if (ev) cudaEventDestroy(ev);
     if (t0) cudaEventDestroy(t0);
