@@ -148,6 +148,12 @@ int edpc_grad_partials(edpc_ctx* ctx, float** dev_ptr, int64_t* n_shared);
 
 int edpc_sync(edpc_ctx* ctx);
 
+/* test/debug read-back of internal fp32 buffers after a step:
+ * 0 gradient partials [8][n_shared], 1 probs, 2 x_local, 3 x_lte, 4 x_global,
+ * 5 local branch outputs [k][B][h_l], 6 global branch outputs, 7 d(embedded
+ * context), 8 logits.  count must equal the buffer's element count. */
+int edpc_debug_read(edpc_ctx* ctx, int32_t which, float* out, int64_t count);
+
 /* ------------------------------------------------------------ measurement
  * CUDA-event timing of kernel regions on the stream each kernel runs on
  * (used by bench.py for the live roofline).  Regions: 0 GEMM, 1 FDM fwd,

@@ -130,6 +130,35 @@ inline cudaError_t gemm_simt(const GemmShape& g, const Epi& epi, cudaStream_t st
 }
 
 // ------------------------------------------------------------- epilogues
+//
+// Every epilogue has an element form (SIMT path) and a row32 form (tcgen05
+// path: one thread owns 32 consecutive columns of one output row).
+
+__device__ __forceinline__ bool aligned16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+__device__ __forceinline__ void load32(const float* src, float (&v)[32]) {
+  if (aligned16(src)) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4) {
+      float4 q = *reinterpret_cast<const float4*>(src + j);
+      v[j] = q.x; v[j + 1] = q.y; v[j + 2] = q.z; v[j + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = src[j];
+  }
+}
+
+__device__ __forceinline__ void store32(float* dst, const float (&v)[32]) {
+  if (aligned16(dst)) {
+#pragma unroll
+    for (int j = 0; j < 32; j += 4)
+      *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) dst[j] = v[j];
+  }
+}
 
 // C[zb] = acc + bias[zb] (row-broadcast); ldc row stride, sC batch stride
 struct EpiBias {
@@ -139,6 +168,13 @@ struct EpiBias {
   int64_t sBias;
   __device__ void operator()(int zb, int, int m, int n, float acc) const {
     C[zb * sC + (int64_t)m * ldc + n] = acc + bias[zb * sBias + n];
+  }
+  __device__ void row32(int zb, int, int m, int n0, float (&v)[32]) const {
+    float b[32];
+    load32(bias + zb * sBias + n0, b);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = v[j] + b[j];
+    store32(C + zb * sC + (int64_t)m * ldc + n0, v);
   }
 };
 
@@ -152,6 +188,14 @@ struct EpiBiasResid {
   __device__ void operator()(int, int, int m, int n, float acc) const {
     C[(int64_t)m * ldc + n] = (acc + bias[n]) + resid[(int64_t)m * ldr + n];
   }
+  __device__ void row32(int, int, int m, int n0, float (&v)[32]) const {
+    float b[32], r[32];
+    load32(bias + n0, b);
+    load32(resid + (int64_t)m * ldr + n0, r);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = (v[j] + b[j]) + r[j];
+    store32(C + (int64_t)m * ldc + n0, v);
+  }
 };
 
 // plain store (dgrad outputs)
@@ -160,6 +204,9 @@ struct EpiStore {
   int64_t ldc;
   __device__ void operator()(int, int, int m, int n, float acc) const {
     C[(int64_t)m * ldc + n] = acc;
+  }
+  __device__ void row32(int, int, int m, int n0, float (&v)[32]) const {
+    store32(C + (int64_t)m * ldc + n0, v);
   }
 };
 
@@ -172,6 +219,9 @@ struct EpiPartial {
   int g0;
   __device__ void operator()(int zb, int zg, int m, int n, float acc) const {
     partials[(int64_t)(g0 + zg) * n_shared + off + zb * sOff + (int64_t)m * ldw + n] = acc;
+  }
+  __device__ void row32(int zb, int zg, int m, int n0, float (&v)[32]) const {
+    store32(partials + (int64_t)(g0 + zg) * n_shared + off + zb * sOff + (int64_t)m * ldw + n0, v);
   }
 };
 

@@ -9,6 +9,7 @@
 
 #include "coder.cuh"
 #include "common.cuh"
+#include "gemm_simt.cuh"
 
 namespace edpc {
 
@@ -98,6 +99,34 @@ struct EpiBwdAct {
       for (int j = 0; j < K; ++j)
         if (j != z) g = g * H[j * plane + e];
       GH[z * plane + e] = g;
+    }
+  }
+  __device__ void row32(int, int, int m, int n0, float (&acc)[32]) const {
+    const int64_t e = (int64_t)m * ld + n0;
+    float p[32], h[32];
+    load32(H + e, p);
+    for (int z = 1; z < K; ++z) {
+      load32(H + z * plane + e, h);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) p[j] = p[j] * h[j];
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float cdf = gelu_cdf(p[j]);
+      const float pdf = 0.39894228040143267794f * expf(-0.5f * p[j] * p[j]);
+      acc[j] = acc[j] * (cdf + p[j] * pdf);  // g_prod
+    }
+    for (int z = 0; z < K; ++z) {
+      float g[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) g[j] = acc[j];
+      for (int jj = 0; jj < K; ++jj) {
+        if (jj == z) continue;
+        load32(H + jj * plane + e, h);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) g[j] = g[j] * h[j];
+      }
+      store32(GH + z * plane + e, g);
     }
   }
 };

@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <initializer_list>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -290,11 +291,35 @@ static int check_cfg(const edpc_config* c) {
 
 // ------------------------------------------------------------ GEMM dispatch
 
+static bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
+
+// tcgen05 path eligibility: shapes that tile cleanly and 16-byte aligned
+// operands / strides (TMA).  The choice depends only on the config and the
+// buffer layout, so compress and decompress always take the same path.
+static bool tc_ok(edpc_ctx* c, int N, int Kchunk, std::initializer_list<const void*> ptrs,
+                  std::initializer_list<int64_t> strides) {
+  if (!c->use_tc || !tc_shape_ok(N, Kchunk)) return false;
+  for (const void* p : ptrs)
+    if (!al16(p)) return false;
+  for (int64_t s : strides)
+    if (s % 4) return false;
+  return true;
+}
+
+static cudaError_t as_cuda(int st) { return st == EDPC_OK ? cudaSuccess : cudaErrorUnknown; }
+
 // out[Bl][N] = A[Bl][Kd] . W[Kd][N] (+ bias) over nzb batches (weights at
 // w + z*sW, bias at bias + z*sW, out at out + z*sOut)
 static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, const float* w,
                               int N, int nzb, int64_t sW, float* out, int64_t sOut,
                               const float* bias, const float* resid, int M) {
+  Scope sc(c, kRegGemm, c->st);
+  if (tc_ok(c, N, Kd, {A, w, out, bias, resid ? resid : out}, {lda, N, sW, sOut})) {
+    TcShape s{M, N, Kd, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 0, 1, 0, 0, 0};
+    TcOperand a{A, lda, 0, 1}, b{w, N, sW, nzb};
+    if (resid) return as_cuda(tc_gemm<false, true>(s, a, b, EpiBiasResid{out, N, bias, resid, N}, c->st));
+    return as_cuda(tc_gemm<false, true>(s, a, b, EpiBias{out, N, sOut, bias, sW}, c->st));
+  }
   GemmShape g{};
   g.M = M;
   g.N = N;
@@ -306,11 +331,6 @@ static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, cons
   g.sB = sW;
   g.nzb = nzb;
   g.nsum = 1;
-  Scope sc(c, kRegGemm, c->st);
-  if (c->use_tc && tc_supported(M, N, Kd)) {
-    if (resid) return tc_linear_fwd(A, lda, w, N, Kd, M, bias, resid, out, nzb, sW, sOut, c->st);
-    return tc_linear_fwd(A, lda, w, N, Kd, M, bias, nullptr, out, nzb, sW, sOut, c->st);
-  }
   if (resid) return gemm_simt<false, false>(g, EpiBiasResid{out, N, bias, resid, N}, c->st);
   return gemm_simt<false, false>(g, EpiBias{out, N, sOut, bias, sW}, c->st);
 }
@@ -319,6 +339,16 @@ static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, cons
 // g's lanes of X[b][m] * G[z][b][n]
 static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, int N, int nzb,
                          int64_t sG, int64_t off, int64_t sOff) {
+  EpiPartial e{c->Gp, c->lay.n_shared, off, sOff, N, c->g_first};
+  Scope sc(c, kRegGemm, c->st);
+  const int glanes = c->lay.B / kNumGroups;
+  if (c->lay.B % kNumGroups == 0 && glanes % kTcBK == 0 &&
+      tc_ok(c, N, glanes, {X, G, c->Gp + off}, {Mw, N, sG, sOff, c->lay.n_shared})) {
+    TcShape s{Mw, N, c->Bl, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 1,
+              c->g_count, c->g_first, c->lay.B, c->lane0};
+    TcOperand a{X, Mw, 0, 1}, b{G, N, sG, nzb};
+    return as_cuda(tc_gemm<true, true>(s, a, b, e, c->st));
+  }
   GemmShape g{};
   g.M = Mw;
   g.N = N;
@@ -334,8 +364,6 @@ static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, in
   g.g0 = c->g_first;
   g.B_global = c->lay.B;
   g.lane0 = c->lane0;
-  EpiPartial e{c->Gp, c->lay.n_shared, off, sOff, N, c->g_first};
-  Scope sc(c, kRegGemm, c->st);
   return gemm_simt<true, false>(g, e, c->st);
 }
 
@@ -354,6 +382,13 @@ static cudaError_t colsum(edpc_ctx* c, const float* src, int N, int nz, int64_t 
 template <class Epi>
 static cudaError_t dgrad(edpc_ctx* c, const float* G, int Kd, int nsum, int64_t sG_sum,
                          const float* w, int64_t sW_sum, int N, const Epi& epi) {
+  Scope sc(c, kRegGemm, c->st);
+  if (tc_ok(c, N, Kd, {G, w}, {Kd, sG_sum, sW_sum})) {
+    TcShape s{c->Bl, N, Kd, 1, nsum, nsum > 1 ? kBatchSum : kBatchNone,
+              nsum > 1 ? kBatchSum : kBatchNone, 0, 1, 0, 0, 0};
+    TcOperand a{G, Kd, sG_sum, nsum}, b{w, Kd, sW_sum, nsum};
+    return as_cuda(tc_gemm<false, false>(s, a, b, epi, c->st));
+  }
   GemmShape g{};
   g.M = c->Bl;
   g.N = N;
@@ -366,7 +401,6 @@ static cudaError_t dgrad(edpc_ctx* c, const float* G, int Kd, int nsum, int64_t 
   g.sB_sum = sW_sum;
   g.nzb = 1;
   g.nsum = nsum;
-  Scope sc(c, kRegGemm, c->st);
   return gemm_simt<false, true>(g, epi, c->st);
 }
 
@@ -1156,6 +1190,31 @@ int edpc_timer(edpc_ctx* c, int32_t op, double* ms) {
     EDPC_CUDA_TRY(cudaEventElapsedTime(&t, c->t0, c->t1));
     *ms = t;
   }
+  return EDPC_OK;
+}
+
+int edpc_debug_read(edpc_ctx* c, int32_t which, float* out, int64_t count) {
+  EDPC_CHECK_ARG(c && out, "null argument");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  const Layout& L = c->lay;
+  const int64_t Bl = c->Bl;
+  const float* src = nullptr;
+  int64_t n = 0;
+  switch (which) {
+    case 0: src = c->Gp; n = (int64_t)kNumGroups * L.n_shared; break;
+    case 1: src = c->probs; n = Bl * 256; break;
+    case 2: src = c->x_local; n = Bl * L.F; break;
+    case 3: src = c->x_lte; n = Bl * L.F; break;
+    case 4: src = c->x_global; n = Bl * L.F; break;
+    case 5: src = c->l_H; n = (int64_t)L.K * Bl * L.HL; break;
+    case 6: src = c->g_H; n = (int64_t)L.K * Bl * L.HG; break;
+    case 7: src = c->gB; n = Bl * L.F; break;
+    case 8: src = c->logits; n = Bl * 256; break;
+    default: EDPC_CHECK_ARG(false, "unknown debug buffer");
+  }
+  EDPC_CHECK_ARG(count == n, "debug buffer size mismatch (expected " + std::to_string(n) + ")");
+  EDPC_CUDA_TRY(cudaMemcpy(out, src, n * 4, cudaMemcpyDeviceToHost));
   return EDPC_OK;
 }
 

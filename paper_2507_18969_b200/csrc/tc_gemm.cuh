@@ -1,14 +1,420 @@
-// tcgen05 (sm_100a) GEMM fast path -- placeholder until the TMEM/TMA kernel lands.
+// tcgen05 / TMA / TMEM GEMM for sm_100a -- the fast path of every per-step
+// contraction of the EDPC predictor and its online update.
+//
+//   D[M x N] (fp32, TMEM) = sum_k A[M x K] * B[K x N], kind::tf32 (fp32 in HBM)
+//
+// One CTA per 128 x BN output tile, warp-specialised:
+//   warp 0      TMA producer: 128B-swizzled tiles of A and B into a
+//               kStages-deep shared-memory ring (mbarrier full/empty pairs)
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (4 MMAs of
+//               K=8 per 32-wide K block); tcgen05.commit frees ring slots
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> registers -> fused
+//               epilogue functor (bias, residual, GeLU/product-rule backward,
+//               lane-group weight-gradient partials) -> global
+// Operands may be K-major or MN-major (the instruction descriptor's
+// transpose bits), so activations stored [lanes][features] serve directly as
+// the MN-major operands of the weight-gradient GEMMs (K = lanes).
+// The MMA order over K is fixed, so results are bitwise reproducible.
 #pragma once
+
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "common.cuh"
+
 namespace edpc {
-inline bool tc_compiled() { return false; }
-inline bool tc_enabled_env() { return false; }
-inline bool tc_supported(int, int, int) { return false; }
-inline cudaError_t tc_linear_fwd(const float*, int, const float*, int, int, int, const float*,
-                                 const float*, float*, int, int64_t, int64_t, cudaStream_t) {
-  return cudaErrorNotSupported;
+
+inline bool tc_compiled() { return true; }
+inline bool tc_enabled_env() {
+  const char* e = getenv("EDPC_TCGEN05");
+  return !(e && e[0] == '0');
 }
+
+constexpr int kTcBM = 128;
+constexpr int kTcBK = 32;  // fp32 elements per 128-byte swizzle row
+constexpr int kTcStages = 4;
+
+// --------------------------------------------------------------- PTX helpers
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+// 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+        "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+        "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+// Shared-memory matrix descriptor (tcgen05 "version 1"), SWIZZLE_128B.
+//   K-major : rows of 128 B (32 fp32 of K); 8-row atoms 1024 B apart (SBO)
+//   MN-major: K-rows of 128 B (32 fp32 of M/N); 32-wide MN blocks LBO apart
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// ------------------------------------------------------------------ shapes
+
+// Where an operand's batch coordinate comes from.
+enum TcBatch { kBatchNone = 0, kBatchZ = 1, kBatchSum = 2 };
+
+struct TcShape {
+  int M, N, K;       // K per summed sub-problem (before any K split)
+  int nzb;           // output batches (blockIdx.z % nzb)
+  int nsum;          // sub-problems accumulated into one tile
+  int a_batch, b_batch;
+  // K split, one output per split index zg = blockIdx.z / nzb:
+  //   kmode 0: none; 1: lane groups [g0+zg] of B_global lanes (minus lane0);
+  //   2: nsplit equal K chunks
+  int kmode, nsplit, g0, B_global, lane0;
+};
+
+// ------------------------------------------------------------------ kernel
+
+template <int BN>
+struct TcSmem {
+  static constexpr int kABytes = kTcBM * kTcBK * 4;  // 16 KB
+  static constexpr int kBBytes = BN * kTcBK * 4;
+  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kBytes = kTcStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BN, bool AMN, bool BMN, class Epi>
+__global__ void __launch_bounds__(192, 1)
+k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+          TcShape s, Epi epi) {
+  extern __shared__ uint8_t smem_raw[];
+  using SM = TcSmem<BN>;
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * SM::kStageBytes);
+  uint64_t* empty = full + kTcStages;
+  uint64_t* accum = empty + kTcStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN;
+  const int m0 = blockIdx.y * kTcBM;
+  const int zb = blockIdx.z % s.nzb;
+  const int zg = blockIdx.z / s.nzb;
+
+  int k_begin = 0, k_end = s.K;
+  if (s.kmode == 1) {
+    k_begin = group_begin(s.g0 + zg, s.B_global) - s.lane0;
+    k_end = group_begin(s.g0 + zg + 1, s.B_global) - s.lane0;
+  } else if (s.kmode == 2) {
+    const int chunk = s.K / s.nsplit;
+    k_begin = zg * chunk;
+    k_end = k_begin + chunk;
+  }
+  const int nkb = (k_end - k_begin) / kTcBK;
+  const int total = nkb * s.nsum;
+
+  if (warp == 0 && lane == 0) {
+    for (int st = 0; st < kTcStages; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"((uint32_t)(BN < 32 ? 32 : BN)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0 && total > 0) {
+      // ---------------- TMA producer
+      for (int it = 0; it < total; ++it) {
+        const int st = it % kTcStages;
+        const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
+        mbar_wait(&empty[st], ph ^ 1u);
+        const int sub = it / nkb;
+        const int k = k_begin + (it - sub * nkb) * kTcBK;
+        const int az = s.a_batch == kBatchZ ? zb : (s.a_batch == kBatchSum ? sub : 0);
+        const int bz = s.b_batch == kBatchZ ? zb : (s.b_batch == kBatchSum ? sub : 0);
+        uint8_t* sa = smem + st * SM::kStageBytes;
+        uint8_t* sb = sa + SM::kABytes;
+        mbar_expect_tx(&full[st], SM::kStageBytes);
+        if (AMN) {
+#pragma unroll
+          for (int j = 0; j < kTcBM / 32; ++j)
+            tma_load_3d(sa + j * 4096, &tma_a, &full[st], m0 + 32 * j, k, az);
+        } else {
+          tma_load_3d(sa, &tma_a, &full[st], k, m0, az);
+        }
+        if (BMN) {
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j)
+            tma_load_3d(sb + j * 4096, &tma_b, &full[st], n0 + 32 * j, k, bz);
+        } else {
+          tma_load_3d(sb, &tma_b, &full[st], k, n0, bz);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && total > 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = idesc_tf32(kTcBM, BN, AMN ? 1 : 0, BMN ? 1 : 0);
+      for (int it = 0; it < total; ++it) {
+        const int st = it % kTcStages;
+        const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
+        mbar_wait(&full[st], ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + st * SM::kStageBytes);
+        const uint32_t sb = sa + SM::kABytes;
+#pragma unroll
+        for (int kk = 0; kk < kTcBK / 8; ++kk) {
+          // K-major: advance 32 B inside the swizzled row; MN-major: one
+          // 1024 B atom (8 K-rows) per step
+          const uint64_t ad = AMN ? sdesc(sa + kk * 1024, 4096, 1024) : sdesc(sa + kk * 32, 16, 1024);
+          const uint64_t bd = BMN ? sdesc(sb + kk * 1024, 4096, 1024) : sdesc(sb + kk * 32, 16, 1024);
+          tc_mma_tf32(tmem, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(&empty[st]);
+      }
+      tc_commit(accum);
+    }
+  } else {
+    // ---------------- epilogue warps 2..5 (TMEM lane quadrant = warp % 4)
+    const int quad = warp & 3;
+    const int m = m0 + quad * 32 + lane;
+    if (total > 0) {
+      mbar_wait(accum, 0);
+      tc_fence_after();
+    }
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      if (total > 0) {
+        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c, v);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+      }
+      if (m < s.M && n0 + c < s.N) epi.row32(zb, zg, m, n0 + c, v);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                 "r"((uint32_t)(BN < 32 ? 32 : BN)));
+  }
+}
+
+// ------------------------------------------------------- host: tensor maps
+
+// 3-D fp32 tensor map: dims {inner, rows, batch}; strides in elements.
+inline int make_tmap(CUtensorMap* map, const float* base, uint64_t inner, uint64_t rows,
+                     uint64_t batch, uint64_t row_stride, uint64_t batch_stride, uint32_t box_inner,
+                     uint32_t box_rows) {
+  cuuint64_t dims[3] = {inner, rows, batch < 1 ? 1 : batch};
+  cuuint64_t strides[2] = {row_stride * 4, (batch_stride ? batch_stride : row_stride * rows) * 4};
+  cuuint32_t box[3] = {box_inner, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims,
+                                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    const char* s = nullptr;
+    cuGetErrorString(r, &s);
+    set_error(std::string("cuTensorMapEncodeTiled: ") + (s ? s : "?"));
+    return EDPC_ERR_CUDA;
+  }
+  return EDPC_OK;
+}
+
+// An operand as stored in global memory: row-major [rows][inner] (+ batch).
+struct TcOperand {
+  const float* ptr;
+  int64_t ld;      // row stride (elements)
+  int64_t sbatch;  // batch stride (elements), 0 if no batch
+  int nbatch;
+};
+
+struct TmapCache {
+  std::mutex mu;
+  std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint32_t,
+                      uint32_t>,
+           CUtensorMap>
+      maps;
+  int get(CUtensorMap* out, const float* base, uint64_t inner, uint64_t rows, uint64_t batch,
+          uint64_t ld, uint64_t sb, uint32_t bi, uint32_t br) {
+    auto key = std::make_tuple((const void*)base, inner, rows, batch, ld, sb, bi, br);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = maps.find(key);
+    if (it != maps.end()) {
+      *out = it->second;
+      return EDPC_OK;
+    }
+    CUtensorMap m;
+    int r = make_tmap(&m, base, inner, rows, batch, ld, sb, bi, br);
+    if (r != EDPC_OK) return r;
+    maps.emplace(key, m);
+    *out = m;
+    return EDPC_OK;
+  }
+};
+
+inline TmapCache& tmap_cache() {
+  static TmapCache c;
+  return c;
+}
+
+// True when the shape tiles cleanly: M any (TMA zero-fills, epilogue masks),
+// N a multiple of 32 (<= 256 per tile or a multiple of 256), K chunks of 32.
+inline bool tc_shape_ok(int N, int Kchunk) {
+  if (N % 32 != 0 || Kchunk % kTcBK != 0 || Kchunk <= 0) return false;
+  return N <= 256 ? (N == 32 || N == 64 || N == 128 || N == 256) : (N % 256 == 0);
+}
+
+template <int BN, bool AMN, bool BMN, class Epi>
+inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, const Epi& epi,
+                     cudaStream_t st) {
+  CUtensorMap ta, tb;
+  int r;
+  // A: K-major -> [M rows][K inner]; MN-major -> [K rows][M inner]
+  if (AMN)
+    r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.M, (uint64_t)s.K, (uint64_t)A.nbatch,
+                         (uint64_t)A.ld, (uint64_t)A.sbatch, 32, 32);
+  else
+    r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.K, (uint64_t)s.M, (uint64_t)A.nbatch,
+                         (uint64_t)A.ld, (uint64_t)A.sbatch, 32, kTcBM);
+  if (r != EDPC_OK) return r;
+  // B: K-major -> [N rows][K inner]; MN-major -> [K rows][N inner]
+  if (BMN)
+    r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.N, (uint64_t)s.K, (uint64_t)B.nbatch,
+                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, 32);
+  else
+    r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.K, (uint64_t)s.N, (uint64_t)B.nbatch,
+                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN);
+  if (r != EDPC_OK) return r;
+  const int nz = s.nzb * (s.kmode == 0 ? 1 : s.nsplit);
+  dim3 grid((unsigned)(s.N / BN), (unsigned)cdiv(s.M, kTcBM), (unsigned)nz);
+  auto kern = k_tc_gemm<BN, AMN, BMN, Epi>;
+  static bool attr_done[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 16 && !attr_done[dev]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<BN>::kBytes);
+    attr_done[dev] = true;
+  }
+  kern<<<grid, 192, TcSmem<BN>::kBytes, st>>>(ta, tb, s, epi);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("k_tc_gemm launch: ") + cudaGetErrorString(e));
+    return EDPC_ERR_CUDA;
+  }
+  return EDPC_OK;
+}
+
+// BN dispatch: the widest tile <= 256 that divides N
+template <bool AMN, bool BMN, class Epi>
+inline int tc_gemm(const TcShape& s, const TcOperand& A, const TcOperand& B, const Epi& epi,
+                   cudaStream_t st) {
+  if (s.N % 256 == 0) return tc_launch<256, AMN, BMN>(s, A, B, epi, st);
+  if (s.N == 128) return tc_launch<128, AMN, BMN>(s, A, B, epi, st);
+  if (s.N == 64) return tc_launch<64, AMN, BMN>(s, A, B, epi, st);
+  if (s.N == 32) return tc_launch<32, AMN, BMN>(s, A, B, epi, st);
+  set_error("tc_gemm: unsupported N");
+  return EDPC_ERR_INVALID;
+}
+
 }  // namespace edpc

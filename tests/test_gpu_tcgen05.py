@@ -1,0 +1,77 @@
+"""tcgen05 (kind::tf32) GEMM path vs the fp32 SIMT path on the same weights and
+inputs: every per-step intermediate and every gradient partial.  Tolerances
+are TF32's (10-bit mantissa operands, fp32 accumulation): relative error of
+each tensor in Frobenius norm <= 2e-3."""
+import ctypes
+import os
+
+import numpy as np
+import pytest
+
+from paper_2507_18969_b200 import _lib
+from paper_2507_18969_b200.config import ModelConfig, param_offsets
+from paper_2507_18969_b200.init import init_params_f32
+from paper_2507_18969_b200.model import DeviceContext
+from helpers import PAPER
+
+pytestmark = pytest.mark.gpu
+REL = 2e-3
+
+
+def _ctx(cfg, tc: bool):
+    os.environ["EDPC_TCGEN05"] = "1" if tc else "0"
+    try:
+        c = DeviceContext(cfg, 4, 0, 0)
+    finally:
+        os.environ.pop("EDPC_TCGEN05", None)
+    c.load_flat(init_params_f32(cfg))
+    return c
+
+
+def _read(c, which, n):
+    out = np.empty(n, dtype=np.float32)
+    _lib.check(_lib.load().edpc_debug_read(c.h, which, out.ctypes.data, n))
+    return out
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(a.astype(np.float64) - b) / max(np.linalg.norm(b.astype(np.float64)), 1e-30))
+
+
+@pytest.mark.parametrize("lanes,extra", [(256, {}), (512, dict(branches=1)), (256, dict(lte_ratio=1))])
+def test_tcgen05_matches_simt(lanes, extra):
+    if not _lib.load().edpc_has_tcgen05():
+        pytest.skip("tcgen05 path not compiled")
+    cfg = ModelConfig(**dict(PAPER, **extra), lanes=lanes)
+    lib = _lib.load()
+    a, b = _ctx(cfg, True), _ctx(cfg, False)
+    rng = np.random.default_rng(0)
+    F, T = cfg.feature_dim, cfg.context_len
+    sizes = {1: lanes * 256, 2: lanes * F, 3: lanes * F, 4: lanes * F,
+             5: cfg.branches * lanes * cfg.hidden_local, 6: cfg.branches * lanes * cfg.hidden_global,
+             7: lanes * F, 8: lanes * 256}
+    for step in range(3):
+        ctx = rng.integers(0, 256, size=(lanes, T), dtype=np.uint8)
+        tg = rng.integers(0, 256, size=lanes, dtype=np.uint8)
+        for c in (a, b):
+            _lib.check(lib.edpc_predict(c.h, ctx.ctypes.data, None))
+        for w in (2, 3, 4, 5, 6, 8, 1):
+            r = _rel(_read(a, w, sizes[w]), _read(b, w, sizes[w]))
+            assert r <= REL, (step, "buffer", w, r)
+        loss = ctypes.c_float()
+        for c in (a, b):
+            _lib.check(lib.edpc_train_step(c.h, tg.ctypes.data, ctypes.byref(loss)))
+        r = _rel(_read(a, 7, sizes[7]), _read(b, 7, sizes[7]))
+        assert r <= REL, (step, "d(context)", r)
+        ga = _read(a, 0, 8 * a.n_shared).reshape(8, -1).sum(0)
+        gb = _read(b, 0, 8 * b.n_shared).reshape(8, -1).sum(0)
+        offs = param_offsets(cfg)
+        lm = offs["lte.lane_mats"][0]
+        fdm = int(np.prod(offs["lte.lane_mats"][1]))
+        for name, (o, shape) in offs.items():
+            if name == "lte.lane_mats":
+                continue
+            so = o if o < lm else o - fdm
+            n = int(np.prod(shape))
+            r = _rel(ga[so: so + n], gb[so: so + n])
+            assert r <= REL, (step, name, r)
