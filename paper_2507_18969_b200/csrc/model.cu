@@ -1193,6 +1193,39 @@ int edpc_timer(edpc_ctx* c, int32_t op, double* ms) {
   return EDPC_OK;
 }
 
+// Standalone GEMM through the tcgen05 path (tests): C[M][N] = A . B with A
+// given [M][K] (a_mn = 0) or [K][M] (a_mn = 1) and B [N][K] (b_mn = 0) or
+// [K][N] (b_mn = 1), all row-major fp32 host arrays.
+int edpc_debug_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn, const float* A,
+                    const float* B, float* C) {
+  EDPC_CHECK_ARG(A && B && C && M > 0 && N > 0 && K > 0, "bad arguments");
+  EDPC_CHECK_ARG(tc_shape_ok(N, K), "shape not supported by the tcgen05 path");
+  float *dA, *dB, *dC;
+  EDPC_CUDA_TRY(cudaMalloc(&dA, (size_t)M * K * 4));
+  EDPC_CUDA_TRY(cudaMalloc(&dB, (size_t)N * K * 4));
+  EDPC_CUDA_TRY(cudaMalloc(&dC, (size_t)M * N * 4));
+  EDPC_CUDA_TRY(cudaMemcpy(dA, A, (size_t)M * K * 4, cudaMemcpyHostToDevice));
+  EDPC_CUDA_TRY(cudaMemcpy(dB, B, (size_t)N * K * 4, cudaMemcpyHostToDevice));
+  EDPC_CUDA_TRY(cudaMemset(dC, 0, (size_t)M * N * 4));
+  TcShape s{M, N, K, 1, 1, kBatchNone, kBatchNone, 0, 1, 0, 0, 0};
+  TcOperand a{dA, a_mn ? M : K, 0, 1}, b{dB, b_mn ? N : K, 0, 1};
+  EpiStore e{dC, N};
+  int st;
+  if (!a_mn && !b_mn) st = tc_gemm<false, false>(s, a, b, e, 0);
+  else if (!a_mn && b_mn) st = tc_gemm<false, true>(s, a, b, e, 0);
+  else if (a_mn && !b_mn) st = tc_gemm<true, false>(s, a, b, e, 0);
+  else st = tc_gemm<true, true>(s, a, b, e, 0);
+  cudaError_t ce = cudaDeviceSynchronize();
+  if (st == EDPC_OK && ce == cudaSuccess)
+    ce = cudaMemcpy(C, dC, (size_t)M * N * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dC);
+  if (st != EDPC_OK) return st;
+  EDPC_CUDA_TRY(ce);
+  return EDPC_OK;
+}
+
 int edpc_debug_read(edpc_ctx* c, int32_t which, float* out, int64_t count) {
   EDPC_CHECK_ARG(c && out, "null argument");
   EDPC_CUDA_TRY(cudaSetDevice(c->device));

@@ -55,9 +55,10 @@ def test_tcgen05_matches_simt(lanes, extra):
         tg = rng.integers(0, 256, size=lanes, dtype=np.uint8)
         for c in (a, b):
             _lib.check(lib.edpc_predict(c.h, ctx.ctypes.data, None))
-        for w in (2, 3, 4, 5, 6, 8, 1):
-            r = _rel(_read(a, w, sizes[w]), _read(b, w, sizes[w]))
-            assert r <= REL, (step, "buffer", w, r)
+        errs = {w: _rel(_read(a, w, sizes[w]), _read(b, w, sizes[w])) for w in (5, 2, 3, 6, 4, 8, 1)}
+        print("step", step, errs)
+        for w, r in errs.items():
+            assert r <= REL, (step, "buffer", w, r, errs)
         loss = ctypes.c_float()
         for c in (a, b):
             _lib.check(lib.edpc_train_step(c.h, tg.ctypes.data, ctypes.byref(loss)))
@@ -75,3 +76,23 @@ def test_tcgen05_matches_simt(lanes, extra):
             n = int(np.prod(shape))
             r = _rel(ga[so: so + n], gb[so: so + n])
             assert r <= REL, (step, name, r)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 32), (128, 256, 64), (256, 512, 256), (200, 128, 96)])
+@pytest.mark.parametrize("a_mn", [0, 1])
+@pytest.mark.parametrize("b_mn", [0, 1])
+def test_tc_gemm_unit(M, N, K, a_mn, b_mn):
+    """Raw tcgen05 GEMM vs float64 numpy on TF32-rounded inputs."""
+    if not _lib.load().edpc_has_tcgen05():
+        pytest.skip("tcgen05 path not compiled")
+    rng = np.random.default_rng(M + N + K)
+    A = rng.normal(size=(M, K)).astype(np.float32)
+    B = rng.normal(size=(K, N)).astype(np.float32)
+    Ah = np.ascontiguousarray(A.T) if a_mn else A
+    Bh = B if b_mn else np.ascontiguousarray(B.T)
+    C = np.empty((M, N), dtype=np.float32)
+    _lib.check(_lib.load().edpc_debug_gemm(M, N, K, a_mn, b_mn, Ah.ctypes.data, Bh.ctypes.data,
+                                           C.ctypes.data))
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    err = np.abs(C - ref).max() / np.abs(ref).max()
+    assert err < 3e-3, (err, C[:2, :4], ref[:2, :4])
