@@ -157,7 +157,7 @@ int edpc_debug_read(edpc_ctx* ctx, int32_t which, float* out, int64_t count);
  * C[M][N] = A . B, A [M][K] (a_mn 0) or [K][M] (a_mn 1), B [N][K] (b_mn 0)
  * or [K][N] (b_mn 1) */
 int edpc_debug_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn, const float* A,
-                    const float* B, float* C);
+                    const float* B, float* C, int32_t dbg);
 
 /* ------------------------------------------------------------ measurement
  * CUDA-event timing of kernel regions on the stream each kernel runs on

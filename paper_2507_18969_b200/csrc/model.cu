@@ -1197,7 +1197,7 @@ int edpc_timer(edpc_ctx* c, int32_t op, double* ms) {
 // given [M][K] (a_mn = 0) or [K][M] (a_mn = 1) and B [N][K] (b_mn = 0) or
 // [K][N] (b_mn = 1), all row-major fp32 host arrays.
 int edpc_debug_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn, const float* A,
-                    const float* B, float* C) {
+                    const float* B, float* C, int32_t dbg) {
   EDPC_CHECK_ARG(A && B && C && M > 0 && N > 0 && K > 0, "bad arguments");
   EDPC_CHECK_ARG(tc_shape_ok(N, K), "shape not supported by the tcgen05 path");
   float *dA, *dB, *dC;
@@ -1207,7 +1207,7 @@ int edpc_debug_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn,
   EDPC_CUDA_TRY(cudaMemcpy(dA, A, (size_t)M * K * 4, cudaMemcpyHostToDevice));
   EDPC_CUDA_TRY(cudaMemcpy(dB, B, (size_t)N * K * 4, cudaMemcpyHostToDevice));
   EDPC_CUDA_TRY(cudaMemset(dC, 0, (size_t)M * N * 4));
-  TcShape s{M, N, K, 1, 1, kBatchNone, kBatchNone, 0, 1, 0, 0, 0};
+  TcShape s{M, N, K, 1, 1, kBatchNone, kBatchNone, 0, 1, 0, 0, 0, dbg};
   TcOperand a{dA, a_mn ? M : K, 0, 1}, b{dB, b_mn ? N : K, 0, 1};
   EpiStore e{dC, N};
   int st;

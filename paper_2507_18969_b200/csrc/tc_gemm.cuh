@@ -153,6 +153,7 @@ struct TcShape {
   //   kmode 0: none; 1: lane groups [g0+zg] of B_global lanes (minus lane0);
   //   2: nsplit equal K chunks
   int kmode, nsplit, g0, B_global, lane0;
+  int dbg = 0;  // tests only: 1 = epilogue writes m*1000+n, 2 = dump smem A stage 0
 };
 
 // ------------------------------------------------------------------ kernel
@@ -280,7 +281,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       float v[32];
-      if (total > 0) {
+      if (s.dbg == 1) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = (float)(m * 1000 + n0 + c + j);
+      } else if (s.dbg == 2) {
+        const float* sa = reinterpret_cast<const float*>(smem);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = sa[(quad * 32 + lane) * 32 + j];
+      } else if (total > 0) {
         tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c, v);
       } else {
 #pragma unroll

@@ -92,7 +92,7 @@ def test_tc_gemm_unit(M, N, K, a_mn, b_mn):
     Bh = B if b_mn else np.ascontiguousarray(B.T)
     C = np.empty((M, N), dtype=np.float32)
     _lib.check(_lib.load().edpc_debug_gemm(M, N, K, a_mn, b_mn, Ah.ctypes.data, Bh.ctypes.data,
-                                           C.ctypes.data))
+                                           C.ctypes.data, 0))
     ref = A.astype(np.float64) @ B.astype(np.float64)
     err = np.abs(C - ref).max() / np.abs(ref).max()
     assert err < 3e-3, (err, C[:2, :4], ref[:2, :4])
