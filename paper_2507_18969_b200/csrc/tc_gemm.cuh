@@ -262,8 +262,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
         for (int kk = 0; kk < kTcBK / 8; ++kk) {
           // K-major: advance 32 B inside the swizzled row; MN-major: one
           // 1024 B atom (8 K-rows) per step
-          const uint64_t ad = AMN ? sdesc(sa + kk * 1024, 4096, 1024) : sdesc(sa + kk * 32, 16, 1024);
-          const uint64_t bd = BMN ? sdesc(sb + kk * 1024, 4096, 1024) : sdesc(sb + kk * 32, 16, 1024);
+          const uint32_t mn_lbo = s.dbg == 3 ? 1024 : 4096, mn_sbo = s.dbg == 3 ? 4096 : 1024;
+          const uint64_t ad = AMN ? sdesc(sa + kk * 1024, mn_lbo, mn_sbo) : sdesc(sa + kk * 32, 16, 1024);
+          const uint64_t bd = BMN ? sdesc(sb + kk * 1024, mn_lbo, mn_sbo) : sdesc(sb + kk * 32, 16, 1024);
           tc_mma_tf32(tmem, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
         }
         tc_commit(&empty[st]);
@@ -284,7 +285,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       if (s.dbg == 1) {
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = (float)(m * 1000 + n0 + c + j);
-      } else if (s.dbg == 2) {
+      } else if (s.dbg == 2 && total > 0) {
+        mbar_wait(accum, 0);
         const float* sa = reinterpret_cast<const float*>(smem);
 #pragma unroll
         for (int j = 0; j < 32; ++j) v[j] = sa[(quad * 32 + lane) * 32 + j];
