@@ -120,18 +120,24 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
-// Shared-memory matrix descriptor (tcgen05 "version 1"), SWIZZLE_128B.
-//   K-major : rows of 128 B (32 fp32 of K); 8-row atoms 1024 B apart (SBO)
-//   MN-major: K-rows of 128 B (32 fp32 of M/N); 32-wide MN blocks LBO apart
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// Shared-memory matrix descriptor (tcgen05 "version 1").
+//   K-major : SWIZZLE_128B (layout 2): rows of 128 B (32 fp32 of K), 8-row
+//             atoms 1024 B apart (SBO); K steps of 8 advance the start by 32 B
+//   MN-major: tf32 admits only SWIZZLE_128B_BASE32B (layout 1): K-rows of
+//             128 B (32 fp32 of M/N) swizzled in 32 B units over 4-row atoms
+//             (SBO = 512 B), 32-wide MN blocks LBO apart; K steps of 8 rows
+//             advance the start by 1024 B
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo,
+                                          uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;  // descriptor version (Blackwell)
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  d |= (uint64_t)layout << 61;
   return d;
 }
+constexpr uint32_t kLayoutSW128 = 2, kLayoutSW128Base32B = 1;
 
 // instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
@@ -262,9 +268,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
         for (int kk = 0; kk < kTcBK / 8; ++kk) {
           // K-major: advance 32 B inside the swizzled row; MN-major: one
           // 1024 B atom (8 K-rows) per step
-          const uint32_t mn_lbo = s.dbg == 3 ? 1024 : 4096, mn_sbo = s.dbg == 3 ? 4096 : 1024;
-          const uint64_t ad = AMN ? sdesc(sa + kk * 1024, mn_lbo, mn_sbo) : sdesc(sa + kk * 32, 16, 1024);
-          const uint64_t bd = BMN ? sdesc(sb + kk * 1024, mn_lbo, mn_sbo) : sdesc(sb + kk * 32, 16, 1024);
+          const uint64_t ad = AMN ? sdesc(sa + kk * 1024, 4096, 512, kLayoutSW128Base32B)
+                                  : sdesc(sa + kk * 32, 16, 1024, kLayoutSW128);
+          const uint64_t bd = BMN ? sdesc(sb + kk * 1024, 4096, 512, kLayoutSW128Base32B)
+                                  : sdesc(sb + kk * 32, 16, 1024, kLayoutSW128);
           tc_mma_tf32(tmem, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
         }
         tc_commit(&empty[st]);
@@ -313,14 +320,16 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
 // 3-D fp32 tensor map: dims {inner, rows, batch}; strides in elements.
 inline int make_tmap(CUtensorMap* map, const float* base, uint64_t inner, uint64_t rows,
                      uint64_t batch, uint64_t row_stride, uint64_t batch_stride, uint32_t box_inner,
-                     uint32_t box_rows) {
+                     uint32_t box_rows, bool mn_major) {
   cuuint64_t dims[3] = {inner, rows, batch < 1 ? 1 : batch};
   cuuint64_t strides[2] = {row_stride * 4, (batch_stride ? batch_stride : row_stride * rows) * 4};
   cuuint32_t box[3] = {box_inner, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims,
                                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                               : CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     const char* s = nullptr;
@@ -342,12 +351,12 @@ struct TcOperand {
 struct TmapCache {
   std::mutex mu;
   std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint32_t,
-                      uint32_t>,
+                      uint32_t, bool>,
            CUtensorMap>
       maps;
   int get(CUtensorMap* out, const float* base, uint64_t inner, uint64_t rows, uint64_t batch,
-          uint64_t ld, uint64_t sb, uint32_t bi, uint32_t br) {
-    auto key = std::make_tuple((const void*)base, inner, rows, batch, ld, sb, bi, br);
+          uint64_t ld, uint64_t sb, uint32_t bi, uint32_t br, bool mn) {
+    auto key = std::make_tuple((const void*)base, inner, rows, batch, ld, sb, bi, br, mn);
     std::lock_guard<std::mutex> g(mu);
     auto it = maps.find(key);
     if (it != maps.end()) {
@@ -355,7 +364,7 @@ struct TmapCache {
       return EDPC_OK;
     }
     CUtensorMap m;
-    int r = make_tmap(&m, base, inner, rows, batch, ld, sb, bi, br);
+    int r = make_tmap(&m, base, inner, rows, batch, ld, sb, bi, br, mn);
     if (r != EDPC_OK) return r;
     maps.emplace(key, m);
     *out = m;
@@ -383,18 +392,18 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
   // A: K-major -> [M rows][K inner]; MN-major -> [K rows][M inner]
   if (AMN)
     r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.M, (uint64_t)s.K, (uint64_t)A.nbatch,
-                         (uint64_t)A.ld, (uint64_t)A.sbatch, 32, 32);
+                         (uint64_t)A.ld, (uint64_t)A.sbatch, 32, 32, true);
   else
     r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.K, (uint64_t)s.M, (uint64_t)A.nbatch,
-                         (uint64_t)A.ld, (uint64_t)A.sbatch, 32, kTcBM);
+                         (uint64_t)A.ld, (uint64_t)A.sbatch, 32, kTcBM, false);
   if (r != EDPC_OK) return r;
   // B: K-major -> [N rows][K inner]; MN-major -> [K rows][N inner]
   if (BMN)
     r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.N, (uint64_t)s.K, (uint64_t)B.nbatch,
-                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, 32);
+                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, 32, true);
   else
     r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.K, (uint64_t)s.N, (uint64_t)B.nbatch,
-                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN);
+                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN, false);
   if (r != EDPC_OK) return r;
   const int nz = s.nzb * (s.kmode == 0 ? 1 : s.nsplit);
   dim3 grid((unsigned)(s.N / BN), (unsigned)cdiv(s.M, kTcBM), (unsigned)nz);
