@@ -41,7 +41,9 @@ def test_predict_and_train_match_oracle(cfg):
         assert abs(lg - lo) < 1e-3 * max(1.0, abs(lo))
     assert worst <= PROB_TOL
     pg = g.parameters_flat().astype(np.float64)
-    assert np.abs(pg - o.value).max() < 2e-3  # a few Adam steps of <= lr each
+    # each Adam step moves a weight by <= ~lr; near-zero gradients may flip
+    # sign between fp32/TF32 and fp64, so the bound is 2 * lr per step
+    assert np.abs(pg - o.value).max() <= 2 * cfg.lr * 6
 
 
 def test_paper_dims_predict_matches_oracle_at_init():

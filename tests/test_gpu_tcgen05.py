@@ -58,13 +58,16 @@ def test_tcgen05_matches_simt(lanes, extra):
             _lib.check(lib.edpc_predict(c.h, ctx.ctypes.data, None))
         errs = {w: _rel(_read(a, w, sizes[w]), _read(b, w, sizes[w])) for w in (5, 2, 3, 6, 4, 8, 1)}
         print("step", step, errs)
+        # step 0 compares identical weights; later steps also carry the
+        # (TF32 vs fp32) difference of the previous updates
+        tol = REL if step == 0 else 4 * REL
         for w, r in errs.items():
-            assert r <= REL, (step, "buffer", w, r, errs)
+            assert r <= tol, (step, "buffer", w, r, errs)
         loss = ctypes.c_float()
         for c in (a, b):
             _lib.check(lib.edpc_train_step(c.h, tg.ctypes.data, ctypes.byref(loss)))
         r = _rel(_read(a, 7, sizes[7]), _read(b, 7, sizes[7]))
-        assert r <= REL, (step, "d(context)", r)
+        assert r <= tol, (step, "d(context)", r)
         ga = _read(a, 0, 8 * a.n_shared).reshape(8, -1).sum(0)
         gb = _read(b, 0, 8 * b.n_shared).reshape(8, -1).sum(0)
         offs = param_offsets(cfg)
@@ -76,7 +79,7 @@ def test_tcgen05_matches_simt(lanes, extra):
             so = o if o < lm else o - fdm
             n = int(np.prod(shape))
             r = _rel(ga[so: so + n], gb[so: so + n])
-            assert r <= REL, (step, name, r)
+            assert r <= tol, (step, name, r)
 
 
 @pytest.mark.parametrize("M,N,K", [(128, 64, 32), (128, 256, 64), (256, 512, 256), (200, 128, 96)])
