@@ -157,26 +157,68 @@ k_ln_bwd(const float* __restrict__ gx0, const float* __restrict__ xhat,
 
 // ------------------------------------------- lane-group column reductions
 
-// partials[g0+zg][off + z*sOff + n] = sum over the group's lanes (ascending)
-// of src[z*sz + b*ld + n] (* mul[b*ld + n] when mul != null): bias and LN
+// partials[g0+zg][off + z*sOff + n] = sum over the group's lanes of
+// src[z*sz + b*ld + n] (* mul[b*ld + n] when mul != null): bias and LN
 // gradients (nn.py:94, :118-119) as 8 fixed lane-group partials.
-__global__ void k_colsum_groups(const float* __restrict__ src, int64_t ld, int64_t sz,
-                                const float* __restrict__ mul, int N, float* __restrict__ partials,
-                                int64_t n_shared, int64_t off, int64_t sOff, int g0, int B_global,
-                                int lane0) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+// Block = one lane group x 128 columns: warp w sums lanes b0+w, b0+w+8, ...
+// (4 columns per thread, float4 when vec), then the 8 warp sums are added in
+// warp order -- a fixed tree, so the result is reproducible.
+__global__ void __launch_bounds__(256)
+k_colsum_groups(const float* __restrict__ src, int64_t ld, int64_t sz,
+                const float* __restrict__ mul, int N, float* __restrict__ partials,
+                int64_t n_shared, int64_t off, int64_t sOff, int g0, int B_global, int lane0,
+                int vec) {
+  __shared__ float4 red[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = blockIdx.x * 128 + lane * 4;
   const int z = blockIdx.y;
   const int gg = g0 + blockIdx.z;
-  if (n >= N) return;
   const int b0 = group_begin(gg, B_global) - lane0, b1 = group_begin(gg + 1, B_global) - lane0;
-  const float* s = src + z * sz + n;
-  float acc = 0.f;
-  if (mul) {
-    for (int b = b0; b < b1; ++b) acc += s[(int64_t)b * ld] * mul[(int64_t)b * ld + n];
-  } else {
-    for (int b = b0; b < b1; ++b) acc += s[(int64_t)b * ld];
+  const float* s = src + z * sz;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (n < N) {
+    for (int b = b0 + warp; b < b1; b += 8) {
+      const float* row = s + (int64_t)b * ld + n;
+      float4 v;
+      if (vec) {
+        v = *reinterpret_cast<const float4*>(row);
+      } else {
+        v.x = row[0];
+        v.y = n + 1 < N ? row[1] : 0.f;
+        v.z = n + 2 < N ? row[2] : 0.f;
+        v.w = n + 3 < N ? row[3] : 0.f;
+      }
+      if (mul) {
+        const float* mr = mul + (int64_t)b * ld + n;
+        float4 q;
+        if (vec) {
+          q = *reinterpret_cast<const float4*>(mr);
+        } else {
+          q.x = mr[0];
+          q.y = n + 1 < N ? mr[1] : 0.f;
+          q.z = n + 2 < N ? mr[2] : 0.f;
+          q.w = n + 3 < N ? mr[3] : 0.f;
+        }
+        v.x *= q.x; v.y *= q.y; v.z *= q.z; v.w *= q.w;
+      }
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
   }
-  partials[(int64_t)gg * n_shared + off + z * sOff + n] = acc;
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && n < N) {
+    float4 t = red[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      const float4 u = red[w][lane];
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
+    float* dst = partials + (int64_t)gg * n_shared + off + z * sOff + n;
+    dst[0] = t.x;
+    if (n + 1 < N) dst[1] = t.y;
+    if (n + 2 < N) dst[2] = t.z;
+    if (n + 3 < N) dst[3] = t.w;
+  }
 }
 
 // ---------------------------------------------------- LTE per-lane matrix
@@ -258,6 +300,102 @@ k_fdm_bwd_adam(const float* __restrict__ down, const float* __restrict__ gmix,
     }
     acc = warp_sum(acc);
     if (lane == 0) gdown[(int64_t)b * FP + i] = acc;
+  }
+}
+
+// ------------------------------------ vectorised FDM kernels (F' = 64/128/256)
+//
+// kTPR threads own one row of U_b (float4 each, kNV per thread); a warp
+// covers 32/kTPR lanes at once.  Row-dot reductions use xor shuffles within
+// the kTPR-thread group (fixed tree -> reproducible).
+
+template <int FP>
+struct FdmGeo {
+  static constexpr int kTPR = FP / 4 < 32 ? FP / 4 : 32;
+  static constexpr int kNV = FP / (4 * kTPR);
+  static constexpr int kLPW = 32 / kTPR;  // lanes (matrices) per warp
+};
+
+template <int FP>
+__global__ void __launch_bounds__(256)
+k_fdm_fwd_v(const float* __restrict__ down, const float* __restrict__ U, float* __restrict__ mixed,
+            int Bl) {
+  using G = FdmGeo<FP>;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int b = warp * G::kLPW + lane / G::kTPR;
+  const int t = lane % G::kTPR;
+  if (b >= Bl) return;
+  const float* d = down + (int64_t)b * FP;
+  const float4* u = reinterpret_cast<const float4*>(U + (int64_t)b * FP * FP);
+  float4 acc[G::kNV];
+#pragma unroll
+  for (int v = 0; v < G::kNV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 8
+  for (int i = 0; i < FP; ++i) {
+    const float di = d[i];
+#pragma unroll
+    for (int v = 0; v < G::kNV; ++v) {
+      const float4 q = u[(i * FP) / 4 + v * G::kTPR + t];
+      acc[v].x = fmaf(di, q.x, acc[v].x);
+      acc[v].y = fmaf(di, q.y, acc[v].y);
+      acc[v].z = fmaf(di, q.z, acc[v].z);
+      acc[v].w = fmaf(di, q.w, acc[v].w);
+    }
+  }
+  float4* out = reinterpret_cast<float4*>(mixed + (int64_t)b * FP);
+#pragma unroll
+  for (int v = 0; v < G::kNV; ++v) out[v * G::kTPR + t] = acc[v];
+}
+
+template <int FP>
+__global__ void __launch_bounds__(256)
+k_fdm_bwd_adam_v(const float* __restrict__ down, const float* __restrict__ gmix,
+                 float* __restrict__ U, float* __restrict__ Um, float* __restrict__ Uv,
+                 float* __restrict__ gdown, int Bl, StepIdx si, AdamConsts c, double b1d,
+                 double b2d) {
+  using G = FdmGeo<FP>;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int b = warp * G::kLPW + lane / G::kTPR;
+  const int t = lane % G::kTPR;
+  const bool live = b < Bl;
+  const int bb = live ? b : 0;
+  float bc1, bc2;
+  adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
+  const float* d = down + (int64_t)bb * FP;
+  const float4* gm4 = reinterpret_cast<const float4*>(gmix + (int64_t)bb * FP);
+  float4 g[G::kNV];
+#pragma unroll
+  for (int v = 0; v < G::kNV; ++v) g[v] = gm4[v * G::kTPR + t];
+  float4* u4 = reinterpret_cast<float4*>(U + (int64_t)bb * FP * FP);
+  float4* m4 = reinterpret_cast<float4*>(Um + (int64_t)bb * FP * FP);
+  float4* v4 = reinterpret_cast<float4*>(Uv + (int64_t)bb * FP * FP);
+#pragma unroll 2
+  for (int i = 0; i < FP; ++i) {
+    const float di = d[i];
+    float part = 0.f;
+#pragma unroll
+    for (int v = 0; v < G::kNV; ++v) {
+      const int e = (i * FP) / 4 + v * G::kTPR + t;
+      float4 w = u4[e], m = m4[e], q = v4[e];
+      part = fmaf(g[v].x, w.x, part);
+      part = fmaf(g[v].y, w.y, part);
+      part = fmaf(g[v].z, w.z, part);
+      part = fmaf(g[v].w, w.w, part);
+      adam_elem(w.x, m.x, q.x, di * g[v].x, c, bc1, bc2);
+      adam_elem(w.y, m.y, q.y, di * g[v].y, c, bc1, bc2);
+      adam_elem(w.z, m.z, q.z, di * g[v].z, c, bc1, bc2);
+      adam_elem(w.w, m.w, q.w, di * g[v].w, c, bc1, bc2);
+      if (live) {
+        u4[e] = w;
+        m4[e] = m;
+        v4[e] = q;
+      }
+    }
+#pragma unroll
+    for (int o = G::kTPR / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    if (live && t == 0) gdown[(int64_t)b * FP + i] = part;
   }
 }
 

@@ -371,10 +371,11 @@ static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, in
 static cudaError_t colsum(edpc_ctx* c, const float* src, int N, int nz, int64_t sz,
                           const float* mul, int64_t off, int64_t sOff) {
   if (c->g_count == 0) return cudaSuccess;
-  dim3 grid((unsigned)cdiv(N, 256), (unsigned)nz, (unsigned)c->g_count);
+  const int vec = (N % 4 == 0 && sz % 4 == 0 && al16(src) && (!mul || al16(mul))) ? 1 : 0;
+  dim3 grid((unsigned)cdiv(N, 128), (unsigned)nz, (unsigned)c->g_count);
   Scope sc(c, kRegColsum, c->st);
   k_colsum_groups<<<grid, 256, 0, c->st>>>(src, N, sz, mul, N, c->Gp, c->lay.n_shared, off, sOff,
-                                           c->g_first, c->lay.B, c->lane0);
+                                           c->g_first, c->lay.B, c->lane0, vec);
   return cudaGetLastError();
 }
 
@@ -453,7 +454,18 @@ static int forward(edpc_ctx* c, ByteCols src) {
                 c->W + L.down_b, nullptr, Bl));
   {
     Scope sc_(c, kRegFdmFwd, c->st);
+    if (L.FP == 64 || L.FP == 128 || L.FP == 256) {
+    const int lpw = 32 / std::min(32, L.FP / 4);
+    const unsigned blocks = (unsigned)cdiv(cdiv(Bl, lpw), 8);
+    if (L.FP == 64)
+      k_fdm_fwd_v<64><<<blocks, 256, 0, c->st>>>(c->down, c->U, c->mixed, Bl);
+    else if (L.FP == 128)
+      k_fdm_fwd_v<128><<<blocks, 256, 0, c->st>>>(c->down, c->U, c->mixed, Bl);
+    else
+      k_fdm_fwd_v<256><<<blocks, 256, 0, c->st>>>(c->down, c->U, c->mixed, Bl);
+  } else {
     k_fdm_fwd<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(c->down, c->U, c->mixed, L.FP, Bl);
+  }
   }
   CK(cudaGetLastError());
   CK(fwd_linear(c, c->mixed, L.FP, L.FP, c->W + L.up_w, L.F, 1, 0, c->x_lte, 0, c->W + L.up_b,
@@ -535,9 +547,26 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   // per-lane FDM: g_down with the old U, then U's Adam step (fused)
   {
     Scope sc_(c, kRegFdmBwd, c->st);
-    k_fdm_bwd_adam<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(
-        c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, FP, Bl, c->si(), c->adam, c->cfg.beta1,
-        c->cfg.beta2);
+    if (FP == 64 || FP == 128 || FP == 256) {
+      const int lpw = 32 / std::min(32, FP / 4);
+      const unsigned blocks = (unsigned)cdiv(cdiv(Bl, lpw), 8);
+      if (FP == 64)
+        k_fdm_bwd_adam_v<64><<<blocks, 256, 0, c->st>>>(c->down, c->gmix, c->U, c->Um, c->Uv,
+                                                        c->gdown, Bl, c->si(), c->adam,
+                                                        c->cfg.beta1, c->cfg.beta2);
+      else if (FP == 128)
+        k_fdm_bwd_adam_v<128><<<blocks, 256, 0, c->st>>>(c->down, c->gmix, c->U, c->Um, c->Uv,
+                                                         c->gdown, Bl, c->si(), c->adam,
+                                                         c->cfg.beta1, c->cfg.beta2);
+      else
+        k_fdm_bwd_adam_v<256><<<blocks, 256, 0, c->st>>>(c->down, c->gmix, c->U, c->Um, c->Uv,
+                                                         c->gdown, Bl, c->si(), c->adam,
+                                                         c->cfg.beta1, c->cfg.beta2);
+    } else {
+      k_fdm_bwd_adam<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(
+          c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, FP, Bl, c->si(), c->adam,
+          c->cfg.beta1, c->cfg.beta2);
+    }
   }
   CK(cudaGetLastError());
   // LTE down
@@ -742,7 +771,7 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
   // embedding-gradient chunks: <= 64 lanes (and <= 4096 context bytes) each,
   // never straddling a lane group
   {
-    const int chunk = std::max(1, std::min(64, 4096 / L.T));
+    const int chunk = std::max(1, std::min(16, 4096 / L.T));
     std::vector<int> tab, grp;
     int k = 0;
     for (int g = c->g_first; g < c->g_first + c->g_count; ++g) {
