@@ -334,6 +334,7 @@ def run_ours(args, wl):
         cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     pk, pk_src = peaks()
+    tc = bool(lib.edpc_has_tcgen05()) and os.environ.get("EDPC_TCGEN05", "1") != "0"
     fl_step = gemm_flops_per_lane(wl["model"]) * B  # per model step (lane column)
     steps_total = K * chunk
     g_ms, g_n = c_regions["gemm"]
@@ -355,19 +356,21 @@ def run_ours(args, wl):
     line = dict(
         metric=METRIC, value=B * chunk * K / (c_ms / 1e3) / 1e6, unit="MB/s", n_gpus=1,
         steps=K, warmup=W, ms_per_step=c_ms / K, higher_is_better=True, scaling="weak",
-        vs_baseline=None, dtype="fp32", data=f"synthetic {wl['kind']}-like (PCG64 seed {wl['seed']},"
+        vs_baseline=None, dtype="tf32" if tc else "fp32", data=f"synthetic {wl['kind']}-like (PCG64 seed {wl['seed']},"
                                               f" sha256 {synth.sha256(data)[:16]})",
         config=dict(workload=wl["desc"], lanes=B, segments=S, columns_per_step=chunk,
                     bytes_per_step=B * chunk, model=wl["model"],
                     l2="no flush: per-step working set ~1 GB > 126 MB L2"),
         decompress_MBps=B * chunk * K / (d_ms / 1e3) / 1e6, lossless_region=lossless,
         region_bits_per_byte=region_bpb, **ratio,
-        roofline=dict(bound="tensor", kernel="per-step GEMMs (SIMT fp32 path)", achieved=achieved,
+        roofline=dict(bound="tensor",
+                      kernel="per-step GEMMs (" + ("tcgen05 kind::tf32" if tc else "SIMT fp32") + ")",
+                      achieved=achieved,
                       peak=peak_t, unit="TFLOP/s", frac=achieved / peak_t, traffic=None,
                       peak_source=f"{pk_src} bf16 dense sustained",
                       flops_per_step=fl_step),
         kernels=kernels, cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches),
-        clocks=clocks, tcgen05=bool(lib.edpc_has_tcgen05()))
+        clocks=clocks, tcgen05=tc)
     print(json.dumps(line), flush=True)
 
 

@@ -177,6 +177,7 @@ k_colsum_groups(const float* __restrict__ src, int64_t ld, int64_t sz,
   const float* s = src + z * sz;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   if (n < N) {
+#pragma unroll 4
     for (int b = b0 + warp; b < b1; b += 8) {
       const float* row = s + (int64_t)b * ld + n;
       float4 v;
@@ -402,14 +403,19 @@ k_fdm_bwd_adam_v(const float* __restrict__ down, const float* __restrict__ gmix,
 // ------------------------------------------------ embedding scatter-add
 
 // Deterministic replacement of np.add.at (model.py:276-278).  Each chunk is
-// <= 64 consecutive lanes of one lane group; thread c owns byte value c and
-// walks the chunk's (lane, position) entries in order.  chunk_tab[k] =
-// {group, local lane begin, local lane end}.
+// <= 16 consecutive lanes of one lane group (<= 4096 context bytes); the
+// chunk's context bytes and gradient rows are staged in shared memory, then
+// thread c (= byte value) walks the (lane, position) entries in order and
+// accumulates the matching rows.  chunk_tab[k] = {group, lane begin, end}.
+constexpr int kEmbChunkLanes = 16;
+constexpr int kEmbSmemFloats = 8192;  // 32 KB of gradient rows per chunk
+
 __global__ void __launch_bounds__(256)
 k_embed_grad_chunks(ByteCols src, StepIdx si, int T, int DE, int F,
                     const float* __restrict__ gx, const int* __restrict__ chunk_tab,
                     float* __restrict__ sub) {
-  __shared__ uint8_t cbytes[64 * 64];
+  __shared__ uint8_t cbytes[4096];
+  __shared__ float grows[kEmbSmemFloats];
   const int k = blockIdx.x;
   const int lb = chunk_tab[3 * k + 1], le = chunk_tab[3 * k + 2];
   const int nl = le - lb;
@@ -417,6 +423,11 @@ k_embed_grad_chunks(ByteCols src, StepIdx si, int T, int DE, int F,
   for (int e = threadIdx.x; e < nl * T; e += blockDim.x) {
     int bl = e / T, p = e - bl * T;
     cbytes[e] = src.base[(int64_t)(lb + bl) * src.ld + col0 + p];
+  }
+  const bool staged = nl * F <= kEmbSmemFloats;
+  if (staged) {
+    const float* g0 = gx + (int64_t)lb * F;
+    for (int e = threadIdx.x; e < nl * F; e += blockDim.x) grows[e] = g0[e];
   }
   __syncthreads();
   const int c = threadIdx.x;
@@ -427,7 +438,8 @@ k_embed_grad_chunks(ByteCols src, StepIdx si, int T, int DE, int F,
     for (int e = 0; e < nl * T; ++e) {
       if (cbytes[e] != c) continue;
       int bl = e / T, p = e - bl * T;
-      const float* g = gx + (int64_t)(lb + bl) * F + p * DE + d0;
+      const float* g = staged ? grows + bl * F + p * DE + d0
+                              : gx + (int64_t)(lb + bl) * F + p * DE + d0;
 #pragma unroll
       for (int d = 0; d < 16; ++d)
         if (d0 + d < DE) acc[d] += g[d];
@@ -679,6 +691,42 @@ __global__ void k_decode_column(uint8_t* __restrict__ mat, int64_t L, StepIdx si
     stp[2] = (int64_t)st.code;
     stp[3] = st.bitpos;
   }
+}
+
+// Split-K epilogue: tile partial of K chunk zg into the workspace.
+struct EpiSplit {
+  float* ws;
+  int64_t ld, plane;
+  __device__ void operator()(int, int zg, int m, int n, float acc) const {
+    ws[zg * plane + (int64_t)m * ld + n] = acc;
+  }
+  __device__ void row32(int, int zg, int m, int n0, float (&v)[32]) const {
+    store32(ws + zg * plane + (int64_t)m * ld + n0, v);
+  }
+};
+
+// out = ((ws0 + ws1) + ws2) + ... (fixed order) then (+ bias) (+ resid):
+// the reduction of a split-K GEMM, fused with its bias/residual epilogue.
+__global__ void k_splitk_reduce(const float* __restrict__ ws, int nsplit, int64_t plane, int N,
+                                const float* __restrict__ bias, const float* __restrict__ resid,
+                                float* __restrict__ out) {
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (e >= plane) return;
+  float4 a = *reinterpret_cast<const float4*>(ws + e);
+  for (int s = 1; s < nsplit; ++s) {
+    const float4 b = *reinterpret_cast<const float4*>(ws + s * plane + e);
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+  }
+  const int n = (int)(e % N);
+  if (bias) {
+    const float4 b = *reinterpret_cast<const float4*>(bias + n);
+    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+  }
+  if (resid) {
+    const float4 r = *reinterpret_cast<const float4*>(resid + e);
+    a.x += r.x; a.y += r.y; a.z += r.z; a.w += r.w;
+  }
+  *reinterpret_cast<float4*>(out + e) = a;
 }
 
 __global__ void k_step_advance(int64_t* i, int64_t* t) {

@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <algorithm>
 #include <initializer_list>
+#include <type_traits>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -187,6 +188,7 @@ struct edpc_ctx {
   float *logits, *probs, *nll;
   // backward temporaries
   float *gl, *gA, *gB, *GH, *gx0, *gmix, *gdown, *emb_sub;
+  float* ws = nullptr;  // split-K workspace [kSplitK][Bl][<=256]
   int *chunk_tab = nullptr, *grp_chunks = nullptr;
   int n_chunks = 0;
   // coder
@@ -308,18 +310,44 @@ static bool tc_ok(edpc_ctx* c, int N, int Kchunk, std::initializer_list<const vo
 
 static cudaError_t as_cuda(int st) { return st == EDPC_OK ? cudaSuccess : cudaErrorUnknown; }
 
+// Skinny-N GEMMs (N <= 256, long K) give only Bl/128 output tiles; split K
+// kSplitK ways so the grid covers the SMs, then reduce in a fixed order.
+constexpr int kSplitK = 4;
+static bool use_split(int N, int64_t Ktot, int Kd) {
+  return N <= 256 && N % 4 == 0 && Ktot >= 1024 && Kd % (kSplitK * kTcBK) == 0;
+}
+
+static cudaError_t splitk_reduce(edpc_ctx* c, int N, const float* bias, const float* resid,
+                                 float* out) {
+  const int64_t plane = (int64_t)c->Bl * N;
+  Scope sc(c, kRegElem, c->st);
+  k_splitk_reduce<<<(unsigned)cdiv(plane / 4, 256), 256, 0, c->st>>>(c->ws, kSplitK, plane, N, bias,
+                                                                    resid, out);
+  return cudaGetLastError();
+}
+
 // out[Bl][N] = A[Bl][Kd] . W[Kd][N] (+ bias) over nzb batches (weights at
 // w + z*sW, bias at bias + z*sW, out at out + z*sOut)
 static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, const float* w,
                               int N, int nzb, int64_t sW, float* out, int64_t sOut,
                               const float* bias, const float* resid, int M) {
-  Scope sc(c, kRegGemm, c->st);
   if (tc_ok(c, N, Kd, {A, w, out, bias, resid ? resid : out}, {lda, N, sW, sOut})) {
-    TcShape s{M, N, Kd, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 0, 1, 0, 0, 0};
     TcOperand a{A, lda, 0, 1}, b{w, N, sW, nzb};
+    if (nzb == 1 && M == c->Bl && use_split(N, Kd, Kd)) {
+      TcShape s{M, N, Kd, 1, 1, kBatchNone, kBatchNone, 2, kSplitK, 0, 0, 0};
+      {
+        Scope sc(c, kRegGemm, c->st);
+        int st = tc_gemm<false, true>(s, a, b, EpiSplit{c->ws, N, (int64_t)M * N}, c->st);
+        if (st != EDPC_OK) return cudaErrorUnknown;
+      }
+      return splitk_reduce(c, N, bias, resid, out);
+    }
+    Scope sc(c, kRegGemm, c->st);
+    TcShape s{M, N, Kd, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 0, 1, 0, 0, 0};
     if (resid) return as_cuda(tc_gemm<false, true>(s, a, b, EpiBiasResid{out, N, bias, resid, N}, c->st));
     return as_cuda(tc_gemm<false, true>(s, a, b, EpiBias{out, N, sOut, bias, sW}, c->st));
   }
+  Scope sc(c, kRegGemm, c->st);
   GemmShape g{};
   g.M = M;
   g.N = N;
@@ -383,13 +411,26 @@ static cudaError_t colsum(edpc_ctx* c, const float* src, int N, int nz, int64_t 
 template <class Epi>
 static cudaError_t dgrad(edpc_ctx* c, const float* G, int Kd, int nsum, int64_t sG_sum,
                          const float* w, int64_t sW_sum, int N, const Epi& epi) {
-  Scope sc(c, kRegGemm, c->st);
   if (tc_ok(c, N, Kd, {G, w}, {Kd, sG_sum, sW_sum})) {
+    TcOperand a{G, Kd, sG_sum, nsum}, b{w, Kd, sW_sum, nsum};
+    if constexpr (std::is_same<Epi, EpiStore>::value) {
+      if (epi.ldc == N && use_split(N, (int64_t)Kd * nsum, Kd)) {
+        TcShape s{c->Bl, N, Kd, 1, nsum, nsum > 1 ? kBatchSum : kBatchNone,
+                  nsum > 1 ? kBatchSum : kBatchNone, 2, kSplitK, 0, 0, 0};
+        {
+          Scope sc(c, kRegGemm, c->st);
+          int st = tc_gemm<false, false>(s, a, b, EpiSplit{c->ws, N, (int64_t)c->Bl * N}, c->st);
+          if (st != EDPC_OK) return cudaErrorUnknown;
+        }
+        return splitk_reduce(c, N, nullptr, nullptr, epi.C);
+      }
+    }
+    Scope sc(c, kRegGemm, c->st);
     TcShape s{c->Bl, N, Kd, 1, nsum, nsum > 1 ? kBatchSum : kBatchNone,
               nsum > 1 ? kBatchSum : kBatchNone, 0, 1, 0, 0, 0};
-    TcOperand a{G, Kd, sG_sum, nsum}, b{w, Kd, sW_sum, nsum};
     return as_cuda(tc_gemm<false, false>(s, a, b, epi, c->st));
   }
+  Scope sc(c, kRegGemm, c->st);
   GemmShape g{};
   g.M = c->Bl;
   g.N = N;
@@ -768,10 +809,11 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
   A_(c->gx0, Bl * F);
   A_(c->gmix, Bl * FP);
   A_(c->gdown, Bl * FP);
+  A_(c->ws, (int64_t)kSplitK * Bl * 256);
   // embedding-gradient chunks: <= 64 lanes (and <= 4096 context bytes) each,
   // never straddling a lane group
   {
-    const int chunk = std::max(1, std::min(16, 4096 / L.T));
+    const int chunk = std::max(1, std::min(kEmbChunkLanes, 4096 / L.T));
     std::vector<int> tab, grp;
     int k = 0;
     for (int g = c->g_first; g < c->g_first + c->g_count; ++g) {

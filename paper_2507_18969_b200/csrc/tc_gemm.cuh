@@ -8,7 +8,8 @@
 //               kStages-deep shared-memory ring (mbarrier full/empty pairs)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (4 MMAs of
 //               K=8 per 32-wide K block); tcgen05.commit frees ring slots
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> registers -> fused
+//   warps 2..9  epilogue (two warps per TMEM lane quadrant, alternating
+//               32-column chunks): tcgen05.ld 32x32b.x32 -> registers -> fused
 //               epilogue functor (bias, residual, GeLU/product-rule backward,
 //               lane-group weight-gradient partials) -> global
 // Operands may be K-major or MN-major (the instruction descriptor's
@@ -172,8 +173,10 @@ struct TcSmem {
   static constexpr int kBytes = kTcStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+constexpr int kTcThreads = 320;
+
 template <int BN, bool AMN, bool BMN, class Epi>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(kTcThreads, 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
           TcShape s, Epi epi) {
   extern __shared__ uint8_t smem_raw[];
@@ -279,15 +282,16 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       tc_commit(accum);
     }
   } else {
-    // ---------------- epilogue warps 2..5 (TMEM lane quadrant = warp % 4)
+    // ---------------- epilogue warps 2..9 (TMEM lane quadrant = warp % 4)
     const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int m = m0 + quad * 32 + lane;
     if (total > 0) {
       mbar_wait(accum, 0);
       tc_fence_after();
     }
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = half * 32; c < BN; c += 64) {
       float v[32];
       if (s.dbg == 1) {
 #pragma unroll
@@ -415,7 +419,7 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<BN>::kBytes);
     attr_done[dev] = true;
   }
-  kern<<<grid, 192, TcSmem<BN>::kBytes, st>>>(ta, tb, s, epi);
+  kern<<<grid, kTcThreads, TcSmem<BN>::kBytes, st>>>(ta, tb, s, epi);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_tc_gemm launch: ") + cudaGetErrorString(e));
