@@ -173,6 +173,7 @@ struct edpc_ctx {
   cudaStream_t st = nullptr, st_enc = nullptr;
   cudaEvent_t ev = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr, tj = nullptr;
+  cudaGraphExec_t graph[2] = {nullptr, nullptr};
   AdamConsts adam{};
 
   std::vector<void*> allocs;
@@ -212,6 +213,8 @@ struct edpc_ctx {
     if (st_enc) cudaStreamSynchronize(st_enc);
     prof.flush();
     prof.release();
+    for (auto& g : graph)
+      if (g) cudaGraphExecDestroy(g);
     for (void* p : allocs) cudaFree(p);
     if (ev) cudaEventDestroy(ev);
     if (t0) cudaEventDestroy(t0);
@@ -669,6 +672,48 @@ static int model_step(edpc_ctx* c, int mode) {
   return EDPC_OK;
 }
 
+// CUDA graphs: kGraphSteps consecutive model steps are captured once per
+// mode and replayed; the step index lives in device memory (d_i / d_t) and is
+// advanced by the last kernel of each step, so replays need no host input.
+constexpr int kGraphSteps = 8;
+
+static bool graphs_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EDPC_GRAPHS");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static int run_model_steps(edpc_ctx* c, int64_t n, int mode) {
+  const bool use_graph = graphs_enabled() && !c->prof.on && !sync_debug();
+  if (use_graph && n >= kGraphSteps) {
+    cudaGraphExec_t& ge = c->graph[mode == kDecode ? 1 : 0];
+    if (!ge) {
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
+      int st = EDPC_OK;
+      for (int k = 0; k < kGraphSteps && st == EDPC_OK; ++k) st = model_step(c, mode);
+      cudaError_t e = cudaStreamEndCapture(c->st, &g);
+      if (st != EDPC_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+      }
+      CK(e);
+      e = cudaGraphInstantiate(&ge, g, 0);
+      cudaGraphDestroy(g);
+      CK(e);
+    }
+    while (n >= kGraphSteps) {
+      CK(cudaGraphLaunch(ge, c->st));
+      n -= kGraphSteps;
+    }
+  }
+  for (; n > 0; --n) EDPC_TRY(model_step(c, mode));
+  return EDPC_OK;
+}
+
 static int set_step(edpc_ctx* c, int64_t i, int64_t t) {
   int64_t h[2] = {i, t};
   CK(cudaMemcpyAsync(c->d_i, &h[0], 8, cudaMemcpyHostToDevice, c->st));
@@ -1012,7 +1057,7 @@ int edpc_compress_steps(edpc_ctx* c, int64_t i0, int64_t i1) {
   const int64_t s0 = std::max<int64_t>(i0, T);
   if (s0 < i1) {
     EDPC_TRY(set_step(c, s0, s0 - T + 1));
-    for (int64_t i = s0; i < i1; ++i) EDPC_TRY(model_step(c, kEncode));
+    EDPC_TRY(run_model_steps(c, i1 - s0, kEncode));
   }
   // DPCA: hand the finished columns to the encoder stream
   c->cols_done = std::max(c->cols_done, i1);
@@ -1111,7 +1156,7 @@ int edpc_decompress_steps(edpc_ctx* c, int64_t i0, int64_t i1) {
   const int64_t s0 = std::max<int64_t>(i0, T);
   if (s0 < i1) {
     EDPC_TRY(set_step(c, s0, s0 - T + 1));
-    for (int64_t i = s0; i < i1; ++i) EDPC_TRY(model_step(c, kDecode));
+    EDPC_TRY(run_model_steps(c, i1 - s0, kDecode));
   }
   return EDPC_OK;
 }
