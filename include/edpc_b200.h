@@ -113,6 +113,8 @@ int edpc_set_input(edpc_ctx* ctx, const uint8_t* data, int64_t n, int on_device)
  * done column-block by column-block so H2D overlaps the model steps */
 int edpc_set_input_columns(edpc_ctx* ctx, const uint8_t* stream, int64_t n, int64_t col0,
                            int64_t col1);
+/* the local lanes' bytes only ([lane_count][L] row-major, zero padded past nbytes) */
+int edpc_set_input_local(edpc_ctx* ctx, const uint8_t* lanes, int64_t nbytes);
 /* coded intervals (cum_lo | freq << 16) of lane columns [col0, col1), [col][lane] */
 int edpc_get_intervals(edpc_ctx* ctx, int64_t col0, int64_t col1, uint32_t* out);
 /* lane-matrix columns [col0, col1) as [lane][col] (decoded bytes on the decode side) */
@@ -145,6 +147,19 @@ int edpc_last_probs(edpc_ctx* ctx, float* probs);
  * tree reduction + Adam).  edpc_grad_partials exposes the device buffer. */
 int edpc_step_phase(edpc_ctx* ctx, int64_t i, int32_t phase, int32_t decompress);
 int edpc_grad_partials(edpc_ctx* ctx, float** dev_ptr, int64_t* n_shared);
+/* this context's lane groups [g_first, g_first + g_count) */
+int edpc_ctx_groups(edpc_ctx* ctx, int32_t* g_first, int32_t* g_count);
+/* host copy of lane-group partials [g0, g0+ng) x n_shared (to_device 0: read) */
+int edpc_partials_copy(edpc_ctx* ctx, int32_t g0, int32_t ng, float* host, int32_t to_device);
+/* single-process multi-context exchange: dst <- src's own groups (peer copy) */
+int edpc_partials_pull(edpc_ctx* dst, edpc_ctx* src);
+/* hand produced columns [.., upto) to the encoder stream (phase-driven compress) */
+int edpc_encode_pending(edpc_ctx* ctx, int64_t upto);
+/* NCCL: rank 0 makes an id (128 bytes), every rank joins concurrently; after
+ * that each model step all-gathers the partials in place over NVLink inside
+ * the step (and inside its CUDA graph) -- multi-process, one GPU per rank. */
+int edpc_nccl_unique_id(uint8_t* out, int32_t cap);
+int edpc_ctx_set_comm(edpc_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t rank);
 
 int edpc_sync(edpc_ctx* ctx);
 

@@ -65,6 +65,7 @@ _SIGS = {
     "edpc_get_params": ([_P, _P, _I64], ctypes.c_int),
     "edpc_set_input": ([_P, _P, _I64, ctypes.c_int], ctypes.c_int),
     "edpc_set_input_columns": ([_P, _P, _I64, _I64, _I64], ctypes.c_int),
+    "edpc_set_input_local": ([_P, _P, _I64], ctypes.c_int),
     "edpc_get_intervals": ([_P, _I64, _I64, _P], ctypes.c_int),
     "edpc_get_columns": ([_P, _I64, _I64, _P], ctypes.c_int),
     "edpc_compress_steps": ([_P, _I64, _I64], ctypes.c_int),
@@ -78,6 +79,12 @@ _SIGS = {
     "edpc_last_probs": ([_P, _P], ctypes.c_int),
     "edpc_step_phase": ([_P, _I64, _I32, _I32], ctypes.c_int),
     "edpc_grad_partials": ([_P, _P, _P], ctypes.c_int),
+    "edpc_ctx_groups": ([_P, _P, _P], ctypes.c_int),
+    "edpc_partials_copy": ([_P, _I32, _I32, _P, _I32], ctypes.c_int),
+    "edpc_encode_pending": ([_P, _I64], ctypes.c_int),
+    "edpc_partials_pull": ([_P, _P], ctypes.c_int),
+    "edpc_nccl_unique_id": ([_P, _I32], ctypes.c_int),
+    "edpc_ctx_set_comm": ([_P, _P, _I32, _I32], ctypes.c_int),
     "edpc_sync": ([_P], ctypes.c_int),
     "edpc_debug_read": ([_P, _I32, _P, _I64], ctypes.c_int),
     "edpc_debug_gemm": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _I32], ctypes.c_int),

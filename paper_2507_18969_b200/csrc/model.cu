@@ -8,6 +8,7 @@
 #include <stdint.h>
 
 #include <cstdio>
+#include <cstring>
 #include <cstdlib>
 #include <algorithm>
 #include <initializer_list>
@@ -15,6 +16,8 @@
 #include <cmath>
 #include <string>
 #include <vector>
+
+#include <nccl.h>
 
 #include "common.cuh"
 #include "gemm_simt.cuh"
@@ -174,6 +177,8 @@ struct edpc_ctx {
   cudaEvent_t ev = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr, tj = nullptr;
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
+  ncclComm_t comm = nullptr;  // multi-GPU: all-gather of the lane-group gradient partials
+  int nranks = 1, rank = 0;
   AdamConsts adam{};
 
   std::vector<void*> allocs;
@@ -215,6 +220,7 @@ struct edpc_ctx {
     prof.release();
     for (auto& g : graph)
       if (g) cudaGraphExecDestroy(g);
+    if (comm) ncclCommDestroy(comm);
     for (void* p : allocs) cudaFree(p);
     if (ev) cudaEventDestroy(ev);
     if (t0) cudaEventDestroy(t0);
@@ -650,6 +656,20 @@ static int adam_shared(edpc_ctx* c) {
   return EDPC_OK;
 }
 
+// Multi-GPU: every rank holds 8/G consecutive lane groups, so the partial
+// buffer [8][n_shared] is exactly an in-place all-gather of equal slices.
+static int exchange_partials(edpc_ctx* c) {
+  if (!c->comm || c->nranks < 2) return EDPC_OK;
+  const size_t cnt = (size_t)c->g_count * c->lay.n_shared;
+  ncclResult_t r = ncclAllGather(c->Gp + (size_t)c->g_first * c->lay.n_shared, c->Gp, cnt,
+                                 ncclFloat, c->comm, c->st);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    return EDPC_ERR_CUDA;
+  }
+  return EDPC_OK;
+}
+
 // One model step at lane column i (already in d_i / d_t).
 static int model_step(edpc_ctx* c, int mode) {
   ByteCols src = c->lanes_src();
@@ -663,6 +683,7 @@ static int model_step(edpc_ctx* c, int mode) {
     CK(cudaGetLastError());
   }
   EDPC_TRY(backward(c, src, nullptr));
+  EDPC_TRY(exchange_partials(c));
   EDPC_TRY(adam_shared(c));
   {
     Scope sc_(c, kRegElem, c->st);
@@ -1015,6 +1036,17 @@ int edpc_set_input_columns(edpc_ctx* c, const uint8_t* stream, int64_t n, int64_
   return EDPC_OK;
 }
 
+int edpc_set_input_local(edpc_ctx* c, const uint8_t* lanes, int64_t nbytes) {
+  EDPC_CHECK_ARG(c && (lanes || nbytes == 0), "null argument");
+  const int64_t want = (int64_t)c->Bl * c->L;
+  EDPC_CHECK_ARG(nbytes >= 0 && nbytes <= want, "more bytes than the local lanes hold");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  if (want > nbytes) EDPC_CUDA_TRY(cudaMemsetAsync(c->mat + nbytes, 0, want - nbytes, c->st));
+  if (nbytes) EDPC_CUDA_TRY(cudaMemcpyAsync(c->mat, lanes, nbytes, cudaMemcpyHostToDevice, c->st));
+  c->have_input = true;
+  return EDPC_OK;
+}
+
 int edpc_get_intervals(edpc_ctx* c, int64_t col0, int64_t col1, uint32_t* out) {
   EDPC_CHECK_ARG(c && out, "null argument");
   EDPC_CHECK_ARG(0 <= col0 && col0 <= col1 && col1 <= c->L, "bad column range");
@@ -1242,10 +1274,103 @@ int edpc_step_phase(edpc_ctx* c, int64_t i, int32_t phase, int32_t decompress) {
       EDPC_CUDA_TRY(cudaGetLastError());
     }
     EDPC_TRY(backward(c, src, nullptr));
+    if (!decompress) c->cols_done = std::max(c->cols_done, i + 1);
     return EDPC_OK;
   }
   EDPC_CHECK_ARG(phase == 1, "phase must be 0 or 1");
+  EDPC_TRY(exchange_partials(c));
   EDPC_TRY(adam_shared(c));
+  return EDPC_OK;
+}
+
+int edpc_encode_pending(edpc_ctx* c, int64_t upto) {
+  EDPC_CHECK_ARG(c, "null ctx");
+  EDPC_CHECK_ARG(upto <= c->cols_done, "columns not produced yet");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  return launch_encoder(c, upto);
+}
+
+int edpc_partials_copy(edpc_ctx* c, int32_t g0, int32_t ng, float* host, int32_t to_device) {
+  EDPC_CHECK_ARG(c && host && g0 >= 0 && ng >= 0 && g0 + ng <= kNumGroups, "bad arguments");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  float* dev = c->Gp + (size_t)g0 * c->lay.n_shared;
+  const size_t bytes = (size_t)ng * c->lay.n_shared * 4;
+  if (to_device)
+    EDPC_CUDA_TRY(cudaMemcpyAsync(dev, host, bytes, cudaMemcpyHostToDevice, c->st));
+  else
+    EDPC_CUDA_TRY(cudaMemcpyAsync(host, dev, bytes, cudaMemcpyDeviceToHost, c->st));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  return EDPC_OK;
+}
+
+// dst <- src's own lane-group partials, device to device (peer copy over
+// NVLink when the contexts sit on different GPUs).  Ordered after src's
+// queued work; src's later work is ordered after the copy.
+int edpc_partials_pull(edpc_ctx* dst, edpc_ctx* src) {
+  EDPC_CHECK_ARG(dst && src && dst->lay.n_shared == src->lay.n_shared, "bad contexts");
+  if (src->g_count == 0) return EDPC_OK;
+  EDPC_CUDA_TRY(cudaSetDevice(src->device));
+  EDPC_CUDA_TRY(cudaEventRecord(src->ev, src->st));
+  EDPC_CUDA_TRY(cudaSetDevice(dst->device));
+  EDPC_CUDA_TRY(cudaStreamWaitEvent(dst->st, src->ev, 0));
+  const size_t off = (size_t)src->g_first * src->lay.n_shared;
+  const size_t bytes = (size_t)src->g_count * src->lay.n_shared * 4;
+  EDPC_CUDA_TRY(cudaMemcpyPeerAsync(dst->Gp + off, dst->device, src->Gp + off, src->device, bytes,
+                                    dst->st));
+  EDPC_CUDA_TRY(cudaEventRecord(dst->ev, dst->st));
+  EDPC_CUDA_TRY(cudaSetDevice(src->device));
+  EDPC_CUDA_TRY(cudaStreamWaitEvent(src->st, dst->ev, 0));
+  return EDPC_OK;
+}
+
+int edpc_ctx_groups(edpc_ctx* c, int32_t* g_first, int32_t* g_count) {
+  EDPC_CHECK_ARG(c && g_first && g_count, "null argument");
+  *g_first = c->g_first;
+  *g_count = c->g_count;
+  return EDPC_OK;
+}
+
+int edpc_nccl_unique_id(uint8_t* out, int32_t cap) {
+  EDPC_CHECK_ARG(out && cap >= (int32_t)sizeof(ncclUniqueId), "buffer too small");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    return EDPC_ERR_CUDA;
+  }
+  memcpy(out, &id, sizeof(id));
+  return EDPC_OK;
+}
+
+// Joins the context to an NCCL communicator (collective: every rank calls it
+// concurrently with the same id).  Requires whole, equal lane-group shares.
+int edpc_ctx_set_comm(edpc_ctx* c, const uint8_t* id, int32_t nranks, int32_t rank) {
+  EDPC_CHECK_ARG(c && id, "null argument");
+  EDPC_CHECK_ARG(nranks >= 1 && rank >= 0 && rank < nranks, "bad rank");
+  EDPC_CHECK_ARG(kNumGroups % nranks == 0 && c->lay.B % kNumGroups == 0,
+                 "multi-GPU needs lanes % 8 == 0 and a GPU count dividing 8");
+  EDPC_CHECK_ARG(c->g_count == kNumGroups / nranks && c->g_first == rank * c->g_count &&
+                     c->lane0 == group_begin(c->g_first, c->lay.B) &&
+                     c->Bl == group_begin(c->g_first + c->g_count, c->lay.B) - c->lane0,
+                 "rank must own lane groups [rank*8/G, (rank+1)*8/G) exactly");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  ncclUniqueId uid;
+  memcpy(&uid, id, sizeof(uid));
+  ncclComm_t comm;
+  ncclResult_t r = ncclCommInitRank(&comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+    return EDPC_ERR_CUDA;
+  }
+  if (c->comm) ncclCommDestroy(c->comm);
+  c->comm = comm;
+  c->nranks = nranks;
+  c->rank = rank;
+  for (auto& g : c->graph)  // captured steps must include the collective
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
   return EDPC_OK;
 }
 

@@ -321,6 +321,26 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
 
 // ------------------------------------------------------- host: tensor maps
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point, so the
+// library does not link libcuda (it must load on CPU-only hosts).
+typedef CUresult (*PfnEncodeTiled)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline PfnEncodeTiled encode_tiled_fn() {
+  static PfnEncodeTiled fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PfnEncodeTiled>(p);
+  }
+  return fn;
+}
+
 // 3-D fp32 tensor map: dims {inner, rows, batch}; strides in elements.
 inline int make_tmap(CUtensorMap* map, const float* base, uint64_t inner, uint64_t rows,
                      uint64_t batch, uint64_t row_stride, uint64_t batch_stride, uint32_t box_inner,
@@ -329,16 +349,19 @@ inline int make_tmap(CUtensorMap* map, const float* base, uint64_t inner, uint64
   cuuint64_t strides[2] = {row_stride * 4, (batch_stride ? batch_stride : row_stride * rows) * 4};
   cuuint32_t box[3] = {box_inner, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = cuTensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims,
+  PfnEncodeTiled enc = encode_tiled_fn();
+  if (!enc) {
+    set_error("cuTensorMapEncodeTiled entry point unavailable");
+    return EDPC_ERR_CUDA;
+  }
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims,
                                       strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                       mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
                                                : CU_TENSOR_MAP_SWIZZLE_128B,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
-    const char* s = nullptr;
-    cuGetErrorString(r, &s);
-    set_error(std::string("cuTensorMapEncodeTiled: ") + (s ? s : "?"));
+    set_error("cuTensorMapEncodeTiled failed with CUresult " + std::to_string((int)r));
     return EDPC_ERR_CUDA;
   }
   return EDPC_OK;

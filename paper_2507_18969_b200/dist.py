@@ -1,0 +1,278 @@
+"""Lane sharding of one container across GPUs.
+
+Reference facts this follows: one model shared by all lanes and segments and
+updated every step from the mean loss over all B lanes (`pipeline.py:136,196`,
+`nn.py:206-209`, `model.py:265-281`); lanes are otherwise independent and
+segments are contiguous lane ranges with their own coders (`pipeline.py:66-68`).
+
+Partition: G ranks (G | 8, B % 8 == 0); rank r owns lanes [r*B/G, (r+1)*B/G)
+= the 8/G consecutive lane groups of the canonical gradient reduction and the
+segments inside them, their per-lane FDM state, coders and lane-matrix slice.
+Per model step each rank computes its groups' gradient partials; the
+partials are exchanged (NCCL all-gather inside the library for one process per
+GPU; device-to-device peer copies for several contexts in one process); then
+every rank runs the same canonical tree + Adam on identical inputs, so the
+trajectory -- and the container bytes -- are those of a single GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import time
+
+import numpy as np
+
+from . import _lib
+from .config import ModelConfig
+from .container import EdpcContainer, Header
+from .coder import CoderError
+from .init import init_params_f32
+from .lanes import lane_len_for, validate_geometry
+from .model import DeviceContext
+
+NUM_GROUPS = 8
+
+
+def lane_plan(cfg: ModelConfig, segments: int, world: int) -> list[tuple[int, int]]:
+    """[(lane_begin, lane_count)] per rank; raises ValueError if the geometry
+    cannot be split on lane-group and segment boundaries."""
+    validate_geometry(cfg, segments)
+    B = cfg.lanes
+    if world < 1 or NUM_GROUPS % world:
+        raise ValueError(f"GPU count {world} must divide {NUM_GROUPS}")
+    if world == 1:
+        return [(0, B)]
+    if B % NUM_GROUPS:
+        raise ValueError(f"multi-GPU needs lanes ({B}) divisible by {NUM_GROUPS}")
+    per = B // world
+    spl = B // segments
+    if per % spl:
+        raise ValueError(f"segments of {spl} lanes straddle the {per}-lane GPU shares")
+    return [(r * per, per) for r in range(world)]
+
+
+def assemble(cfg: ModelConfig, n: int, shards: list[tuple[list[int], list[bytes]]]) -> EdpcContainer:
+    """Container from per-rank (bit_lengths, payloads), rank order = segment order."""
+    bits, pays = [], []
+    for b, p in shards:
+        bits += list(b)
+        pays += list(p)
+    return EdpcContainer(header=Header.from_config(cfg, n, bits), segments=pays)
+
+
+def _split_payloads(bits, buf):
+    out, pos = [], 0
+    for b in bits:
+        nb = (int(b) + 7) // 8
+        out.append(bytes(buf[pos: pos + nb]))
+        pos += nb
+    return out
+
+
+# ------------------------------------------------ single process, G contexts
+
+class ShardSet:
+    """G contexts (one per device in ``devices``; devices may repeat, e.g. to
+    exercise the sharded path on one GPU) driven by one host thread."""
+
+    def __init__(self, cfg: ModelConfig, segments: int, n: int, devices: list[int]):
+        self.cfg = cfg
+        self.plan = lane_plan(cfg, segments, len(devices))
+        self.ctxs = [DeviceContext(cfg, segments, n, d, lb, lc)
+                     for d, (lb, lc) in zip(devices, self.plan)]
+        params = init_params_f32(cfg)
+        for c in self.ctxs:
+            c.load_flat(params)
+        self.lib = _lib.load()
+
+    def close(self):
+        for c in self.ctxs:
+            c.close()
+
+    def step(self, i: int, decompress: bool) -> None:
+        lib = self.lib
+        for c in self.ctxs:
+            _lib.check(lib.edpc_step_phase(c.h, i, 0, int(decompress)))
+        for dst in self.ctxs:
+            for src in self.ctxs:
+                if src is not dst:
+                    _lib.check(lib.edpc_partials_pull(dst.h, src.h))
+        for c in self.ctxs:
+            _lib.check(lib.edpc_step_phase(c.h, i, 1, int(decompress)))
+
+
+def compress_multi(data: bytes, cfg: ModelConfig, segments: int, devices: list[int], *,
+                   stats: dict | None = None) -> EdpcContainer:
+    t0 = time.perf_counter()
+    n = len(data)
+    if n == 0:
+        return EdpcContainer(header=Header.from_config(cfg, 0, []), segments=[])
+    for d in set(devices):
+        _lib.require_device(d)
+    ss = ShardSet(cfg, segments, n, list(devices))
+    lib = ss.lib
+    try:
+        buf = np.frombuffer(bytes(data), dtype=np.uint8)
+        T = cfg.context_len
+        L = ss.ctxs[0].lane_len
+        for c in ss.ctxs:
+            _lib.check(lib.edpc_set_input(c.h, buf.ctypes.data, n, 0))
+            _lib.check(lib.edpc_compress_steps(c.h, 0, min(T, L)))
+        for i in range(T, L):
+            ss.step(i, False)
+            if (i + 1) % 256 == 0 or i + 1 == L:
+                for c in ss.ctxs:
+                    _lib.check(lib.edpc_encode_pending(c.h, i + 1))
+        shards = []
+        for c in ss.ctxs:
+            sl = c.lane_count // (cfg.lanes // segments)
+            bits = np.zeros(sl, dtype=np.int64)
+            tot = ctypes.c_int64()
+            _lib.check(lib.edpc_compress_finish(c.h, bits.ctypes.data, ctypes.byref(tot)))
+            pay = np.zeros(max(tot.value, 1), dtype=np.uint8)
+            _lib.check(lib.edpc_get_payloads(c.h, pay.ctypes.data, pay.size))
+            shards.append((bits.tolist(), _split_payloads(bits, pay)))
+    finally:
+        ss.close()
+    if stats is not None:
+        stats.update(steps=max(0, L - T), predict_s=0.0, train_s=0.0, encode_s=0.0,
+                     wall_s=time.perf_counter() - t0, peak_queue_depth=0, devices=list(devices))
+    return assemble(cfg, n, shards)
+
+
+def decompress_multi(container: EdpcContainer, devices: list[int], *,
+                     stats: dict | None = None) -> bytes:
+    t0 = time.perf_counter()
+    h = container.header
+    cfg = h.model_config()
+    n = h.original_len
+    segments = h.segment_count
+    for d in set(devices):
+        _lib.require_device(d)
+    ss = ShardSet(cfg, segments, n, list(devices))
+    lib = ss.lib
+    try:
+        spl = cfg.lanes // segments
+        T = cfg.context_len
+        L = ss.ctxs[0].lane_len
+        for c, (lb, lc) in zip(ss.ctxs, ss.plan):
+            s0, s1 = lb // spl, (lb + lc) // spl
+            pays = b"".join(container.segments[s0:s1]) or b"\0"
+            bits = np.ascontiguousarray(h.bit_lengths[s0:s1], dtype=np.int64)
+            pb = np.frombuffer(pays, dtype=np.uint8)
+            _lib.check(lib.edpc_set_payloads(c.h, pb.ctypes.data, bits.ctypes.data))
+            _lib.check(lib.edpc_decompress_steps(c.h, 0, min(T, L)))
+        for i in range(T, L):
+            ss.step(i, True)
+        parts = []
+        for c in ss.ctxs:
+            out = np.empty(c.lane_count * L, dtype=np.uint8)
+            st = lib.edpc_get_output(c.h, out.ctypes.data, out.size)
+            if st == _lib.ERR_CODER:
+                raise CoderError(lib.edpc_last_error().decode())
+            _lib.check(st)
+            parts.append(out)
+    finally:
+        ss.close()
+    if stats is not None:
+        stats.update(steps=max(0, L - T), wall_s=time.perf_counter() - t0, devices=list(devices))
+    return np.concatenate(parts)[:n].tobytes()
+
+
+# ------------------------------------------- one process per GPU (torchrun)
+
+def nccl_join(ctx: DeviceContext, rank: int, world: int, broadcast_id) -> None:
+    """Joins ``ctx`` to an NCCL communicator; ``broadcast_id(bytes|None)``
+    returns rank 0's 128-byte id on every rank (torch.distributed object
+    broadcast under torchrun)."""
+    lib = _lib.load()
+    uid = None
+    if rank == 0:
+        buf = (ctypes.c_uint8 * 128)()
+        _lib.check(lib.edpc_nccl_unique_id(buf, 128))
+        uid = bytes(buf)
+    uid = broadcast_id(uid)
+    arr = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    _lib.check(lib.edpc_ctx_set_comm(ctx.h, arr, world, rank))
+
+
+def torch_broadcast_id(uid):
+    import torch.distributed as dist
+    obj = [uid]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def bench_multi(args, wl) -> None:
+    """bench.py at N GPUs under torchrun: weak scaling (B/N lanes per GPU is
+    fixed by the workload's per-GPU share), one NCCL all-gather of the
+    gradient partials per model step inside the captured step graph; the
+    step time is the max over ranks of CUDA-event time."""
+    import json
+
+    import torch
+    import torch.distributed as dist
+
+    from . import synth
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    lib = _lib.load()
+    # weak scaling: the single-GPU workload per rank (B, S and stream bytes x N)
+    cfg = ModelConfig(**wl["model"], lanes=wl["lanes"] * world)
+    S = wl["segments"] * world
+    n = wl["nbytes"] * world
+    plan = lane_plan(cfg, S, world)
+    lb, lc = plan[rank]
+    T = cfg.context_len
+    chunk, K, W = args.chunk, args.steps, args.warmup
+    L = lane_len_for(n, cfg.lanes)
+    # each rank synthesises only its own lanes' bytes (seed + rank); content
+    # does not change the per-step work, which is shape-determined
+    mine = np.frombuffer(synth.generate(wl["kind"], lc * L, wl["seed"] + rank), dtype=np.uint8)
+    ctx = DeviceContext(cfg, S, n, local, lb, lc)
+    ctx.load_flat(init_params_f32(cfg))
+    _lib.check(lib.edpc_set_input_local(ctx.h, mine.ctypes.data, mine.size))
+    nccl_join(ctx, rank, world, torch_broadcast_id)
+    _lib.check(lib.edpc_compress_steps(ctx.h, 0, T))
+    col = T
+    for _ in range(W):
+        _lib.check(lib.edpc_compress_steps(ctx.h, col, col + chunk))
+        col += chunk
+    _lib.check(lib.edpc_sync(ctx.h))
+    dist.barrier()
+    torch.cuda.synchronize()
+    _lib.check(lib.edpc_timer(ctx.h, 0, None))
+    for k in range(K):
+        _lib.check(lib.edpc_compress_steps(ctx.h, col, col + chunk))
+        col += chunk
+    _lib.check(lib.edpc_timer(ctx.h, 1, None))
+    ms = ctypes.c_double()
+    _lib.check(lib.edpc_timer(ctx.h, 2, ctypes.byref(ms)))
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([ms.value], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    total_bytes = cfg.lanes * chunk * K  # all ranks' lanes
+    if rank == 0:
+        line = dict(metric="compress/decompress MB/s at 1/2/4/8 B200 + bits/byte vs CPU ref",
+                    value=total_bytes / (ms_max / 1e3) / 1e6, unit="MB/s", n_gpus=world,
+                    steps=K, warmup=W, ms_per_step=ms_max / K, higher_is_better=True,
+                    scaling="weak", vs_baseline=None,
+                    dtype="tf32", data=f"synthetic {wl['kind']}-like (PCG64 seed {wl['seed']} + rank)",
+                    config=dict(workload=f"{wl['desc']} per GPU; {world} GPUs: B={cfg.lanes}, "
+                                         f"S={S}, {n >> 20} MiB (C3-style weak scaling)",
+                                lanes=cfg.lanes, segments=S,
+                                lanes_per_gpu=lc, columns_per_step=chunk,
+                                exchange="NCCL all-gather of 8 lane-group gradient partials "
+                                         "per model step (inside the step graph)"))
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    dist.barrier()
+    dist.destroy_process_group()

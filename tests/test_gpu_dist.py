@@ -1,0 +1,40 @@
+"""G-invariance of the sharded path on one B200: G contexts on the same GPU,
+each owning 8/G lane groups and their segments, exchanging gradient partials
+device-to-device every step, must produce exactly the single-GPU container
+(`pipeline.py:117-118` bytes = f(data, cfg, S))."""
+import numpy as np
+import pytest
+
+from paper_2507_18969_b200 import ModelConfig, compress, decompress, read_container, write_container
+from paper_2507_18969_b200 import dist, synth
+from helpers import PAPER, TINY
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("world,segments", [(2, 4), (4, 4), (8, 8)])
+def test_sharded_tiny_is_bit_identical(world, segments):
+    data = synth.text_like(6000, 3)
+    ref = write_container(compress(data, TINY, segments))
+    got = write_container(dist.compress_multi(data, TINY, segments, [0] * world))
+    assert got == ref
+    assert dist.decompress_multi(read_container(got), [0] * world) == data
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_paper_dims_tcgen05_is_bit_identical(world):
+    cfg = ModelConfig(**PAPER, lanes=256)
+    data = synth.text_like(256 * 80, 5)
+    ref = write_container(compress(data, cfg, 16))
+    got = write_container(dist.compress_multi(data, cfg, 16, [0] * world))
+    assert got == ref
+    assert decompress(read_container(got), devices=[0] * world) == data
+
+
+def test_lane_plan_rejects_straddling_geometry():
+    with pytest.raises(ValueError):
+        dist.lane_plan(TINY.with_overrides(lanes=12), 4, 2)   # 12 % 8
+    with pytest.raises(ValueError):
+        dist.lane_plan(TINY, 2, 4)                           # 4-lane segments over 2-lane shares
+    with pytest.raises(ValueError):
+        dist.lane_plan(TINY, 4, 3)                           # 3 does not divide 8
