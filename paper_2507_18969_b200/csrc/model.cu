@@ -372,36 +372,53 @@ static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, cons
   return gemm_simt<false, false>(g, EpiBias{out, N, sOut, bias, sW}, c->st);
 }
 
+static cudaError_t colsum(edpc_ctx* c, const float* src, int N, int nz, int64_t sz,
+                          const float* mul, int64_t off, int64_t sOff);
+
 // weight-gradient partials: Gp[g][off + z*sOff + m*N + n] = sum over group
-// g's lanes of X[b][m] * G[z][b][n]
+// g's lanes of X[b][m] * G[z][b][n], and (bias_off >= 0) the bias partials
+// Gp[g][bias_off + z*sOff + n] = sum over the group's lanes of G[z][b][n] --
+// on the tcgen05 path those come from the GEMM's own B tiles in shared memory.
 static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, int N, int nzb,
-                         int64_t sG, int64_t off, int64_t sOff) {
+                         int64_t sG, int64_t off, int64_t sOff, int64_t bias_off) {
   EpiPartial e{c->Gp, c->lay.n_shared, off, sOff, N, c->g_first};
-  Scope sc(c, kRegGemm, c->st);
   const int glanes = c->lay.B / kNumGroups;
   if (c->lay.B % kNumGroups == 0 && glanes % kTcBK == 0 &&
       tc_ok(c, N, glanes, {X, G, c->Gp + off}, {Mw, N, sG, sOff, c->lay.n_shared})) {
+    Scope sc(c, kRegGemm, c->st);
     TcShape s{Mw, N, c->Bl, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 1,
               c->g_count, c->g_first, c->lay.B, c->lane0};
+    if (bias_off >= 0) {
+      s.bias_part = c->Gp;
+      s.bias_gstride = c->lay.n_shared;
+      s.bias_off = bias_off;
+      s.bias_zstride = sOff;
+    }
     TcOperand a{X, Mw, 0, 1}, b{G, N, sG, nzb};
     return as_cuda(tc_gemm<true, true>(s, a, b, e, c->st));
   }
-  GemmShape g{};
-  g.M = Mw;
-  g.N = N;
-  g.K = c->Bl;
-  g.A = X;
-  g.lda = Mw;
-  g.B = G;
-  g.ldb = N;
-  g.sB = sG;
-  g.nzb = nzb;
-  g.nsum = 1;
-  g.ngroups = c->g_count;
-  g.g0 = c->g_first;
-  g.B_global = c->lay.B;
-  g.lane0 = c->lane0;
-  return gemm_simt<true, false>(g, e, c->st);
+  {
+    Scope sc(c, kRegGemm, c->st);
+    GemmShape g{};
+    g.M = Mw;
+    g.N = N;
+    g.K = c->Bl;
+    g.A = X;
+    g.lda = Mw;
+    g.B = G;
+    g.ldb = N;
+    g.sB = sG;
+    g.nzb = nzb;
+    g.nsum = 1;
+    g.ngroups = c->g_count;
+    g.g0 = c->g_first;
+    g.B_global = c->lay.B;
+    g.lane0 = c->lane0;
+    cudaError_t r = gemm_simt<true, false>(g, e, c->st);
+    if (r != cudaSuccess) return r;
+  }
+  if (bias_off >= 0) return colsum(c, G, N, nzb, sG, nullptr, bias_off, sOff);
+  return cudaSuccess;
 }
 
 // bias-gradient partials (column sums per lane group)
@@ -555,11 +572,9 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
   // g_ff = g_up . out_w^T, epilogue -> GH[z] (product rule + GeLU')
   CK(dgrad(c, g_up, F, 1, 0, c->W + o.out_w, 0, H, EpiBwdAct{b.H, c->GH, K, plane, H}));
   // out_w / out_b gradients
-  CK(wgrad(c, b.ff, H, g_up, F, 1, 0, o.out_w, 0));
-  CK(colsum(c, g_up, F, 1, 0, nullptr, o.out_b, 0));
+  CK(wgrad(c, b.ff, H, g_up, F, 1, 0, o.out_w, 0, o.out_b));
   // branch weights / biases
-  CK(wgrad(c, b.x0, F, c->GH, H, K, plane, o.w0, o.wstride));
-  CK(colsum(c, c->GH, H, K, plane, nullptr, o.b0, o.wstride));
+  CK(wgrad(c, b.x0, F, c->GH, H, K, plane, o.w0, o.wstride, o.b0));
   // g_x0 = sum_z GH[z] . W_z^T
   CK(dgrad(c, c->GH, H, K, plane, c->W + o.w0, o.wstride, F, EpiStore{c->gx0, F}));
   // LN gain / bias gradients, then LN backward + residual
@@ -584,15 +599,13 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   }
   CK(cudaGetLastError());
   // head
-  CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0));
-  CK(colsum(c, c->gl, 256, 1, 0, nullptr, L.head_b, 0));
+  CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0, L.head_b));
   CK(dgrad(c, c->gl, 256, 1, 0, c->W + L.head_w, 0, F, EpiStore{c->gA, F}));
   // global MBRB: gA -> gB
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
   EDPC_TRY(mbrb_backward(c, L.glo, gb, c->gA, c->gB));
   // LTE up
-  CK(wgrad(c, c->mixed, FP, c->gB, F, 1, 0, L.up_w, 0));
-  CK(colsum(c, c->gB, F, 1, 0, nullptr, L.up_b, 0));
+  CK(wgrad(c, c->mixed, FP, c->gB, F, 1, 0, L.up_w, 0, L.up_b));
   CK(dgrad(c, c->gB, F, 1, 0, c->W + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
   // per-lane FDM: g_down with the old U, then U's Adam step (fused)
   {
@@ -620,8 +633,7 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   }
   CK(cudaGetLastError());
   // LTE down
-  CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0));
-  CK(colsum(c, c->gdown, FP, 1, 0, nullptr, L.down_b, 0));
+  CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
   CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore{c->gA, F}));
   // local MBRB: gA -> gB (gradient w.r.t. the embedded context)
   MbrbBufs lb{c->x_emb, c->l_xhat, c->l_rstd, c->l_x0, c->l_H, c->l_ff, c->x_local};

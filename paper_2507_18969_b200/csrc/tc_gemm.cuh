@@ -153,14 +153,18 @@ enum TcBatch { kBatchNone = 0, kBatchZ = 1, kBatchSum = 2 };
 
 struct TcShape {
   int M, N, K;       // K per summed sub-problem (before any K split)
-  int nzb;           // output batches (blockIdx.z % nzb)
+  int nzb;           // output batches
   int nsum;          // sub-problems accumulated into one tile
   int a_batch, b_batch;
-  // K split, one output per split index zg = blockIdx.z / nzb:
+  // K split, one output per split index zg:
   //   kmode 0: none; 1: lane groups [g0+zg] of B_global lanes (minus lane0);
   //   2: nsplit equal K chunks
   int kmode, nsplit, g0, B_global, lane0;
-  int dbg = 0;  // tests only: 1 = epilogue writes m*1000+n, 2 = dump smem A stage 0
+  int dbg = 0;  // tests only: 1 = epilogue writes m*1000+n
+  // fused column sums of B over K (weight-gradient GEMMs: the bias gradient
+  // of lane group g0+zg); needs MN-major B
+  float* bias_part = nullptr;
+  int64_t bias_gstride = 0, bias_off = 0, bias_zstride = 0;
 };
 
 // ------------------------------------------------------------------ kernel
@@ -171,54 +175,89 @@ struct TcSmem {
   static constexpr int kBBytes = BN * kTcBK * 4;
   static constexpr int kStageBytes = kABytes + kBBytes;
   static constexpr int kBytes = kTcStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered
 };
 
-constexpr int kTcThreads = 320;
+constexpr int kTcEpiWarps = 8;
+constexpr int kTcBiasWarps = 4;
+__host__ __device__ constexpr int tc_threads(bool bias) {
+  return 32 * (2 + kTcEpiWarps + (bias ? kTcBiasWarps : 0));
+}
 
-template <int BN, bool AMN, bool BMN, class Epi>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// Persistent, warp-specialised tcgen05 GEMM.  CTAs walk tiles t = blockIdx.x,
+// blockIdx.x + gridDim.x, ... (tn fastest, then tm, then batch/split z).
+//   warp 0      TMA producer over all k-blocks of all its tiles (kTcStages ring)
+//   warp 1      TMEM allocator + single-thread MMA issuer; accumulator double
+//               buffered in TMEM so tile t's epilogue overlaps tile t+1's MMAs
+//   warps 2..9  epilogue (two per TMEM lane quadrant, alternating 32-column
+//               chunks): tcgen05.ld -> fused epilogue -> global
+//   warps 10-13 (BIAS only) column sums of the B tile of every k-block of
+//               the tiles with tm == 0, read straight from the smem ring
+template <int BN, bool AMN, bool BMN, bool BIAS, class Epi>
+__global__ void __launch_bounds__(tc_threads(BIAS), 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
           TcShape s, Epi epi) {
+  static_assert(!BIAS || BMN, "fused bias sums read an MN-major B tile");
   extern __shared__ uint8_t smem_raw[];
   using SM = TcSmem<BN>;
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * SM::kStageBytes);
   uint64_t* empty = full + kTcStages;
-  uint64_t* accum = empty + kTcStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+  uint64_t* tfull = empty + kTcStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN;
-  const int m0 = blockIdx.y * kTcBM;
-  const int zb = blockIdx.z % s.nzb;
-  const int zg = blockIdx.z / s.nzb;
+  const int n_tn = s.N / BN;
+  const int n_tm = (s.M + kTcBM - 1) / kTcBM;
+  const int nzt = s.nzb * (s.kmode == 0 ? 1 : s.nsplit);
+  const int n_tiles = n_tn * n_tm * nzt;
 
-  int k_begin = 0, k_end = s.K;
-  if (s.kmode == 1) {
-    k_begin = group_begin(s.g0 + zg, s.B_global) - s.lane0;
-    k_end = group_begin(s.g0 + zg + 1, s.B_global) - s.lane0;
-  } else if (s.kmode == 2) {
-    const int chunk = s.K / s.nsplit;
-    k_begin = zg * chunk;
-    k_end = k_begin + chunk;
-  }
-  const int nkb = (k_end - k_begin) / kTcBK;
-  const int total = nkb * s.nsum;
+  auto tile_coords = [&](int t, int& tn, int& tm, int& zb, int& zg, int& kb0, int& nkb) {
+    tn = t % n_tn;
+    const int r = t / n_tn;
+    tm = r % n_tm;
+    const int z = r / n_tm;
+    zb = z % s.nzb;
+    zg = z / s.nzb;
+    int k_begin = 0, k_end = s.K;
+    if (s.kmode == 1) {
+      k_begin = group_begin(s.g0 + zg, s.B_global) - s.lane0;
+      k_end = group_begin(s.g0 + zg + 1, s.B_global) - s.lane0;
+    } else if (s.kmode == 2) {
+      const int chunk = s.K / s.nsplit;
+      k_begin = zg * chunk;
+      k_end = k_begin + chunk;
+    }
+    kb0 = k_begin;
+    nkb = (k_end - k_begin) / kTcBK;
+  };
 
   if (warp == 0 && lane == 0) {
     for (int st = 0; st < kTcStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], 1);
+      mbar_init(&empty[st], BIAS ? 2 : 1);
     }
-    mbar_init(accum, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], kTcEpiWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"((uint32_t)(BN < 32 ? 32 : BN)));
+                 "r"(SM::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   tc_fence_before();
@@ -227,87 +266,150 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   const uint32_t tmem = *tmem_slot;
 
   if (warp == 0) {
-    if (lane == 0 && total > 0) {
+    if (lane == 0) {
       // ---------------- TMA producer
-      for (int it = 0; it < total; ++it) {
-        const int st = it % kTcStages;
-        const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
-        mbar_wait(&empty[st], ph ^ 1u);
-        const int sub = it / nkb;
-        const int k = k_begin + (it - sub * nkb) * kTcBK;
-        const int az = s.a_batch == kBatchZ ? zb : (s.a_batch == kBatchSum ? sub : 0);
-        const int bz = s.b_batch == kBatchZ ? zb : (s.b_batch == kBatchSum ? sub : 0);
-        uint8_t* sa = smem + st * SM::kStageBytes;
-        uint8_t* sb = sa + SM::kABytes;
-        mbar_expect_tx(&full[st], SM::kStageBytes);
-        if (AMN) {
+      int it = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        int tn, tm, zb, zg, kb0, nkb;
+        tile_coords(t, tn, tm, zb, zg, kb0, nkb);
+        const int n0 = tn * BN, m0 = tm * kTcBM;
+        for (int q = 0; q < nkb * s.nsum; ++q, ++it) {
+          const int st = it % kTcStages;
+          const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
+          mbar_wait(&empty[st], ph ^ 1u);
+          const int sub = q / nkb;
+          const int k = kb0 + (q - sub * nkb) * kTcBK;
+          const int az = s.a_batch == kBatchZ ? zb : (s.a_batch == kBatchSum ? sub : 0);
+          const int bz = s.b_batch == kBatchZ ? zb : (s.b_batch == kBatchSum ? sub : 0);
+          uint8_t* sa = smem + st * SM::kStageBytes;
+          uint8_t* sb = sa + SM::kABytes;
+          mbar_expect_tx(&full[st], SM::kStageBytes);
+          if (AMN) {
 #pragma unroll
-          for (int j = 0; j < kTcBM / 32; ++j)
-            tma_load_3d(sa + j * 4096, &tma_a, &full[st], m0 + 32 * j, k, az);
-        } else {
-          tma_load_3d(sa, &tma_a, &full[st], k, m0, az);
-        }
-        if (BMN) {
+            for (int j = 0; j < kTcBM / 32; ++j)
+              tma_load_3d(sa + j * 4096, &tma_a, &full[st], m0 + 32 * j, k, az);
+          } else {
+            tma_load_3d(sa, &tma_a, &full[st], k, m0, az);
+          }
+          if (BMN) {
 #pragma unroll
-          for (int j = 0; j < BN / 32; ++j)
-            tma_load_3d(sb + j * 4096, &tma_b, &full[st], n0 + 32 * j, k, bz);
-        } else {
-          tma_load_3d(sb, &tma_b, &full[st], k, n0, bz);
+            for (int j = 0; j < BN / 32; ++j)
+              tma_load_3d(sb + j * 4096, &tma_b, &full[st], n0 + 32 * j, k, bz);
+          } else {
+            tma_load_3d(sb, &tma_b, &full[st], k, n0, bz);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0 && total > 0) {
+    if (lane == 0) {
       // ---------------- MMA issuer
       constexpr uint32_t idesc = idesc_tf32(kTcBM, BN, AMN ? 1 : 0, BMN ? 1 : 0);
-      for (int it = 0; it < total; ++it) {
+      int it = 0, lt = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+        int tn, tm, zb, zg, kb0, nkb;
+        tile_coords(t, tn, tm, zb, zg, kb0, nkb);
+        const int acc = lt & 1;
+        mbar_wait(&tempty[acc], (((uint32_t)lt >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        const uint32_t dtm = tmem + (uint32_t)(acc * BN);
+        const int nq = nkb * s.nsum;
+        for (int q = 0; q < nq; ++q, ++it) {
+          const int st = it % kTcStages;
+          const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
+          mbar_wait(&full[st], ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + st * SM::kStageBytes);
+          const uint32_t sb = sa + SM::kABytes;
+#pragma unroll
+          for (int kk = 0; kk < kTcBK / 8; ++kk) {
+            const uint64_t ad = AMN ? sdesc(sa + kk * 1024, 4096, 512, kLayoutSW128Base32B)
+                                    : sdesc(sa + kk * 32, 16, 1024, kLayoutSW128);
+            const uint64_t bd = BMN ? sdesc(sb + kk * 1024, 4096, 512, kLayoutSW128Base32B)
+                                    : sdesc(sb + kk * 32, 16, 1024, kLayoutSW128);
+            tc_mma_tf32(dtm, ad, bd, idesc, (q > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[st]);
+        }
+        tc_commit(&tfull[acc]);
+      }
+    }
+  } else if (warp < 2 + kTcEpiWarps) {
+    // ---------------- epilogue warps (TMEM lane quadrant = warp % 4)
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;
+    int lt = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+      int tn, tm, zb, zg, kb0, nkb;
+      tile_coords(t, tn, tm, zb, zg, kb0, nkb);
+      const int acc = lt & 1;
+      const int n0 = tn * BN;
+      const int m = tm * kTcBM + quad * 32 + lane;
+      const bool any = nkb * s.nsum > 0;
+      mbar_wait(&tfull[acc], ((uint32_t)lt >> 1) & 1u);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = half * 32; c < BN; c += 64) {
+        float v[32];
+        if (any) {
+          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c), v);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        }
+        if (s.dbg == 1) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = (float)(m * 1000 + n0 + c + j);
+        }
+        if (m < s.M && n0 + c < s.N) epi.row32(zb, zg, m, n0 + c, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+  } else if (BIAS) {
+    // ---------------- bias warps: column sums of B over this tile's K range
+    const int bt = threadIdx.x - 32 * (2 + kTcEpiWarps);  // 0..127
+    constexpr int kCols = BN / (32 * kTcBiasWarps) > 0 ? BN / (32 * kTcBiasWarps) : 1;
+    int it = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int tn, tm, zb, zg, kb0, nkb;
+      tile_coords(t, tn, tm, zb, zg, kb0, nkb);
+      const bool do_sum = tm == 0 && s.bias_part != nullptr;
+      float sum[kCols];
+#pragma unroll
+      for (int j = 0; j < kCols; ++j) sum[j] = 0.f;
+      const int nq = nkb * s.nsum;
+      for (int q = 0; q < nq; ++q, ++it) {
         const int st = it % kTcStages;
         const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
         mbar_wait(&full[st], ph);
-        tc_fence_after();
-        const uint32_t sa = smem_u32(smem + st * SM::kStageBytes);
-        const uint32_t sb = sa + SM::kABytes;
+        if (do_sum) {
+          const uint8_t* sb = smem + st * SM::kStageBytes + SM::kABytes;
 #pragma unroll
-        for (int kk = 0; kk < kTcBK / 8; ++kk) {
-          // K-major: advance 32 B inside the swizzled row; MN-major: one
-          // 1024 B atom (8 K-rows) per step
-          const uint64_t ad = AMN ? sdesc(sa + kk * 1024, 4096, 512, kLayoutSW128Base32B)
-                                  : sdesc(sa + kk * 32, 16, 1024, kLayoutSW128);
-          const uint64_t bd = BMN ? sdesc(sb + kk * 1024, 4096, 512, kLayoutSW128Base32B)
-                                  : sdesc(sb + kk * 32, 16, 1024, kLayoutSW128);
-          tc_mma_tf32(tmem, ad, bd, idesc, (it > 0 || kk > 0) ? 1u : 0u);
+          for (int j = 0; j < kCols; ++j) {
+            const int n = bt + j * 32 * kTcBiasWarps;
+            if (n < BN) {
+              const int box = n >> 5, nn = n & 31, chunk = nn >> 3;
+              const float* base = reinterpret_cast<const float*>(sb + box * 4096) + (nn & 7);
+#pragma unroll 8
+              for (int k = 0; k < kTcBK; ++k)
+                sum[j] += base[(k * 128 + ((chunk ^ (k & 3)) << 5)) >> 2];
+            }
+          }
         }
-        tc_commit(&empty[st]);
+        named_bar(1, 32 * kTcBiasWarps);
+        if (bt == 0) mbar_arrive(&empty[st]);
       }
-      tc_commit(accum);
-    }
-  } else {
-    // ---------------- epilogue warps 2..9 (TMEM lane quadrant = warp % 4)
-    const int quad = warp & 3;
-    const int half = (warp - 2) >> 2;
-    const int m = m0 + quad * 32 + lane;
-    if (total > 0) {
-      mbar_wait(accum, 0);
-      tc_fence_after();
-    }
-#pragma unroll 1
-    for (int c = half * 32; c < BN; c += 64) {
-      float v[32];
-      if (s.dbg == 1) {
+      if (do_sum) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = (float)(m * 1000 + n0 + c + j);
-      } else if (s.dbg == 2 && total > 0) {
-        mbar_wait(accum, 0);
-        const float* sa = reinterpret_cast<const float*>(smem);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = sa[(quad * 32 + lane) * 32 + j];
-      } else if (total > 0) {
-        tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c, v);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+        for (int j = 0; j < kCols; ++j) {
+          const int n = bt + j * 32 * kTcBiasWarps;
+          if (n < BN && tn * BN + n < s.N)
+            s.bias_part[(int64_t)(s.g0 + zg) * s.bias_gstride + s.bias_off + zb * s.bias_zstride +
+                        tn * BN + n] = sum[j];
+        }
       }
-      if (m < s.M && n0 + c < s.N) epi.row32(zb, zg, m, n0 + c, v);
     }
   }
   tc_fence_before();
@@ -315,7 +417,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
-                 "r"((uint32_t)(BN < 32 ? 32 : BN)));
+                 "r"(SM::kTmemCols));
   }
 }
 
@@ -411,6 +513,14 @@ inline bool tc_shape_ok(int N, int Kchunk) {
   return N <= 256 ? (N == 32 || N == 64 || N == 128 || N == 256) : (N % 256 == 0);
 }
 
+inline int num_sms() {
+  static int n[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 16 && !n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+  return dev < 16 && n[dev] ? n[dev] : 148;
+}
+
 template <int BN, bool AMN, bool BMN, class Epi>
 inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, const Epi& epi,
                      cudaStream_t st) {
@@ -433,17 +543,34 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
                          (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN, false);
   if (r != EDPC_OK) return r;
   const int nz = s.nzb * (s.kmode == 0 ? 1 : s.nsplit);
-  dim3 grid((unsigned)(s.N / BN), (unsigned)cdiv(s.M, kTcBM), (unsigned)nz);
-  auto kern = k_tc_gemm<BN, AMN, BMN, Epi>;
-  static bool attr_done[16] = {};
+  const int n_tiles = (s.N / BN) * cdiv(s.M, kTcBM) * nz;
+  const int grid = n_tiles < num_sms() ? n_tiles : num_sms();
+  static bool attr_done[2][16] = {};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 16 && !attr_done[dev]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<BN>::kBytes);
-    attr_done[dev] = true;
+  cudaError_t e;
+  bool launched = false;
+  if constexpr (BMN) {
+    if (s.bias_part) {
+      auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi>;
+      if (dev < 16 && !attr_done[1][dev]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             TcSmem<BN>::kBytes);
+        attr_done[1][dev] = true;
+      }
+      kern<<<grid, tc_threads(true), TcSmem<BN>::kBytes, st>>>(ta, tb, s, epi);
+      launched = true;
+    }
   }
-  kern<<<grid, kTcThreads, TcSmem<BN>::kBytes, st>>>(ta, tb, s, epi);
-  cudaError_t e = cudaGetLastError();
+  if (!launched) {
+    auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi>;
+    if (dev < 16 && !attr_done[0][dev]) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<BN>::kBytes);
+      attr_done[0][dev] = true;
+    }
+    kern<<<grid, tc_threads(false), TcSmem<BN>::kBytes, st>>>(ta, tb, s, epi);
+  }
+  e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_tc_gemm launch: ") + cudaGetErrorString(e));
     return EDPC_ERR_CUDA;
