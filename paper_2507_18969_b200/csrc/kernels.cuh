@@ -80,6 +80,33 @@ __global__ void k_mbrb_act(const float* __restrict__ H, int K, int64_t plane, fl
   ff[e] = p * gelu_cdf(p);
 }
 
+// MBRB forward epilogue of the multi-branch GEMM (model.py:97-101): H_z =
+// acc_z + b_z (kept for the backward product rule), ff = GeLU(prod_z H_z).
+template <int ZIN>
+struct EpiBranchAct {
+  float* H;         // [ZIN][M][N]
+  float* ff;        // [M][N]
+  const float* b0;  // bias of branch 0; branch z at b0 + z*sBias
+  int64_t sBias, N, plane;
+  __device__ void rowz(int m, int n0, float (&v)[ZIN][32]) const {
+    float p[32];
+#pragma unroll
+    for (int z = 0; z < ZIN; ++z) {
+      float b[32];
+      load32(b0 + z * sBias + n0, b);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[z][j] = v[z][j] + b[j];
+      store32(H + z * plane + (int64_t)m * N + n0, v[z]);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) p[j] = z == 0 ? v[0][j] : p[j] * v[z][j];
+    }
+#pragma unroll
+    for (int j = 0; j < 32; ++j) p[j] = p[j] * gelu_cdf(p[j]);
+    store32(ff + (int64_t)m * N + n0, p);
+  }
+  __device__ void row32(int, int, int, int, float (&)[32]) const {}
+};
+
 // MBRB backward epilogue of the out-projection dgrad (model.py:107-119):
 // g_prod = g_ff * GeLU'(prod); g_H_z = g_prod * prod_{j != z} H_j
 struct EpiBwdAct {
@@ -153,6 +180,97 @@ k_ln_bwd(const float* __restrict__ gx0, const float* __restrict__ xhat,
     float g = gx0[o + f] * gain[f];
     out[o + f] = (g - gm - xhat[o + f] * gxm) * r + up[o + f];
   }
+}
+
+// LN backward + residual fused with the LN gain / bias gradient partials
+// (nn.py:116-125): grid (chunks, groups); a block owns 64 lanes of one lane
+// group.  Warps walk lanes w, w+8, ...; each thread keeps column sums of
+// gx0 * xhat and gx0 for columns lane, lane+32, ...; warp sums are combined
+// in warp order, chunk sums in chunk order by the last block of the group
+// (ticket counter) -- a fixed order, so reproducible.
+constexpr int kLnChunk = 64;
+constexpr int kLnMaxF = 512;
+
+__global__ void __launch_bounds__(256)
+k_ln_bwd_fused(const float* __restrict__ gx0, const float* __restrict__ xhat,
+               const float* __restrict__ rstd, const float* __restrict__ gain,
+               const float* __restrict__ up, float* __restrict__ out, int F, int B_global,
+               int lane0, int g0, float* __restrict__ partials, int64_t n_shared, int64_t off_g,
+               int64_t off_b, float* __restrict__ scratch, unsigned* __restrict__ tickets) {
+  __shared__ float red[8][2 * kLnMaxF];
+  __shared__ unsigned ticket;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gg = g0 + blockIdx.y;
+  const int gb0 = group_begin(gg, B_global) - lane0, gb1 = group_begin(gg + 1, B_global) - lane0;
+  const int lb = gb0 + blockIdx.x * kLnChunk, le = min(gb1, lb + kLnChunk);
+  constexpr int kJ = kLnMaxF / 32;
+  float sg[kJ], sb[kJ];
+#pragma unroll
+  for (int j = 0; j < kJ; ++j) sg[j] = sb[j] = 0.f;
+  for (int b = lb + warp; b < le; b += 8) {
+    const int64_t o = (int64_t)b * F;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int f = lane + 32 * j;
+      if (f < F) {
+        const float gx = gx0[o + f], xh = xhat[o + f];
+        const float g = gx * gain[f];
+        s1 += g;
+        s2 += g * xh;
+        sg[j] += gx * xh;
+        sb[j] += gx;
+      }
+    }
+    const float gm = warp_sum(s1) / (float)F;
+    const float gxm = warp_sum(s2) / (float)F;
+    const float r = rstd[b];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int f = lane + 32 * j;
+      if (f < F) {
+        const float g = gx0[o + f] * gain[f];
+        out[o + f] = (g - gm - xhat[o + f] * gxm) * r + up[o + f];
+      }
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < kJ; ++j) {
+    const int f = lane + 32 * j;
+    if (f < F) {
+      red[warp][f] = sg[j];
+      red[warp][kLnMaxF + f] = sb[j];
+    }
+  }
+  __syncthreads();
+  const int nchunk = gridDim.x;
+  float* mine = scratch + ((int64_t)blockIdx.y * nchunk + blockIdx.x) * 2 * F;
+  for (int f = threadIdx.x; f < F; f += blockDim.x) {
+    float a = red[0][f], c = red[0][kLnMaxF + f];
+    for (int w = 1; w < 8; ++w) {
+      a += red[w][f];
+      c += red[w][kLnMaxF + f];
+    }
+    mine[f] = a;
+    mine[F + f] = c;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) ticket = atomicAdd(&tickets[blockIdx.y], 1u);
+  __syncthreads();
+  if (ticket != (unsigned)(nchunk - 1)) return;
+  __threadfence();
+  const float* all = scratch + (int64_t)blockIdx.y * nchunk * 2 * F;
+  for (int f = threadIdx.x; f < F; f += blockDim.x) {
+    float a = all[f], c = all[F + f];
+    for (int k = 1; k < nchunk; ++k) {
+      a += all[(int64_t)k * 2 * F + f];
+      c += all[(int64_t)k * 2 * F + F + f];
+    }
+    partials[(int64_t)gg * n_shared + off_g + f] = a;
+    partials[(int64_t)gg * n_shared + off_b + f] = c;
+  }
+  if (threadIdx.x == 0) tickets[blockIdx.y] = 0u;
 }
 
 // ------------------------------------------- lane-group column reductions

@@ -195,6 +195,8 @@ struct edpc_ctx {
   // backward temporaries
   float *gl, *gA, *gB, *GH, *gx0, *gmix, *gdown, *emb_sub;
   float* ws = nullptr;  // split-K workspace [kSplitK][Bl][<=256]
+  float* ln_scratch = nullptr;  // LN-gradient chunk sums
+  unsigned* ln_tickets = nullptr;
   int *chunk_tab = nullptr, *grp_chunks = nullptr;
   int n_chunks = 0;
   // coder
@@ -492,22 +494,37 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
   const Layout& L = c->lay;
   const int Bl = c->Bl, F = L.F, H = o.H;
   dim3 g8((unsigned)cdiv(Bl, 8));
-  Scope sc_ln(c, kRegElem, c->st);
-  if (gather)
-    k_embed_ln<true><<<g8, 256, 0, c->st>>>(src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
-                                            c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0);
-  else
-    k_embed_ln<false><<<g8, 256, 0, c->st>>>(src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
-                                             c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0);
-  CK(cudaGetLastError());
-  const int64_t plane = (int64_t)Bl * H;
-  CK(fwd_linear(c, b.x0, F, F, c->W + o.w0, H, L.K, o.wstride, b.H, plane, c->W + o.b0, nullptr,
-                Bl));
   {
+    Scope sc_ln(c, kRegElem, c->st);
+    if (gather)
+      k_embed_ln<true><<<g8, 256, 0, c->st>>>(src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
+                                              c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0);
+    else
+      k_embed_ln<false><<<g8, 256, 0, c->st>>>(src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
+                                               c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0);
+    CK(cudaGetLastError());
+  }
+  const int64_t plane = (int64_t)Bl * H;
+  // branch GEMMs with the product + GeLU fused into the epilogue when all
+  // branches of a tile fit one CTA's TMEM (k = 2, 3); else GEMM + k_mbrb_act
+  if ((L.K == 2 || L.K == 3) && H % 128 == 0 &&
+      tc_ok(c, H, F, {b.x0, c->W + o.w0, b.H, b.ff, c->W + o.b0}, {F, H, o.wstride, plane})) {
+    Scope sc(c, kRegGemm, c->st);
+    TcShape s{Bl, H, F, L.K, 1, kBatchNone, kBatchZ, 0, 1, 0, 0, 0};
+    TcOperand a{b.x0, F, 0, 1}, bw{c->W + o.w0, H, o.wstride, L.K};
+    const int st =
+        L.K == 2 ? tc_launch_zin<128, 2, true>(
+                       s, a, bw, EpiBranchAct<2>{b.H, b.ff, c->W + o.b0, o.wstride, H, plane}, c->st)
+                 : tc_launch_zin<64, 3, true>(
+                       s, a, bw, EpiBranchAct<3>{b.H, b.ff, c->W + o.b0, o.wstride, H, plane}, c->st);
+    if (st != EDPC_OK) return st;
+  } else {
+    CK(fwd_linear(c, b.x0, F, F, c->W + o.w0, H, L.K, o.wstride, b.H, plane, c->W + o.b0, nullptr,
+                  Bl));
     Scope sc_(c, kRegElem, c->st);
     k_mbrb_act<<<(unsigned)cdiv(plane, 256), 256, 0, c->st>>>(b.H, L.K, plane, b.ff);
+    CK(cudaGetLastError());
   }
-  CK(cudaGetLastError());
   CK(fwd_linear(c, b.ff, H, H, c->W + o.out_w, F, 1, 0, b.out, 0, c->W + o.out_b, b.x, Bl));
   return EDPC_OK;
 }
@@ -577,15 +594,25 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
   CK(wgrad(c, b.x0, F, c->GH, H, K, plane, o.w0, o.wstride, o.b0));
   // g_x0 = sum_z GH[z] . W_z^T
   CK(dgrad(c, c->GH, H, K, plane, c->W + o.w0, o.wstride, F, EpiStore{c->gx0, F}));
-  // LN gain / bias gradients, then LN backward + residual
-  CK(colsum(c, c->gx0, F, 1, 0, b.xhat, o.ln_g, 0));
-  CK(colsum(c, c->gx0, F, 1, 0, nullptr, o.ln_b, 0));
-  {
-    Scope sc_(c, kRegElem, c->st);
+  // LN backward + residual, with the LN gain / bias gradient partials
+  if (F <= kLnMaxF && c->g_count > 0) {
+    int maxg = 0;
+    for (int g = c->g_first; g < c->g_first + c->g_count; ++g)
+      maxg = std::max(maxg, group_begin(g + 1, L.B) - group_begin(g, L.B));
+    dim3 grid((unsigned)std::max(1, cdiv(maxg, kLnChunk)), (unsigned)c->g_count);
+    Scope sc(c, kRegElem, c->st);
+    k_ln_bwd_fused<<<grid, 256, 0, c->st>>>(c->gx0, b.xhat, b.rstd, c->W + o.ln_g, g_up, g_in, F,
+                                            L.B, c->lane0, c->g_first, c->Gp, L.n_shared, o.ln_g,
+                                            o.ln_b, c->ln_scratch, c->ln_tickets);
+    CK(cudaGetLastError());
+  } else {
+    CK(colsum(c, c->gx0, F, 1, 0, b.xhat, o.ln_g, 0));
+    CK(colsum(c, c->gx0, F, 1, 0, nullptr, o.ln_b, 0));
+    Scope sc(c, kRegElem, c->st);
     k_ln_bwd<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(c->gx0, b.xhat, b.rstd, c->W + o.ln_g, g_up,
                                                        g_in, F, Bl);
+    CK(cudaGetLastError());
   }
-  CK(cudaGetLastError());
   return EDPC_OK;
 }
 
@@ -888,6 +915,8 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
   A_(c->gmix, Bl * FP);
   A_(c->gdown, Bl * FP);
   A_(c->ws, (int64_t)kSplitK * Bl * 256);
+  A_(c->ln_scratch, (int64_t)kNumGroups * (cdiv(Bl, kLnChunk) + 1) * 2 * F);
+  A_(c->ln_tickets, kNumGroups);
   // embedding-gradient chunks: <= 64 lanes (and <= 4096 context bytes) each,
   // never straddling a lane group
   {
@@ -937,6 +966,7 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
   cudaMemsetAsync(c->Gp, 0, (int64_t)kNumGroups * L.n_shared * 4, c->st);
   cudaMemsetAsync(c->enc_words, 0, c->enc_cap_words * c->Sl * 4, c->st);
   cudaMemsetAsync(c->dec_err, 0, c->Sl * 4, c->st);
+  cudaMemsetAsync(c->ln_tickets, 0, kNumGroups * 4, c->st);
   {
     std::vector<int64_t> es(4 * (size_t)c->Sl);
     for (int s = 0; s < c->Sl; ++s) {

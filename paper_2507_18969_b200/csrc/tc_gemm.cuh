@@ -169,13 +169,18 @@ struct TcShape {
 
 // ------------------------------------------------------------------ kernel
 
-template <int BN>
+// ZIN > 1: ZIN batches (the MBRB branches) are computed by the same CTA for
+// the same (tm, tn) tile -- one A tile and ZIN B tiles per stage, ZIN
+// accumulators per TMEM buffer -- so the epilogue sees all branches at once.
+template <int BN, int ZIN = 1>
 struct TcSmem {
   static constexpr int kABytes = kTcBM * kTcBK * 4;  // 16 KB
   static constexpr int kBBytes = BN * kTcBK * 4;
-  static constexpr int kStageBytes = kABytes + kBBytes;
+  static constexpr int kStageBytes = kABytes + ZIN * kBBytes;
   static constexpr int kBytes = kTcStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
-  static constexpr uint32_t kTmemCols = 2 * BN < 32 ? 32 : 2 * BN;  // double-buffered
+  static constexpr int kCols = 2 * ZIN * BN;  // double-buffered accumulators
+  static constexpr uint32_t kTmemCols =
+      kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
 };
 
 constexpr int kTcEpiWarps = 8;
@@ -201,13 +206,15 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 //               chunks): tcgen05.ld -> fused epilogue -> global
 //   warps 10-13 (BIAS only) column sums of the B tile of every k-block of
 //               the tiles with tm == 0, read straight from the smem ring
-template <int BN, bool AMN, bool BMN, bool BIAS, class Epi>
+template <int BN, bool AMN, bool BMN, bool BIAS, class Epi, int ZIN = 1>
 __global__ void __launch_bounds__(tc_threads(BIAS), 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
           TcShape s, Epi epi) {
   static_assert(!BIAS || BMN, "fused bias sums read an MN-major B tile");
+  static_assert(ZIN == 1 || !BIAS, "multi-branch tiles have no fused bias");
+  static_assert(TcSmem<BN, ZIN>::kCols <= 512, "TMEM holds 512 columns");
   extern __shared__ uint8_t smem_raw[];
-  using SM = TcSmem<BN>;
+  using SM = TcSmem<BN, ZIN>;
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * SM::kStageBytes);
   uint64_t* empty = full + kTcStages;
@@ -219,7 +226,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   const int lane = threadIdx.x & 31;
   const int n_tn = s.N / BN;
   const int n_tm = (s.M + kTcBM - 1) / kTcBM;
-  const int nzt = s.nzb * (s.kmode == 0 ? 1 : s.nsplit);
+  const int nzt = (ZIN > 1 ? 1 : s.nzb) * (s.kmode == 0 ? 1 : s.nsplit);
   const int n_tiles = n_tn * n_tm * nzt;
 
   auto tile_coords = [&](int t, int& tn, int& tm, int& zb, int& zg, int& kb0, int& nkb) {
@@ -227,8 +234,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
     const int r = t / n_tn;
     tm = r % n_tm;
     const int z = r / n_tm;
-    zb = z % s.nzb;
-    zg = z / s.nzb;
+    const int nzb = ZIN > 1 ? 1 : s.nzb;
+    zb = z % nzb;
+    zg = z / nzb;
     int k_begin = 0, k_end = s.K;
     if (s.kmode == 1) {
       k_begin = group_begin(s.g0 + zg, s.B_global) - s.lane0;
@@ -291,12 +299,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
           } else {
             tma_load_3d(sa, &tma_a, &full[st], k, m0, az);
           }
-          if (BMN) {
 #pragma unroll
-            for (int j = 0; j < BN / 32; ++j)
-              tma_load_3d(sb + j * 4096, &tma_b, &full[st], n0 + 32 * j, k, bz);
-          } else {
-            tma_load_3d(sb, &tma_b, &full[st], k, n0, bz);
+          for (int zi = 0; zi < ZIN; ++zi) {
+            const int bzz = ZIN > 1 ? zi : bz;
+            uint8_t* sbz = sb + zi * SM::kBBytes;
+            if (BMN) {
+#pragma unroll
+              for (int j = 0; j < BN / 32; ++j)
+                tma_load_3d(sbz + j * 4096, &tma_b, &full[st], n0 + 32 * j, k, bzz);
+            } else {
+              tma_load_3d(sbz, &tma_b, &full[st], k, n0, bzz);
+            }
           }
         }
       }
@@ -312,7 +325,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
         const int acc = lt & 1;
         mbar_wait(&tempty[acc], (((uint32_t)lt >> 1) & 1u) ^ 1u);
         tc_fence_after();
-        const uint32_t dtm = tmem + (uint32_t)(acc * BN);
+        const uint32_t dtm = tmem + (uint32_t)(acc * ZIN * BN);
         const int nq = nkb * s.nsum;
         for (int q = 0; q < nq; ++q, ++it) {
           const int st = it % kTcStages;
@@ -320,14 +333,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
           mbar_wait(&full[st], ph);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + st * SM::kStageBytes);
-          const uint32_t sb = sa + SM::kABytes;
 #pragma unroll
-          for (int kk = 0; kk < kTcBK / 8; ++kk) {
-            const uint64_t ad = AMN ? sdesc(sa + kk * 1024, 4096, 512, kLayoutSW128Base32B)
-                                    : sdesc(sa + kk * 32, 16, 1024, kLayoutSW128);
-            const uint64_t bd = BMN ? sdesc(sb + kk * 1024, 4096, 512, kLayoutSW128Base32B)
-                                    : sdesc(sb + kk * 32, 16, 1024, kLayoutSW128);
-            tc_mma_tf32(dtm, ad, bd, idesc, (q > 0 || kk > 0) ? 1u : 0u);
+          for (int zi = 0; zi < ZIN; ++zi) {
+            const uint32_t sb = sa + SM::kABytes + zi * SM::kBBytes;
+#pragma unroll
+            for (int kk = 0; kk < kTcBK / 8; ++kk) {
+              const uint64_t ad = AMN ? sdesc(sa + kk * 1024, 4096, 512, kLayoutSW128Base32B)
+                                      : sdesc(sa + kk * 32, 16, 1024, kLayoutSW128);
+              const uint64_t bd = BMN ? sdesc(sb + kk * 1024, 4096, 512, kLayoutSW128Base32B)
+                                      : sdesc(sb + kk * 32, 16, 1024, kLayoutSW128);
+              tc_mma_tf32(dtm + (uint32_t)(zi * BN), ad, bd, idesc, (q > 0 || kk > 0) ? 1u : 0u);
+            }
           }
           tc_commit(&empty[st]);
         }
@@ -350,18 +366,28 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       tc_fence_after();
 #pragma unroll 1
       for (int c = half * 32; c < BN; c += 64) {
-        float v[32];
-        if (any) {
-          tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c), v);
+        if constexpr (ZIN == 1) {
+          float v[32];
+          if (any) {
+            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c), v);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          }
+          if (s.dbg == 1) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = (float)(m * 1000 + n0 + c + j);
+          }
+          if (m < s.M && n0 + c < s.N) epi.row32(zb, zg, m, n0 + c, v);
         } else {
+          float v[ZIN][32];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = 0.f;
+          for (int zi = 0; zi < ZIN; ++zi)
+            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) +
+                          (uint32_t)((acc * ZIN + zi) * BN + c),
+                      v[zi]);
+          if (m < s.M && n0 + c < s.N) epi.rowz(m, n0 + c, v);
         }
-        if (s.dbg == 1) {
-#pragma unroll
-          for (int j = 0; j < 32; ++j) v[j] = (float)(m * 1000 + n0 + c + j);
-        }
-        if (m < s.M && n0 + c < s.N) epi.row32(zb, zg, m, n0 + c, v);
       }
       tc_fence_before();
       __syncwarp();
@@ -573,6 +599,41 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
   e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_tc_gemm launch: ") + cudaGetErrorString(e));
+    return EDPC_ERR_CUDA;
+  }
+  return EDPC_OK;
+}
+
+// Multi-branch launch: ZIN branch GEMMs sharing A, one CTA per (tm, tn).
+template <int BN, int ZIN, bool BMN, class Epi>
+inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& B,
+                         const Epi& epi, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  int r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.K, (uint64_t)s.M, (uint64_t)A.nbatch,
+                           (uint64_t)A.ld, (uint64_t)A.sbatch, 32, kTcBM, false);
+  if (r != EDPC_OK) return r;
+  if (BMN)
+    r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.N, (uint64_t)s.K, (uint64_t)B.nbatch,
+                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, 32, true);
+  else
+    r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.K, (uint64_t)s.N, (uint64_t)B.nbatch,
+                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN, false);
+  if (r != EDPC_OK) return r;
+  const int n_tiles = (s.N / BN) * cdiv(s.M, kTcBM);
+  const int grid = n_tiles < num_sms() ? n_tiles : num_sms();
+  auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN>;
+  static bool attr_done[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 16 && !attr_done[dev]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         TcSmem<BN, ZIN>::kBytes);
+    attr_done[dev] = true;
+  }
+  kern<<<grid, tc_threads(false), TcSmem<BN, ZIN>::kBytes, st>>>(ta, tb, s, epi);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("k_tc_gemm<zin> launch: ") + cudaGetErrorString(e));
     return EDPC_ERR_CUDA;
   }
   return EDPC_OK;
