@@ -160,6 +160,20 @@ __device__ __forceinline__ void store32(float* dst, const float (&v)[32]) {
   }
 }
 
+// tcgen05 epilogues see a 32x32 block transposed into shared memory:
+// T[r * 33 + j] = D(m_base + r, n0 + j); lane j walks the 32 rows of column
+// n0 + j, so each warp access is one coalesced 128-byte row segment.
+#define EDPC_TILE_ROWS(BODY)                                  \
+  {                                                           \
+    const int lane_ = threadIdx.x & 31;                       \
+    _Pragma("unroll 4") for (int r = 0; r < 32; ++r) {        \
+      const int m = m_base + r;                               \
+      if (m >= M) break;                                      \
+      const float acc = T[r * 33 + lane_];                    \
+      BODY                                                    \
+    }                                                         \
+  }
+
 // C[zb] = acc + bias[zb] (row-broadcast); ldc row stride, sC batch stride
 struct EpiBias {
   float* C;
@@ -175,6 +189,12 @@ struct EpiBias {
 #pragma unroll
     for (int j = 0; j < 32; ++j) v[j] = v[j] + b[j];
     store32(C + zb * sC + (int64_t)m * ldc + n0, v);
+  }
+  __device__ void tile(const float* T, int zb, int, int m_base, int n0, int M) const {
+    const int n = n0 + (threadIdx.x & 31);
+    const float b = bias[zb * sBias + n];
+    float* Cz = C + zb * sC + n;
+    EDPC_TILE_ROWS(Cz[(int64_t)m * ldc] = acc + b;)
   }
 };
 
@@ -196,6 +216,11 @@ struct EpiBiasResid {
     for (int j = 0; j < 32; ++j) v[j] = (v[j] + b[j]) + r[j];
     store32(C + (int64_t)m * ldc + n0, v);
   }
+  __device__ void tile(const float* T, int, int, int m_base, int n0, int M) const {
+    const int n = n0 + (threadIdx.x & 31);
+    const float b = bias[n];
+    EDPC_TILE_ROWS(C[(int64_t)m * ldc + n] = (acc + b) + resid[(int64_t)m * ldr + n];)
+  }
 };
 
 // plain store (dgrad outputs)
@@ -207,6 +232,10 @@ struct EpiStore {
   }
   __device__ void row32(int, int, int m, int n0, float (&v)[32]) const {
     store32(C + (int64_t)m * ldc + n0, v);
+  }
+  __device__ void tile(const float* T, int, int, int m_base, int n0, int M) const {
+    const int n = n0 + (threadIdx.x & 31);
+    EDPC_TILE_ROWS(C[(int64_t)m * ldc + n] = acc;)
   }
 };
 
@@ -222,6 +251,10 @@ struct EpiPartial {
   }
   __device__ void row32(int zb, int zg, int m, int n0, float (&v)[32]) const {
     store32(partials + (int64_t)(g0 + zg) * n_shared + off + zb * sOff + (int64_t)m * ldw + n0, v);
+  }
+  __device__ void tile(const float* T, int zb, int zg, int m_base, int n0, int M) const {
+    float* P = partials + (int64_t)(g0 + zg) * n_shared + off + zb * sOff + n0 + (threadIdx.x & 31);
+    EDPC_TILE_ROWS(P[(int64_t)m * ldw] = acc;)
   }
 };
 

@@ -105,6 +105,29 @@ struct EpiBranchAct {
     store32(ff + (int64_t)m * N + n0, p);
   }
   __device__ void row32(int, int, int, int, float (&)[32]) const {}
+  __device__ void tile(const float*, int, int, int, int, int) const {}
+  // T holds ZIN transposed 32x32 blocks (branch z at T + z*32*33)
+  __device__ void tile_z(const float* T, int m_base, int n0, int M) const {
+    const int lane = threadIdx.x & 31;
+    const int n = n0 + lane;
+    float b[ZIN];
+#pragma unroll
+    for (int z = 0; z < ZIN; ++z) b[z] = b0[z * sBias + n];
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      const int m = m_base + r;
+      if (m >= M) break;
+      const int64_t e = (int64_t)m * N + n;
+      float p = 0.f;
+#pragma unroll
+      for (int z = 0; z < ZIN; ++z) {
+        const float h = T[z * 32 * 33 + r * 33 + lane] + b[z];
+        H[z * plane + e] = h;
+        p = z == 0 ? h : p * h;
+      }
+      ff[e] = p * gelu_cdf(p);
+    }
+  }
 };
 
 // MBRB backward epilogue of the out-projection dgrad (model.py:107-119):
@@ -154,6 +177,32 @@ struct EpiBwdAct {
         for (int j = 0; j < 32; ++j) g[j] = g[j] * h[j];
       }
       store32(GH + z * plane + e, g);
+    }
+  }
+  __device__ void tile(const float* T, int, int, int m_base, int n0, int M) const {
+    const int lane = threadIdx.x & 31;
+    const int n = n0 + lane;
+#pragma unroll 4
+    for (int r = 0; r < 32; ++r) {
+      const int m = m_base + r;
+      if (m >= M) break;
+      const int64_t e = (int64_t)m * ld + n;
+      float h[3];
+      float p = 0.f;
+      for (int z = 0; z < K; ++z) {
+        const float hz = H[z * plane + e];
+        if (z < 3) h[z] = hz;
+        p = z == 0 ? hz : p * hz;
+      }
+      const float cdf = gelu_cdf(p);
+      const float pdf = 0.39894228040143267794f * expf(-0.5f * p * p);
+      const float gp = T[r * 33 + lane] * (cdf + p * pdf);
+      for (int z = 0; z < K; ++z) {
+        float g = gp;
+        for (int j = 0; j < K; ++j)
+          if (j != z) g = g * (j < 3 ? h[j] : H[j * plane + e]);
+        GH[z * plane + e] = g;
+      }
     }
   }
 };
@@ -820,6 +869,10 @@ struct EpiSplit {
   }
   __device__ void row32(int, int zg, int m, int n0, float (&v)[32]) const {
     store32(ws + zg * plane + (int64_t)m * ld + n0, v);
+  }
+  __device__ void tile(const float* T, int, int zg, int m_base, int n0, int M) const {
+    float* W = ws + zg * plane + n0 + (threadIdx.x & 31);
+    EDPC_TILE_ROWS(W[(int64_t)m * ld] = acc;)
   }
 };
 

@@ -172,12 +172,23 @@ struct TcShape {
 // ZIN > 1: ZIN batches (the MBRB branches) are computed by the same CTA for
 // the same (tm, tn) tile -- one A tile and ZIN B tiles per stage, ZIN
 // accumulators per TMEM buffer -- so the epilogue sees all branches at once.
+// Epilogue warps transpose each 32x32 accumulator block through shared
+// memory (padded rows of 33) so that every global load/store of the
+// epilogue is a coalesced 128-byte row segment.
+constexpr int kTcEpiWarpsC = 8;
+constexpr int kTcTileFloats = 32 * 33;
+
 template <int BN, int ZIN = 1>
 struct TcSmem {
   static constexpr int kABytes = kTcBM * kTcBK * 4;  // 16 KB
   static constexpr int kBBytes = BN * kTcBK * 4;
   static constexpr int kStageBytes = kABytes + ZIN * kBBytes;
-  static constexpr int kBytes = kTcStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kEpiBytes = kTcEpiWarpsC * ZIN * kTcTileFloats * 4;
+  static constexpr int kFixed = 1024 /*align*/ + 256 /*barriers*/ + kEpiBytes;
+  static constexpr int kStages = (4 * kStageBytes + kFixed <= 232448) ? 4 : 3;
+  static constexpr int kEpiOffset = kStages * kStageBytes;
+  static constexpr int kBarOffset = kEpiOffset + kEpiBytes;
+  static constexpr int kBytes = kStages * kStageBytes + kFixed;
   static constexpr int kCols = 2 * ZIN * BN;  // double-buffered accumulators
   static constexpr uint32_t kTmemCols =
       kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
@@ -216,9 +227,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   extern __shared__ uint8_t smem_raw[];
   using SM = TcSmem<BN, ZIN>;
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kTcStages * SM::kStageBytes);
-  uint64_t* empty = full + kTcStages;
-  uint64_t* tfull = empty + kTcStages;
+  constexpr int kStages = SM::kStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::kBarOffset);
+  uint64_t* empty = full + kStages;
+  uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -251,7 +263,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   };
 
   if (warp == 0 && lane == 0) {
-    for (int st = 0; st < kTcStages; ++st) {
+    for (int st = 0; st < kStages; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], BIAS ? 2 : 1);
     }
@@ -282,8 +294,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
         tile_coords(t, tn, tm, zb, zg, kb0, nkb);
         const int n0 = tn * BN, m0 = tm * kTcBM;
         for (int q = 0; q < nkb * s.nsum; ++q, ++it) {
-          const int st = it % kTcStages;
-          const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
+          const int st = it % kStages;
+          const uint32_t ph = (uint32_t)(it / kStages) & 1u;
           mbar_wait(&empty[st], ph ^ 1u);
           const int sub = q / nkb;
           const int k = kb0 + (q - sub * nkb) * kTcBK;
@@ -328,8 +340,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
         const uint32_t dtm = tmem + (uint32_t)(acc * ZIN * BN);
         const int nq = nkb * s.nsum;
         for (int q = 0; q < nq; ++q, ++it) {
-          const int st = it % kTcStages;
-          const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
+          const int st = it % kStages;
+          const uint32_t ph = (uint32_t)(it / kStages) & 1u;
           mbar_wait(&full[st], ph);
           tc_fence_after();
           const uint32_t sa = smem_u32(smem + st * SM::kStageBytes);
@@ -364,12 +376,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       const bool any = nkb * s.nsum > 0;
       mbar_wait(&tfull[acc], ((uint32_t)lt >> 1) & 1u);
       tc_fence_after();
+      float* T = reinterpret_cast<float*>(smem + SM::kEpiOffset) + (warp - 2) * ZIN * kTcTileFloats;
+      const int m_base = tm * kTcBM + quad * 32;
 #pragma unroll 1
       for (int c = half * 32; c < BN; c += 64) {
-        if constexpr (ZIN == 1) {
+#pragma unroll
+        for (int zi = 0; zi < ZIN; ++zi) {
           float v[32];
           if (any) {
-            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c), v);
+            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) +
+                          (uint32_t)((acc * ZIN + zi) * BN + c),
+                      v);
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
@@ -378,16 +395,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = (float)(m * 1000 + n0 + c + j);
           }
-          if (m < s.M && n0 + c < s.N) epi.row32(zb, zg, m, n0 + c, v);
-        } else {
-          float v[ZIN][32];
 #pragma unroll
-          for (int zi = 0; zi < ZIN; ++zi)
-            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) +
-                          (uint32_t)((acc * ZIN + zi) * BN + c),
-                      v[zi]);
-          if (m < s.M && n0 + c < s.N) epi.rowz(m, n0 + c, v);
+          for (int j = 0; j < 32; ++j) T[zi * kTcTileFloats + lane * 33 + j] = v[j];
         }
+        __syncwarp();
+        if (m_base < s.M) {
+          if constexpr (ZIN == 1)
+            epi.tile(T, zb, zg, m_base, n0 + c, s.M);
+          else
+            epi.tile_z(T, m_base, n0 + c, s.M);
+        }
+        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
@@ -407,8 +425,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       for (int j = 0; j < kCols; ++j) sum[j] = 0.f;
       const int nq = nkb * s.nsum;
       for (int q = 0; q < nq; ++q, ++it) {
-        const int st = it % kTcStages;
-        const uint32_t ph = (uint32_t)(it / kTcStages) & 1u;
+        const int st = it % kStages;
+        const uint32_t ph = (uint32_t)(it / kStages) & 1u;
         mbar_wait(&full[st], ph);
         if (do_sum) {
           const uint8_t* sb = smem + st * SM::kStageBytes + SM::kABytes;
