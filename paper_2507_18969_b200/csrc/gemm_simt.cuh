@@ -217,9 +217,22 @@ struct EpiBiasResid {
     store32(C + (int64_t)m * ldc + n0, v);
   }
   __device__ void tile(const float* T, int, int, int m_base, int n0, int M) const {
-    const int n = n0 + (threadIdx.x & 31);
+    const int lane = threadIdx.x & 31;
+    const int n = n0 + lane;
     const float b = bias[n];
-    EDPC_TILE_ROWS(C[(int64_t)m * ldc + n] = (acc + b) + resid[(int64_t)m * ldr + n];)
+    const float* __restrict__ R = resid;
+    float* __restrict__ O = C;
+#pragma unroll 1
+    for (int r0 = 0; r0 < 32; r0 += 8) {
+      float rv[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        rv[r] = m_base + r0 + r < M ? R[(int64_t)(m_base + r0 + r) * ldr + n] : 0.f;
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (m_base + r0 + r < M)
+          O[(int64_t)(m_base + r0 + r) * ldc + n] = (T[(r0 + r) * 33 + lane] + b) + rv[r];
+    }
   }
 };
 

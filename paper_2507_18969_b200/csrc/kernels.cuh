@@ -179,29 +179,50 @@ struct EpiBwdAct {
       store32(GH + z * plane + e, g);
     }
   }
+  // rows in batches of 8: all H loads of a batch are issued before any
+  // GH store (the stores could otherwise alias the loads for the compiler)
   __device__ void tile(const float* T, int, int, int m_base, int n0, int M) const {
     const int lane = threadIdx.x & 31;
     const int n = n0 + lane;
-#pragma unroll 4
+    const float* __restrict__ Hr = H;
+    float* __restrict__ Gw = GH;
+    if (K == 2 && m_base + 32 <= M) {
+#pragma unroll 1
+      for (int r0 = 0; r0 < 32; r0 += 8) {
+        float h0[8], h1[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int64_t e = (int64_t)(m_base + r0 + r) * ld + n;
+          h0[r] = Hr[e];
+          h1[r] = Hr[plane + e];
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int64_t e = (int64_t)(m_base + r0 + r) * ld + n;
+          const float p = h0[r] * h1[r];
+          const float cdf = gelu_cdf(p);
+          const float pdf = 0.39894228040143267794f * expf(-0.5f * p * p);
+          const float gp = T[(r0 + r) * 33 + lane] * (cdf + p * pdf);
+          Gw[e] = gp * h1[r];
+          Gw[plane + e] = gp * h0[r];
+        }
+      }
+      return;
+    }
     for (int r = 0; r < 32; ++r) {
       const int m = m_base + r;
       if (m >= M) break;
       const int64_t e = (int64_t)m * ld + n;
-      float h[3];
-      float p = 0.f;
-      for (int z = 0; z < K; ++z) {
-        const float hz = H[z * plane + e];
-        if (z < 3) h[z] = hz;
-        p = z == 0 ? hz : p * hz;
-      }
+      float p = Hr[e];
+      for (int z = 1; z < K; ++z) p = p * Hr[z * plane + e];
       const float cdf = gelu_cdf(p);
       const float pdf = 0.39894228040143267794f * expf(-0.5f * p * p);
       const float gp = T[r * 33 + lane] * (cdf + p * pdf);
       for (int z = 0; z < K; ++z) {
         float g = gp;
-        for (int j = 0; j < K; ++j)
-          if (j != z) g = g * (j < 3 ? h[j] : H[j * plane + e]);
-        GH[z * plane + e] = g;
+        for (int jj = 0; jj < K; ++jj)
+          if (jj != z) g = g * Hr[jj * plane + e];
+        Gw[z * plane + e] = g;
       }
     }
   }
