@@ -309,6 +309,20 @@ static bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 // tcgen05 path eligibility: shapes that tile cleanly and 16-byte aligned
 // operands / strides (TMA).  The choice depends only on the config and the
 // buffer layout, so compress and decompress always take the same path.
+// EDPC_TC_MASK (debug): bit 0 forward linears, 1 branch GEMMs, 2 dgrads, 3 wgrads
+static int tc_mask() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EDPC_TC_MASK");
+    v = e ? atoi(e) : 15;
+  }
+  return v;
+}
+
+static bool tc_ok_m(edpc_ctx* c, int bit, int N, int Kchunk,
+                    std::initializer_list<const void*> ptrs,
+                    std::initializer_list<int64_t> strides);
+
 static bool tc_ok(edpc_ctx* c, int N, int Kchunk, std::initializer_list<const void*> ptrs,
                   std::initializer_list<int64_t> strides) {
   if (!c->use_tc || !tc_shape_ok(N, Kchunk)) return false;
@@ -317,6 +331,12 @@ static bool tc_ok(edpc_ctx* c, int N, int Kchunk, std::initializer_list<const vo
   for (int64_t s : strides)
     if (s % 4) return false;
   return true;
+}
+
+static bool tc_ok_m(edpc_ctx* c, int bit, int N, int Kchunk,
+                    std::initializer_list<const void*> ptrs,
+                    std::initializer_list<int64_t> strides) {
+  return (tc_mask() >> bit & 1) && tc_ok(c, N, Kchunk, ptrs, strides);
 }
 
 static cudaError_t as_cuda(int st) { return st == EDPC_OK ? cudaSuccess : cudaErrorUnknown; }
@@ -342,7 +362,7 @@ static cudaError_t splitk_reduce(edpc_ctx* c, int N, const float* bias, const fl
 static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, const float* w,
                               int N, int nzb, int64_t sW, float* out, int64_t sOut,
                               const float* bias, const float* resid, int M) {
-  if (tc_ok(c, N, Kd, {A, w, out, bias, resid ? resid : out}, {lda, N, sW, sOut})) {
+  if (tc_ok_m(c, 0, N, Kd, {A, w, out, bias, resid ? resid : out}, {lda, N, sW, sOut})) {
     TcOperand a{A, lda, 0, 1}, b{w, N, sW, nzb};
     if (nzb == 1 && M == c->Bl && use_split(N, Kd, Kd)) {
       TcShape s{M, N, Kd, 1, 1, kBatchNone, kBatchNone, 2, kSplitK, 0, 0, 0};
@@ -386,7 +406,7 @@ static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, in
   EpiPartial e{c->Gp, c->lay.n_shared, off, sOff, N, c->g_first};
   const int glanes = c->lay.B / kNumGroups;
   if (c->lay.B % kNumGroups == 0 && glanes % kTcBK == 0 &&
-      tc_ok(c, N, glanes, {X, G, c->Gp + off}, {Mw, N, sG, sOff, c->lay.n_shared})) {
+      tc_ok_m(c, 3, N, glanes, {X, G, c->Gp + off}, {Mw, N, sG, sOff, c->lay.n_shared})) {
     Scope sc(c, kRegGemm, c->st);
     TcShape s{Mw, N, c->Bl, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 1,
               c->g_count, c->g_first, c->lay.B, c->lane0};
@@ -439,7 +459,7 @@ static cudaError_t colsum(edpc_ctx* c, const float* src, int N, int nz, int64_t 
 template <class Epi>
 static cudaError_t dgrad(edpc_ctx* c, const float* G, int Kd, int nsum, int64_t sG_sum,
                          const float* w, int64_t sW_sum, int N, const Epi& epi) {
-  if (tc_ok(c, N, Kd, {G, w}, {Kd, sG_sum, sW_sum})) {
+  if (tc_ok_m(c, 2, N, Kd, {G, w}, {Kd, sG_sum, sW_sum})) {
     TcOperand a{G, Kd, sG_sum, nsum}, b{w, Kd, sW_sum, nsum};
     if constexpr (std::is_same<Epi, EpiStore>::value) {
       if (epi.ldc == N && use_split(N, (int64_t)Kd * nsum, Kd)) {
@@ -508,7 +528,7 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
   // branch GEMMs with the product + GeLU fused into the epilogue when all
   // branches of a tile fit one CTA's TMEM (k = 2, 3); else GEMM + k_mbrb_act
   if ((L.K == 2 || L.K == 3) && H % 128 == 0 &&
-      tc_ok(c, H, F, {b.x0, c->W + o.w0, b.H, b.ff, c->W + o.b0}, {F, H, o.wstride, plane})) {
+      tc_ok_m(c, 1, H, F, {b.x0, c->W + o.w0, b.H, b.ff, c->W + o.b0}, {F, H, o.wstride, plane})) {
     Scope sc(c, kRegGemm, c->st);
     TcShape s{Bl, H, F, L.K, 1, kBatchNone, kBatchZ, 0, 1, 0, 0, 0};
     TcOperand a{b.x0, F, 0, 1}, bw{c->W + o.w0, H, o.wstride, L.K};
