@@ -222,17 +222,13 @@ struct EpiBiasResid {
     const float b = bias[n];
     const float* __restrict__ R = resid;
     float* __restrict__ O = C;
-#pragma unroll 1
-    for (int r0 = 0; r0 < 32; r0 += 8) {
-      float rv[8];
+    float rv[32];
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
-        rv[r] = m_base + r0 + r < M ? R[(int64_t)(m_base + r0 + r) * ldr + n] : 0.f;
+    for (int r = 0; r < 32; ++r)
+      rv[r] = m_base + r < M ? R[(int64_t)(m_base + r) * ldr + n] : 0.f;
 #pragma unroll
-      for (int r = 0; r < 8; ++r)
-        if (m_base + r0 + r < M)
-          O[(int64_t)(m_base + r0 + r) * ldc + n] = (T[(r0 + r) * 33 + lane] + b) + rv[r];
-    }
+    for (int r = 0; r < 32; ++r)
+      if (m_base + r < M) O[(int64_t)(m_base + r) * ldc + n] = (T[r * 33 + lane] + b) + rv[r];
   }
 };
 

@@ -187,25 +187,23 @@ struct EpiBwdAct {
     const float* __restrict__ Hr = H;
     float* __restrict__ Gw = GH;
     if (K == 2 && m_base + 32 <= M) {
-#pragma unroll 1
-      for (int r0 = 0; r0 < 32; r0 += 8) {
-        float h0[8], h1[8];
+      // all 64 loads of the 32x32 block in flight before any compute
+      float h0[32], h1[32];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const int64_t e = (int64_t)(m_base + r0 + r) * ld + n;
-          h0[r] = Hr[e];
-          h1[r] = Hr[plane + e];
-        }
+      for (int r = 0; r < 32; ++r) {
+        const int64_t e = (int64_t)(m_base + r) * ld + n;
+        h0[r] = Hr[e];
+        h1[r] = Hr[plane + e];
+      }
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const int64_t e = (int64_t)(m_base + r0 + r) * ld + n;
-          const float p = h0[r] * h1[r];
-          const float cdf = gelu_cdf(p);
-          const float pdf = 0.39894228040143267794f * expf(-0.5f * p * p);
-          const float gp = T[(r0 + r) * 33 + lane] * (cdf + p * pdf);
-          Gw[e] = gp * h1[r];
-          Gw[plane + e] = gp * h0[r];
-        }
+      for (int r = 0; r < 32; ++r) {
+        const int64_t e = (int64_t)(m_base + r) * ld + n;
+        const float p = h0[r] * h1[r];
+        const float cdf = gelu_cdf(p);
+        const float pdf = 0.39894228040143267794f * expf(-0.5f * p * p);
+        const float gp = T[r * 33 + lane] * (cdf + p * pdf);
+        Gw[e] = gp * h1[r];
+        Gw[plane + e] = gp * h0[r];
       }
       return;
     }
