@@ -256,7 +256,7 @@ k_ln_bwd(const float* __restrict__ gx0, const float* __restrict__ xhat,
 // gx0 * xhat and gx0 for columns lane, lane+32, ...; warp sums are combined
 // in warp order, chunk sums in chunk order by the last block of the group
 // (ticket counter) -- a fixed order, so reproducible.
-constexpr int kLnChunk = 64;
+constexpr int kLnChunk = 16;
 constexpr int kLnMaxF = 512;
 
 __global__ void __launch_bounds__(256)
@@ -594,36 +594,91 @@ k_fdm_bwd_adam_v(const float* __restrict__ down, const float* __restrict__ gmix,
 // thread c (= byte value) walks the (lane, position) entries in order and
 // accumulates the matching rows.  chunk_tab[k] = {group, lane begin, end}.
 constexpr int kEmbChunkLanes = 16;
-constexpr int kEmbSmemFloats = 8192;  // 32 KB of gradient rows per chunk
+constexpr int kEmbSmemFloats = 4096;  // 16 KB of gradient rows per chunk
 
+// Block-local stable counting sort of the chunk's (lane, position) entries
+// by context byte: histogram (int atomics: order-free) -> exclusive scan ->
+// stable ranks from __match_any_sync + per-warp counts.  Thread c then sums
+// exactly its byte's rows in entry order -- the same order as a sequential
+// scan, so results do not depend on scheduling.
 __global__ void __launch_bounds__(256)
 k_embed_grad_chunks(ByteCols src, StepIdx si, int T, int DE, int F,
                     const float* __restrict__ gx, const int* __restrict__ chunk_tab,
                     float* __restrict__ sub) {
   __shared__ uint8_t cbytes[4096];
   __shared__ float grows[kEmbSmemFloats];
+  __shared__ int hist[256], off[256], run[256];
+  __shared__ int wcnt[8][256];
+  __shared__ short order[4096];
   const int k = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int lb = chunk_tab[3 * k + 1], le = chunk_tab[3 * k + 2];
   const int nl = le - lb;
+  const int n = nl * T;
   const int64_t col0 = *si.i - T;
-  for (int e = threadIdx.x; e < nl * T; e += blockDim.x) {
+  for (int e = tid; e < n; e += blockDim.x) {
     int bl = e / T, p = e - bl * T;
     cbytes[e] = src.base[(int64_t)(lb + bl) * src.ld + col0 + p];
   }
   const bool staged = nl * F <= kEmbSmemFloats;
   if (staged) {
     const float* g0 = gx + (int64_t)lb * F;
-    for (int e = threadIdx.x; e < nl * F; e += blockDim.x) grows[e] = g0[e];
+    for (int e = tid; e < nl * F; e += blockDim.x) grows[e] = g0[e];
+  }
+  hist[tid] = 0;
+  __syncthreads();
+  for (int e = tid; e < n; e += blockDim.x) atomicAdd(&hist[cbytes[e]], 1);
+  __syncthreads();
+  // exclusive scan of hist (256 entries, one per thread): warp scans + totals
+  {
+    const int h = hist[tid];
+    int incl = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (lane == 31) wcnt[0][warp] = incl;
+    __syncthreads();
+    int before = 0;
+    for (int w = 0; w < warp; ++w) before += wcnt[0][w];
+    off[tid] = before + incl - h;
+    run[tid] = before + incl - h;
   }
   __syncthreads();
-  const int c = threadIdx.x;
+  // stable positions, 256 entries per pass
+  for (int t0 = 0; t0 < n; t0 += 256) {
+    const int e = t0 + tid;
+    const bool live = e < n;
+    const int b = live ? cbytes[e] : 256 + lane;  // distinct dummies never match real bytes
+    const unsigned same = __match_any_sync(0xffffffffu, b);
+    const int lrank = __popc(same & ((1u << lane) - 1u));
+    for (int q = tid; q < 8 * 256; q += blockDim.x) (&wcnt[0][0])[q] = 0;
+    __syncthreads();
+    if (live && lrank == 0) wcnt[warp][b] = __popc(same);
+    __syncthreads();
+    if (live) {
+      int r = run[b] + lrank;
+      for (int w = 0; w < warp; ++w) r += wcnt[w][b];
+      order[r] = (short)e;
+    }
+    __syncthreads();
+    {  // advance the running per-byte counters past this pass
+      int add = 0;
+      for (int w = 0; w < 8; ++w) add += wcnt[w][tid];
+      run[tid] += add;
+    }
+    __syncthreads();
+  }
+  const int c = tid;
+  const int o0 = off[c], o1 = off[c] + hist[c];
   for (int d0 = 0; d0 < DE; d0 += 16) {
     float acc[16];
 #pragma unroll
     for (int d = 0; d < 16; ++d) acc[d] = 0.f;
-    for (int e = 0; e < nl * T; ++e) {
-      if (cbytes[e] != c) continue;
-      int bl = e / T, p = e - bl * T;
+    for (int q = o0; q < o1; ++q) {
+      const int e = order[q];
+      const int bl = e / T, p = e - bl * T;
       const float* g = staged ? grows + bl * F + p * DE + d0
                               : gx + (int64_t)(lb + bl) * F + p * DE + d0;
 #pragma unroll
