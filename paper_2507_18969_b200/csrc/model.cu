@@ -174,6 +174,8 @@ struct edpc_ctx {
   int g_first = 0, g_count = 0;  // local lane groups
   bool use_tc = false;
   cudaStream_t st = nullptr, st_enc = nullptr;
+  cudaStream_t st_aux = nullptr;  // weight-gradient GEMMs run here, joined before Adam
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr, tj = nullptr;
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
@@ -193,7 +195,9 @@ struct edpc_ctx {
   float *g_xhat, *g_rstd, *g_x0, *g_H, *g_ff, *x_global;
   float *logits, *probs, *nll;
   // backward temporaries
-  float *gl, *gA, *gB, *GH, *gx0, *gmix, *gdown, *emb_sub;
+  float *gl, *gx0, *gmix, *gdown, *emb_sub;
+  float *g_head, *g_lte, *g_loc, *g_emb;  // dL/d(x_global), d(x_lte), d(x_local), d(x_emb)
+  float *GH_g, *GH_l;                     // branch-output gradients per MBRB
   float* ws = nullptr;  // split-K workspace [kSplitK][Bl][<=256]
   float* ln_scratch = nullptr;  // LN-gradient chunk sums
   unsigned* ln_tickets = nullptr;
@@ -218,6 +222,7 @@ struct edpc_ctx {
   ~edpc_ctx() {
     if (st) cudaStreamSynchronize(st);
     if (st_enc) cudaStreamSynchronize(st_enc);
+    if (st_aux) cudaStreamSynchronize(st_aux);
     prof.flush();
     prof.release();
     for (auto& g : graph)
@@ -230,6 +235,9 @@ struct edpc_ctx {
     if (tj) cudaEventDestroy(tj);
     if (st) cudaStreamDestroy(st);
     if (st_enc) cudaStreamDestroy(st_enc);
+    if (st_aux) cudaStreamDestroy(st_aux);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
   }
 
   template <typename T>
@@ -395,19 +403,46 @@ static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, cons
 }
 
 static cudaError_t colsum(edpc_ctx* c, const float* src, int N, int nz, int64_t sz,
-                          const float* mul, int64_t off, int64_t sOff);
+                          const float* mul, int64_t off, int64_t sOff, cudaStream_t st = nullptr);
 
 // weight-gradient partials: Gp[g][off + z*sOff + m*N + n] = sum over group
 // g's lanes of X[b][m] * G[z][b][n], and (bias_off >= 0) the bias partials
 // Gp[g][bias_off + z*sOff + n] = sum over the group's lanes of G[z][b][n] --
 // on the tcgen05 path those come from the GEMM's own B tiles in shared memory.
+static bool aux_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EDPC_AUX_STREAM");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// work of the weight-gradient stream (joined back before the exchange / Adam)
+static cudaStream_t wst(edpc_ctx* c) { return aux_enabled() ? c->st_aux : c->st; }
+
+static cudaError_t fork_aux(edpc_ctx* c) {
+  if (!aux_enabled()) return cudaSuccess;
+  cudaError_t e = cudaEventRecord(c->ev_fork, c->st);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->st_aux, c->ev_fork, 0);
+  return e;
+}
+
+static cudaError_t join_aux(edpc_ctx* c) {
+  if (!aux_enabled()) return cudaSuccess;
+  cudaError_t e = cudaEventRecord(c->ev_join, c->st_aux);
+  if (e == cudaSuccess) e = cudaStreamWaitEvent(c->st, c->ev_join, 0);
+  return e;
+}
+
 static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, int N, int nzb,
                          int64_t sG, int64_t off, int64_t sOff, int64_t bias_off) {
   EpiPartial e{c->Gp, c->lay.n_shared, off, sOff, N, c->g_first};
+  cudaStream_t ws = wst(c);
   const int glanes = c->lay.B / kNumGroups;
   if (c->lay.B % kNumGroups == 0 && glanes % kTcBK == 0 &&
       tc_ok_m(c, 3, N, glanes, {X, G, c->Gp + off}, {Mw, N, sG, sOff, c->lay.n_shared})) {
-    Scope sc(c, kRegGemm, c->st);
+    Scope sc(c, kRegGemm, ws);
     TcShape s{Mw, N, c->Bl, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 1,
               c->g_count, c->g_first, c->lay.B, c->lane0};
     if (bias_off >= 0) {
@@ -417,10 +452,10 @@ static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, in
       s.bias_zstride = sOff;
     }
     TcOperand a{X, Mw, 0, 1}, b{G, N, sG, nzb};
-    return as_cuda(tc_gemm<true, true>(s, a, b, e, c->st));
+    return as_cuda(tc_gemm<true, true>(s, a, b, e, ws));
   }
   {
-    Scope sc(c, kRegGemm, c->st);
+    Scope sc(c, kRegGemm, ws);
     GemmShape g{};
     g.M = Mw;
     g.N = N;
@@ -436,21 +471,22 @@ static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, in
     g.g0 = c->g_first;
     g.B_global = c->lay.B;
     g.lane0 = c->lane0;
-    cudaError_t r = gemm_simt<true, false>(g, e, c->st);
+    cudaError_t r = gemm_simt<true, false>(g, e, ws);
     if (r != cudaSuccess) return r;
   }
-  if (bias_off >= 0) return colsum(c, G, N, nzb, sG, nullptr, bias_off, sOff);
+  if (bias_off >= 0) return colsum(c, G, N, nzb, sG, nullptr, bias_off, sOff, ws);
   return cudaSuccess;
 }
 
 // bias-gradient partials (column sums per lane group)
 static cudaError_t colsum(edpc_ctx* c, const float* src, int N, int nz, int64_t sz,
-                          const float* mul, int64_t off, int64_t sOff) {
+                          const float* mul, int64_t off, int64_t sOff, cudaStream_t st) {
   if (c->g_count == 0) return cudaSuccess;
+  if (!st) st = c->st;
   const int vec = (N % 4 == 0 && sz % 4 == 0 && al16(src) && (!mul || al16(mul))) ? 1 : 0;
   dim3 grid((unsigned)cdiv(N, 128), (unsigned)nz, (unsigned)c->g_count);
-  Scope sc(c, kRegColsum, c->st);
-  k_colsum_groups<<<grid, 256, 0, c->st>>>(src, N, sz, mul, N, c->Gp, c->lay.n_shared, off, sOff,
+  Scope sc(c, kRegColsum, st);
+  k_colsum_groups<<<grid, 256, 0, st>>>(src, N, sz, mul, N, c->Gp, c->lay.n_shared, off, sOff,
                                            c->g_first, c->lay.B, c->lane0, vec);
   return cudaGetLastError();
 }
@@ -602,18 +638,18 @@ static int softmax_quant(edpc_ctx* c, int mode, ByteCols src) {
 // g_up: gradient w.r.t. the block output [Bl][F]; writes the gradient w.r.t.
 // the block input into g_in
 static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, const float* g_up,
-                         float* g_in) {
+                         float* g_in, float* GH) {
   const Layout& L = c->lay;
   const int Bl = c->Bl, F = L.F, H = o.H, K = L.K;
   const int64_t plane = (int64_t)Bl * H;
   // g_ff = g_up . out_w^T, epilogue -> GH[z] (product rule + GeLU')
-  CK(dgrad(c, g_up, F, 1, 0, c->W + o.out_w, 0, H, EpiBwdAct{b.H, c->GH, K, plane, H}));
-  // out_w / out_b gradients
+  CK(dgrad(c, g_up, F, 1, 0, c->W + o.out_w, 0, H, EpiBwdAct{b.H, GH, K, plane, H}));
+  // weight gradients on the side stream: out_w/out_b, branch weights/biases
+  CK(fork_aux(c));
   CK(wgrad(c, b.ff, H, g_up, F, 1, 0, o.out_w, 0, o.out_b));
-  // branch weights / biases
-  CK(wgrad(c, b.x0, F, c->GH, H, K, plane, o.w0, o.wstride, o.b0));
+  CK(wgrad(c, b.x0, F, GH, H, K, plane, o.w0, o.wstride, o.b0));
   // g_x0 = sum_z GH[z] . W_z^T
-  CK(dgrad(c, c->GH, H, K, plane, c->W + o.w0, o.wstride, F, EpiStore{c->gx0, F}));
+  CK(dgrad(c, GH, H, K, plane, c->W + o.w0, o.wstride, F, EpiStore{c->gx0, F}));
   // LN backward + residual, with the LN gain / bias gradient partials
   if (F <= kLnMaxF && c->g_count > 0) {
     int maxg = 0;
@@ -646,14 +682,16 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   }
   CK(cudaGetLastError());
   // head
+  CK(fork_aux(c));
   CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0, L.head_b));
-  CK(dgrad(c, c->gl, 256, 1, 0, c->W + L.head_w, 0, F, EpiStore{c->gA, F}));
-  // global MBRB: gA -> gB
+  CK(dgrad(c, c->gl, 256, 1, 0, c->W + L.head_w, 0, F, EpiStore{c->g_head, F}));
+  // global MBRB: d(x_global) -> d(x_lte)
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
-  EDPC_TRY(mbrb_backward(c, L.glo, gb, c->gA, c->gB));
+  EDPC_TRY(mbrb_backward(c, L.glo, gb, c->g_head, c->g_lte, c->GH_g));
   // LTE up
-  CK(wgrad(c, c->mixed, FP, c->gB, F, 1, 0, L.up_w, 0, L.up_b));
-  CK(dgrad(c, c->gB, F, 1, 0, c->W + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
+  CK(fork_aux(c));
+  CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
+  CK(dgrad(c, c->g_lte, F, 1, 0, c->W + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
   // per-lane FDM: g_down with the old U, then U's Adam step (fused)
   {
     Scope sc_(c, kRegFdmBwd, c->st);
@@ -680,17 +718,18 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   }
   CK(cudaGetLastError());
   // LTE down
+  CK(fork_aux(c));
   CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
-  CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore{c->gA, F}));
-  // local MBRB: gA -> gB (gradient w.r.t. the embedded context)
+  CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore{c->g_loc, F}));
+  // local MBRB: d(x_local) -> d(x_emb) (gradient w.r.t. the embedded context)
   MbrbBufs lb{c->x_emb, c->l_xhat, c->l_rstd, c->l_x0, c->l_H, c->l_ff, c->x_local};
-  EDPC_TRY(mbrb_backward(c, L.loc, lb, c->gA, c->gB));
+  EDPC_TRY(mbrb_backward(c, L.loc, lb, c->g_loc, c->g_emb, c->GH_l));
   // embedding scatter-add as per-group partials
   if (c->n_chunks > 0) {
     {
       Scope sc_(c, kRegEmbed, c->st);
       k_embed_grad_chunks<<<(unsigned)c->n_chunks, 256, 0, c->st>>>(src, c->si(), L.T, L.DE, F,
-                                                                    c->gB, c->chunk_tab, c->emb_sub);
+                                                                    c->g_emb, c->chunk_tab, c->emb_sub);
     }
     CK(cudaGetLastError());
     dim3 gr((unsigned)cdiv(256 * L.DE, 256), (unsigned)c->g_count);
@@ -701,6 +740,7 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
     }
     CK(cudaGetLastError());
   }
+  CK(join_aux(c));
   return EDPC_OK;
 }
 
@@ -884,14 +924,16 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
   };
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->st_enc, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->st_aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     set_error("stream/event creation failed");
     return fail(EDPC_ERR_CUDA);
   }
   const Layout& L = c->lay;
   const int Bl = c->Bl;
   const int64_t F = L.F, FP = L.FP;
-  const int Hm = std::max(L.HL, L.HG);
 #define A_(p, n)                        \
   do {                                  \
     int _r = c->alloc(&(p), (n));       \
@@ -928,9 +970,12 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
   A_(c->probs, (int64_t)Bl * 256);
   A_(c->nll, Bl);
   A_(c->gl, (int64_t)Bl * 256);
-  A_(c->gA, Bl * F);
-  A_(c->gB, Bl * F);
-  A_(c->GH, (int64_t)L.K * Bl * Hm);
+  A_(c->g_head, Bl * F);
+  A_(c->g_lte, Bl * F);
+  A_(c->g_loc, Bl * F);
+  A_(c->g_emb, Bl * F);
+  A_(c->GH_g, (int64_t)L.K * Bl * L.HG);
+  A_(c->GH_l, (int64_t)L.K * Bl * L.HL);
   A_(c->gx0, Bl * F);
   A_(c->gmix, Bl * FP);
   A_(c->gdown, Bl * FP);
@@ -1447,6 +1492,7 @@ int edpc_prof(edpc_ctx* c, int enable) {
   EDPC_CHECK_ARG(c, "null ctx");
   EDPC_CUDA_TRY(cudaSetDevice(c->device));
   cudaStreamSynchronize(c->st);
+  cudaStreamSynchronize(c->st_aux);
   cudaStreamSynchronize(c->st_enc);
   c->prof.reset();
   c->prof.on = enable != 0;
@@ -1458,6 +1504,7 @@ int edpc_prof_read(edpc_ctx* c, int32_t region, double* ms, int64_t* count) {
   EDPC_CHECK_ARG(region >= -1 && region < kNumRegions, "bad region");
   EDPC_CUDA_TRY(cudaSetDevice(c->device));
   cudaStreamSynchronize(c->st);
+  cudaStreamSynchronize(c->st_aux);
   cudaStreamSynchronize(c->st_enc);
   c->prof.flush();
   if (region < 0) {
@@ -1545,7 +1592,7 @@ int edpc_debug_read(edpc_ctx* c, int32_t which, float* out, int64_t count) {
     case 4: src = c->x_global; n = Bl * L.F; break;
     case 5: src = c->l_H; n = (int64_t)L.K * Bl * L.HL; break;
     case 6: src = c->g_H; n = (int64_t)L.K * Bl * L.HG; break;
-    case 7: src = c->gB; n = Bl * L.F; break;
+    case 7: src = c->g_emb; n = Bl * L.F; break;
     case 8: src = c->logits; n = Bl * 256; break;
     default: EDPC_CHECK_ARG(false, "unknown debug buffer");
   }
@@ -1557,6 +1604,7 @@ int edpc_debug_read(edpc_ctx* c, int32_t which, float* out, int64_t count) {
 int edpc_sync(edpc_ctx* c) {
   EDPC_CHECK_ARG(c, "null ctx");
   EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st_aux));
   EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
   EDPC_CUDA_TRY(cudaStreamSynchronize(c->st_enc));
   return EDPC_OK;
