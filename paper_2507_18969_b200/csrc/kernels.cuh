@@ -558,31 +558,50 @@ k_fdm_bwd_adam_v(const float* __restrict__ down, const float* __restrict__ gmix,
   float4* u4 = reinterpret_cast<float4*>(U + (int64_t)bb * FP * FP);
   float4* m4 = reinterpret_cast<float4*>(Um + (int64_t)bb * FP * FP);
   float4* v4 = reinterpret_cast<float4*>(Uv + (int64_t)bb * FP * FP);
-#pragma unroll 2
-  for (int i = 0; i < FP; ++i) {
-    const float di = d[i];
-    float part = 0.f;
+  // rows in batches of 8: all 24 float4 loads of a batch are in flight
+  // before the Adam math; the 8 row-dot reductions follow the stores
+  constexpr int kR = 8;
+#pragma unroll 1
+  for (int i0 = 0; i0 < FP; i0 += kR) {
+    float4 w[kR][G::kNV], m[kR][G::kNV], q[kR][G::kNV];
 #pragma unroll
-    for (int v = 0; v < G::kNV; ++v) {
-      const int e = (i * FP) / 4 + v * G::kTPR + t;
-      float4 w = u4[e], m = m4[e], q = v4[e];
-      part = fmaf(g[v].x, w.x, part);
-      part = fmaf(g[v].y, w.y, part);
-      part = fmaf(g[v].z, w.z, part);
-      part = fmaf(g[v].w, w.w, part);
-      adam_elem(w.x, m.x, q.x, di * g[v].x, c, bc1, bc2);
-      adam_elem(w.y, m.y, q.y, di * g[v].y, c, bc1, bc2);
-      adam_elem(w.z, m.z, q.z, di * g[v].z, c, bc1, bc2);
-      adam_elem(w.w, m.w, q.w, di * g[v].w, c, bc1, bc2);
-      if (live) {
-        u4[e] = w;
-        m4[e] = m;
-        v4[e] = q;
+    for (int r = 0; r < kR; ++r)
+#pragma unroll
+      for (int v = 0; v < G::kNV; ++v) {
+        const int e = ((i0 + r) * FP) / 4 + v * G::kTPR + t;
+        w[r][v] = u4[e];
+        m[r][v] = m4[e];
+        q[r][v] = v4[e];
+      }
+    float part[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      const float di = d[i0 + r];
+      part[r] = 0.f;
+#pragma unroll
+      for (int v = 0; v < G::kNV; ++v) {
+        part[r] = fmaf(g[v].x, w[r][v].x, part[r]);
+        part[r] = fmaf(g[v].y, w[r][v].y, part[r]);
+        part[r] = fmaf(g[v].z, w[r][v].z, part[r]);
+        part[r] = fmaf(g[v].w, w[r][v].w, part[r]);
+        adam_elem(w[r][v].x, m[r][v].x, q[r][v].x, di * g[v].x, c, bc1, bc2);
+        adam_elem(w[r][v].y, m[r][v].y, q[r][v].y, di * g[v].y, c, bc1, bc2);
+        adam_elem(w[r][v].z, m[r][v].z, q[r][v].z, di * g[v].z, c, bc1, bc2);
+        adam_elem(w[r][v].w, m[r][v].w, q[r][v].w, di * g[v].w, c, bc1, bc2);
+        if (live) {
+          const int e = ((i0 + r) * FP) / 4 + v * G::kTPR + t;
+          u4[e] = w[r][v];
+          m4[e] = m[r][v];
+          v4[e] = q[r][v];
+        }
       }
     }
 #pragma unroll
-    for (int o = G::kTPR / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    if (live && t == 0) gdown[(int64_t)b * FP + i] = part;
+    for (int r = 0; r < kR; ++r) {
+#pragma unroll
+      for (int o = G::kTPR / 2; o > 0; o >>= 1) part[r] += __shfl_xor_sync(0xffffffffu, part[r], o);
+      if (live && t == 0) gdown[(int64_t)b * FP + i0 + r] = part[r];
+    }
   }
 }
 
