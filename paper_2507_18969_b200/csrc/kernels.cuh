@@ -71,13 +71,34 @@ k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE,
   if (lane == 0) rstd[b] = r;
 }
 
-// ff = GeLU(prod_i H_i) (model.py:98-101, _kernels.py:35-42)
-__global__ void k_mbrb_act(const float* __restrict__ H, int K, int64_t plane, float* __restrict__ ff) {
+constexpr int kMaxBranches = 8;
+
+__device__ __forceinline__ float gelu_dcdf(float p, float cdf) {
+  return cdf + p * (0.39894228040143267794f * expf(-0.5f * p * p));
+}
+
+// ff = GeLU(prod_z H_z) (model.py:98-101, _kernels.py:35-42).  H_z is then
+// overwritten with D_z = GeLU'(prod) * prod_{j != z} H_j, everything the
+// backward product rule needs (model.py:107-119): g_H_z = g_ff * D_z.
+__global__ void k_mbrb_act(float* __restrict__ H, int K, int64_t plane, float* __restrict__ ff) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= plane) return;
+  float h[kMaxBranches];
   float p = H[e];
-  for (int z = 1; z < K; ++z) p = p * H[z * plane + e];
-  ff[e] = p * gelu_cdf(p);
+  h[0] = p;
+  for (int z = 1; z < K; ++z) {
+    h[z] = H[z * plane + e];
+    p = p * h[z];
+  }
+  const float cdf = gelu_cdf(p);
+  ff[e] = p * cdf;
+  const float dg = gelu_dcdf(p, cdf);
+  for (int z = 0; z < K; ++z) {
+    float d = dg;
+    for (int j = 0; j < K; ++j)
+      if (j != z) d = d * h[j];
+    H[z * plane + e] = d;
+  }
 }
 
 // MBRB forward epilogue of the multi-branch GEMM (model.py:97-101): H_z =
@@ -96,17 +117,35 @@ struct EpiBranchAct {
       load32(b0 + z * sBias + n0, b);
 #pragma unroll
       for (int j = 0; j < 32; ++j) v[z][j] = v[z][j] + b[j];
-      store32(H + z * plane + (int64_t)m * N + n0, v[z]);
 #pragma unroll
       for (int j = 0; j < 32; ++j) p[j] = z == 0 ? v[0][j] : p[j] * v[z][j];
     }
+    float f[32];
 #pragma unroll
-    for (int j = 0; j < 32; ++j) p[j] = p[j] * gelu_cdf(p[j]);
-    store32(ff + (int64_t)m * N + n0, p);
+    for (int j = 0; j < 32; ++j) {
+      const float cdf = gelu_cdf(p[j]);
+      f[j] = p[j] * cdf;
+      p[j] = gelu_dcdf(p[j], cdf);
+    }
+    store32(ff + (int64_t)m * N + n0, f);
+#pragma unroll
+    for (int z = 0; z < ZIN; ++z) {
+      float d[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        d[j] = p[j];
+#pragma unroll
+        for (int y = 0; y < ZIN; ++y)
+          if (y != z) d[j] = d[j] * v[y][j];
+      }
+      store32(H + z * plane + (int64_t)m * N + n0, d);
+    }
   }
   __device__ void row32(int, int, int, int, float (&)[32]) const {}
   __device__ void tile(const float*, int, int, int, int, int) const {}
-  // T holds ZIN transposed 32x32 blocks (branch z at T + z*32*33)
+  // T holds ZIN transposed 32x32 blocks (branch z at T + z*32*33).  Stores
+  // ff and D_z = GeLU'(prod) * prod_{j != z} H_j (the backward's product-rule
+  // factors) -- the backward epilogue is then g_H_z = g_ff * D_z.
   __device__ void tile_z(const float* T, int m_base, int n0, int M) const {
     const int lane = threadIdx.x & 31;
     const int n = n0 + lane;
@@ -118,113 +157,68 @@ struct EpiBranchAct {
       const int m = m_base + r;
       if (m >= M) break;
       const int64_t e = (int64_t)m * N + n;
+      float h[ZIN];
       float p = 0.f;
 #pragma unroll
       for (int z = 0; z < ZIN; ++z) {
-        const float h = T[z * 32 * 33 + r * 33 + lane] + b[z];
-        H[z * plane + e] = h;
-        p = z == 0 ? h : p * h;
+        h[z] = T[z * 32 * 33 + r * 33 + lane] + b[z];
+        p = z == 0 ? h[0] : p * h[z];
       }
-      ff[e] = p * gelu_cdf(p);
+      const float cdf = gelu_cdf(p);
+      ff[e] = p * cdf;
+      const float dg = gelu_dcdf(p, cdf);
+#pragma unroll
+      for (int z = 0; z < ZIN; ++z) {
+        float d = dg;
+#pragma unroll
+        for (int y = 0; y < ZIN; ++y)
+          if (y != z) d = d * h[y];
+        H[z * plane + e] = d;
+      }
     }
   }
 };
 
 // MBRB backward epilogue of the out-projection dgrad (model.py:107-119):
-// g_prod = g_ff * GeLU'(prod); g_H_z = g_prod * prod_{j != z} H_j
+// g_H_z = g_ff * D_z with D_z = GeLU'(prod) * prod_{j != z} H_j stored by
+// the forward (k_mbrb_act / EpiBranchAct) in place of H_z.
 struct EpiBwdAct {
-  const float* H;
+  const float* H;  // holds D_z
   float* GH;
   int K;
   int64_t plane, ld;
   __device__ void operator()(int, int, int m, int n, float acc) const {
     const int64_t e = (int64_t)m * ld + n;
-    float p = H[e];
-    for (int z = 1; z < K; ++z) p = p * H[z * plane + e];
-    const float cdf = gelu_cdf(p);
-    const float pdf = 0.39894228040143267794f * expf(-0.5f * p * p);
-    const float gp = acc * (cdf + p * pdf);
-    for (int z = 0; z < K; ++z) {
-      float g = gp;
-      for (int j = 0; j < K; ++j)
-        if (j != z) g = g * H[j * plane + e];
-      GH[z * plane + e] = g;
-    }
+    for (int z = 0; z < K; ++z) GH[z * plane + e] = acc * H[z * plane + e];
   }
   __device__ void row32(int, int, int m, int n0, float (&acc)[32]) const {
     const int64_t e = (int64_t)m * ld + n0;
-    float p[32], h[32];
-    load32(H + e, p);
-    for (int z = 1; z < K; ++z) {
-      load32(H + z * plane + e, h);
-#pragma unroll
-      for (int j = 0; j < 32; ++j) p[j] = p[j] * h[j];
-    }
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const float cdf = gelu_cdf(p[j]);
-      const float pdf = 0.39894228040143267794f * expf(-0.5f * p[j] * p[j]);
-      acc[j] = acc[j] * (cdf + p[j] * pdf);  // g_prod
-    }
     for (int z = 0; z < K; ++z) {
-      float g[32];
+      float d[32];
+      load32(H + z * plane + e, d);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) g[j] = acc[j];
-      for (int jj = 0; jj < K; ++jj) {
-        if (jj == z) continue;
-        load32(H + jj * plane + e, h);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) g[j] = g[j] * h[j];
-      }
-      store32(GH + z * plane + e, g);
+      for (int j = 0; j < 32; ++j) d[j] = acc[j] * d[j];
+      store32(GH + z * plane + e, d);
     }
   }
-  // rows in batches of 8: all H loads of a batch are issued before any
-  // GH store (the stores could otherwise alias the loads for the compiler)
+  // all loads of the 32x32 block in flight before the stores
   __device__ void tile(const float* T, int, int, int m_base, int n0, int M) const {
     const int lane = threadIdx.x & 31;
     const int n = n0 + lane;
-    const float* __restrict__ Hr = H;
+    const float* __restrict__ Dr = H;
     float* __restrict__ Gw = GH;
-    if (K == 2 && m_base + 32 <= M) {
-      // all 64 loads of the 32x32 block in flight before any compute
-      float h0[32], h1[32];
+    for (int z = 0; z < K; ++z) {
+      float d[32];
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const int64_t e = (int64_t)(m_base + r) * ld + n;
-        h0[r] = Hr[e];
-        h1[r] = Hr[plane + e];
-      }
+      for (int r = 0; r < 32; ++r)
+        d[r] = m_base + r < M ? Dr[z * plane + (int64_t)(m_base + r) * ld + n] : 0.f;
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const int64_t e = (int64_t)(m_base + r) * ld + n;
-        const float p = h0[r] * h1[r];
-        const float cdf = gelu_cdf(p);
-        const float pdf = 0.39894228040143267794f * expf(-0.5f * p * p);
-        const float gp = T[r * 33 + lane] * (cdf + p * pdf);
-        Gw[e] = gp * h1[r];
-        Gw[plane + e] = gp * h0[r];
-      }
-      return;
-    }
-    for (int r = 0; r < 32; ++r) {
-      const int m = m_base + r;
-      if (m >= M) break;
-      const int64_t e = (int64_t)m * ld + n;
-      float p = Hr[e];
-      for (int z = 1; z < K; ++z) p = p * Hr[z * plane + e];
-      const float cdf = gelu_cdf(p);
-      const float pdf = 0.39894228040143267794f * expf(-0.5f * p * p);
-      const float gp = T[r * 33 + lane] * (cdf + p * pdf);
-      for (int z = 0; z < K; ++z) {
-        float g = gp;
-        for (int jj = 0; jj < K; ++jj)
-          if (jj != z) g = g * Hr[jj * plane + e];
-        Gw[z * plane + e] = g;
-      }
+      for (int r = 0; r < 32; ++r)
+        if (m_base + r < M) Gw[z * plane + (int64_t)(m_base + r) * ld + n] = T[r * 33 + lane] * d[r];
     }
   }
 };
+
 
 // LN backward + residual (nn.py:116-125, model.py:120-121); one warp per lane
 __global__ void __launch_bounds__(256)

@@ -301,6 +301,7 @@ static int check_cfg(const edpc_config* c) {
   EDPC_CHECK_ARG(c->context_len >= 1, "context_len must be >= 1");
   EDPC_CHECK_ARG(c->embed_dim >= 1, "embed_dim must be >= 1");
   EDPC_CHECK_ARG(c->branches >= 1, "branches must be >= 1");
+  EDPC_CHECK_ARG(c->branches <= kMaxBranches, "branches > 8 unsupported");
   EDPC_CHECK_ARG(c->lanes >= 1, "lanes must be >= 1");
   EDPC_CHECK_ARG(c->hidden_local >= 1 && c->hidden_global >= 1, "hidden dims must be >= 1");
   int64_t f = (int64_t)c->context_len * c->embed_dim;
