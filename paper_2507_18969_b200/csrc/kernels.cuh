@@ -207,6 +207,23 @@ struct EpiBwdAct {
     const int n = n0 + lane;
     const float* __restrict__ Dr = H;
     float* __restrict__ Gw = GH;
+    if (K == 2 && m_base + 32 <= M) {
+      float d0[32], d1[32];
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int64_t e = (int64_t)(m_base + r) * ld + n;
+        d0[r] = Dr[e];
+        d1[r] = Dr[plane + e];
+      }
+#pragma unroll
+      for (int r = 0; r < 32; ++r) {
+        const int64_t e = (int64_t)(m_base + r) * ld + n;
+        const float a = T[r * 33 + lane];
+        Gw[e] = a * d0[r];
+        Gw[plane + e] = a * d1[r];
+      }
+      return;
+    }
     for (int z = 0; z < K; ++z) {
       float d[32];
 #pragma unroll
