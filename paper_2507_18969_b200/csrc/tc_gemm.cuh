@@ -79,6 +79,44 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+// TMA load multicast to the CTAs of the cluster in cta_mask (same smem offset
+// and mbarrier offset in every destination CTA)
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c0, int c1, int c2, uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+// arrive on the mbarrier at the same offset in cluster CTA `rank`
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote)
+               : "memory");
+}
+
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
@@ -217,7 +255,11 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 //               chunks): tcgen05.ld -> fused epilogue -> global
 //   warps 10-13 (BIAS only) column sums of the B tile of every k-block of
 //               the tiles with tm == 0, read straight from the smem ring
-template <int BN, bool AMN, bool BMN, bool BIAS, class Epi, int ZIN = 1>
+// CL = 2: CTA pairs (clusters of 2 along x) own m-tiles 2p and 2p+1 of the
+// same (tn, z); each CTA TMA-multicasts one half of the shared B tile to
+// both, so per-SM operand traffic per k-block drops from A+B to A+B/2.
+// Stage reuse then needs both CTAs' MMA commits (and bias reads).
+template <int BN, bool AMN, bool BMN, bool BIAS, class Epi, int ZIN = 1, int CL = 1>
 __global__ void __launch_bounds__(tc_threads(BIAS), 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
           TcShape s, Epi epi) {
@@ -239,13 +281,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   const int n_tn = s.N / BN;
   const int n_tm = (s.M + kTcBM - 1) / kTcBM;
   const int nzt = (ZIN > 1 ? 1 : s.nzb) * (s.kmode == 0 ? 1 : s.nsplit);
-  const int n_tiles = n_tn * n_tm * nzt;
+  const int crank = CL > 1 ? (int)cluster_rank() : 0;
+  const int n_tmu = n_tm / CL;               // m-tile units (pairs when CL = 2)
+  const int n_tiles = n_tn * n_tmu * nzt;    // work units
+  const int u0 = blockIdx.x / CL, ustride = gridDim.x / CL;
+  constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
 
   auto tile_coords = [&](int t, int& tn, int& tm, int& zb, int& zg, int& kb0, int& nkb) {
     tn = t % n_tn;
     const int r = t / n_tn;
-    tm = r % n_tm;
-    const int z = r / n_tm;
+    tm = (r % n_tmu) * CL + crank;
+    const int z = r / n_tmu;
     const int nzb = ZIN > 1 ? 1 : s.nzb;
     zb = z % nzb;
     zg = z / nzb;
@@ -265,7 +311,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   if (warp == 0 && lane == 0) {
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&full[st], 1);
-      mbar_init(&empty[st], BIAS ? 2 : 1);
+      mbar_init(&empty[st], CL * (BIAS ? 2 : 1));
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -282,6 +328,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // peer barriers initialised before any multicast
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -289,7 +336,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
     if (lane == 0) {
       // ---------------- TMA producer
       int it = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      for (int t = u0; t < n_tiles; t += ustride) {
         int tn, tm, zb, zg, kb0, nkb;
         tile_coords(t, tn, tm, zb, zg, kb0, nkb);
         const int n0 = tn * BN, m0 = tm * kTcBM;
@@ -315,12 +362,28 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
           for (int zi = 0; zi < ZIN; ++zi) {
             const int bzz = ZIN > 1 ? zi : bz;
             uint8_t* sbz = sb + zi * SM::kBBytes;
-            if (BMN) {
+            if constexpr (CL == 1) {
+              if (BMN) {
 #pragma unroll
-              for (int j = 0; j < BN / 32; ++j)
-                tma_load_3d(sbz + j * 4096, &tma_b, &full[st], n0 + 32 * j, k, bzz);
+                for (int j = 0; j < BN / 32; ++j)
+                  tma_load_3d(sbz + j * 4096, &tma_b, &full[st], n0 + 32 * j, k, bzz);
+              } else {
+                tma_load_3d(sbz, &tma_b, &full[st], k, n0, bzz);
+              }
             } else {
-              tma_load_3d(sbz, &tma_b, &full[st], k, n0, bzz);
+              // this CTA's half of B, multicast into both CTAs of the pair
+              if (BMN) {
+                constexpr int nb = BN / 32 / CL;
+#pragma unroll
+                for (int jj = 0; jj < nb; ++jj) {
+                  const int j = crank * nb + jj;
+                  tma_load_3d_mc(sbz + j * 4096, &tma_b, &full[st], n0 + 32 * j, k, bzz, kMask);
+                }
+              } else {
+                constexpr int rows = BN / CL;
+                tma_load_3d_mc(sbz + crank * rows * 128, &tma_b, &full[st], k, n0 + crank * rows,
+                               bzz, kMask);
+              }
             }
           }
         }
@@ -331,7 +394,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       // ---------------- MMA issuer
       constexpr uint32_t idesc = idesc_tf32(kTcBM, BN, AMN ? 1 : 0, BMN ? 1 : 0);
       int it = 0, lt = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+      for (int t = u0; t < n_tiles; t += ustride, ++lt) {
         int tn, tm, zb, zg, kb0, nkb;
         tile_coords(t, tn, tm, zb, zg, kb0, nkb);
         const int acc = lt & 1;
@@ -357,7 +420,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
               tc_mma_tf32(dtm + (uint32_t)(zi * BN), ad, bd, idesc, (q > 0 || kk > 0) ? 1u : 0u);
             }
           }
-          tc_commit(&empty[st]);
+          if constexpr (CL == 1)
+            tc_commit(&empty[st]);
+          else
+            tc_commit_mc(&empty[st], kMask);
         }
         tc_commit(&tfull[acc]);
       }
@@ -367,7 +433,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;
     int lt = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++lt) {
+    for (int t = u0; t < n_tiles; t += ustride, ++lt) {
       int tn, tm, zb, zg, kb0, nkb;
       tile_coords(t, tn, tm, zb, zg, kb0, nkb);
       const int acc = lt & 1;
@@ -416,7 +482,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
     const int bt = threadIdx.x - 32 * (2 + kTcEpiWarps);  // 0..127
     constexpr int kCols = BN / (32 * kTcBiasWarps) > 0 ? BN / (32 * kTcBiasWarps) : 1;
     int it = 0;
-    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+    for (int t = u0; t < n_tiles; t += ustride) {
       int tn, tm, zb, zg, kb0, nkb;
       tile_coords(t, tn, tm, zb, zg, kb0, nkb);
       const bool do_sum = tm == 0 && s.bias_part != nullptr;
@@ -443,7 +509,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
           }
         }
         named_bar(1, 32 * kTcBiasWarps);
-        if (bt == 0) mbar_arrive(&empty[st]);
+        if (bt == 0) {
+          if constexpr (CL == 1) {
+            mbar_arrive(&empty[st]);
+          } else {
+#pragma unroll
+            for (int r = 0; r < CL; ++r) mbar_arrive_cluster(&empty[st], (uint32_t)r);
+          }
+        }
       }
       if (do_sum) {
 #pragma unroll
@@ -458,6 +531,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   }
   tc_fence_before();
   __syncthreads();
+  if (CL > 1) cluster_sync_all();  // no CTA leaves while its peer may still signal it
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -565,9 +639,47 @@ inline int num_sms() {
   return dev < 16 && n[dev] ? n[dev] : 148;
 }
 
+inline bool cluster_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EDPC_CLUSTER");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename Kern, typename Epi>
+inline cudaError_t launch_tc(Kern kern, int grid, int threads, int smem, cudaStream_t st, int cl,
+                             const CUtensorMap& ta, const CUtensorMap& tb, const TcShape& s,
+                             const Epi& epi) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)cl;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, s, epi);
+}
+
+template <typename Kern>
+inline void set_smem_attr(Kern kern, int bytes, bool& done) {
+  if (!done) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    done = true;
+  }
+}
+
 template <int BN, bool AMN, bool BMN, class Epi>
 inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, const Epi& epi,
                      cudaStream_t st) {
+  const int n_tm = cdiv(s.M, kTcBM);
+  const int cl = (cluster_enabled() && n_tm % 2 == 0) ? 2 : 1;
   CUtensorMap ta, tb;
   int r;
   // A: K-major -> [M rows][K inner]; MN-major -> [K rows][M inner]
@@ -578,43 +690,53 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
     r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.K, (uint64_t)s.M, (uint64_t)A.nbatch,
                          (uint64_t)A.ld, (uint64_t)A.sbatch, 32, kTcBM, false);
   if (r != EDPC_OK) return r;
-  // B: K-major -> [N rows][K inner]; MN-major -> [K rows][N inner]
+  // B: K-major -> [N rows][K inner] (box BN/cl rows); MN-major -> [K rows][N inner]
   if (BMN)
     r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.N, (uint64_t)s.K, (uint64_t)B.nbatch,
                          (uint64_t)B.ld, (uint64_t)B.sbatch, 32, 32, true);
   else
     r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.K, (uint64_t)s.N, (uint64_t)B.nbatch,
-                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN, false);
+                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN / cl, false);
   if (r != EDPC_OK) return r;
   const int nz = s.nzb * (s.kmode == 0 ? 1 : s.nsplit);
-  const int n_tiles = (s.N / BN) * cdiv(s.M, kTcBM) * nz;
-  const int grid = n_tiles < num_sms() ? n_tiles : num_sms();
-  static bool attr_done[2][16] = {};
+  const int units = (s.N / BN) * (n_tm / cl) * nz;
+  const int max_units = num_sms() / cl;
+  const int grid = (units < max_units ? units : max_units) * cl;
   int dev = 0;
   cudaGetDevice(&dev);
-  cudaError_t e;
+  const int di = dev < 16 ? dev : 0;
+  cudaError_t e = cudaSuccess;
   bool launched = false;
   if constexpr (BMN) {
     if (s.bias_part) {
-      auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi>;
-      if (dev < 16 && !attr_done[1][dev]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             TcSmem<BN>::kBytes);
-        attr_done[1][dev] = true;
+      if (cl == 2) {
+        static bool done[16] = {};
+        auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi, 1, 2>;
+        set_smem_attr(kern, TcSmem<BN>::kBytes, done[di]);
+        e = launch_tc(kern, grid, tc_threads(true), TcSmem<BN>::kBytes, st, 2, ta, tb, s, epi);
+      } else {
+        static bool done[16] = {};
+        auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi, 1, 1>;
+        set_smem_attr(kern, TcSmem<BN>::kBytes, done[di]);
+        e = launch_tc(kern, grid, tc_threads(true), TcSmem<BN>::kBytes, st, 1, ta, tb, s, epi);
       }
-      kern<<<grid, tc_threads(true), TcSmem<BN>::kBytes, st>>>(ta, tb, s, epi);
       launched = true;
     }
   }
   if (!launched) {
-    auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi>;
-    if (dev < 16 && !attr_done[0][dev]) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, TcSmem<BN>::kBytes);
-      attr_done[0][dev] = true;
+    if (cl == 2) {
+      static bool done[16] = {};
+      auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi, 1, 2>;
+      set_smem_attr(kern, TcSmem<BN>::kBytes, done[di]);
+      e = launch_tc(kern, grid, tc_threads(false), TcSmem<BN>::kBytes, st, 2, ta, tb, s, epi);
+    } else {
+      static bool done[16] = {};
+      auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi, 1, 1>;
+      set_smem_attr(kern, TcSmem<BN>::kBytes, done[di]);
+      e = launch_tc(kern, grid, tc_threads(false), TcSmem<BN>::kBytes, st, 1, ta, tb, s, epi);
     }
-    kern<<<grid, tc_threads(false), TcSmem<BN>::kBytes, st>>>(ta, tb, s, epi);
   }
-  e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_tc_gemm launch: ") + cudaGetErrorString(e));
     return EDPC_ERR_CUDA;
@@ -626,6 +748,8 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
 template <int BN, int ZIN, bool BMN, class Epi>
 inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& B,
                          const Epi& epi, cudaStream_t st) {
+  const int n_tm = cdiv(s.M, kTcBM);
+  const int cl = (cluster_enabled() && n_tm % 2 == 0) ? 2 : 1;
   CUtensorMap ta, tb;
   int r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.K, (uint64_t)s.M, (uint64_t)A.nbatch,
                            (uint64_t)A.ld, (uint64_t)A.sbatch, 32, kTcBM, false);
@@ -635,21 +759,27 @@ inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& 
                          (uint64_t)B.ld, (uint64_t)B.sbatch, 32, 32, true);
   else
     r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.K, (uint64_t)s.N, (uint64_t)B.nbatch,
-                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN, false);
+                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN / cl, false);
   if (r != EDPC_OK) return r;
-  const int n_tiles = (s.N / BN) * cdiv(s.M, kTcBM);
-  const int grid = n_tiles < num_sms() ? n_tiles : num_sms();
-  auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN>;
-  static bool attr_done[16] = {};
+  const int units = (s.N / BN) * (n_tm / cl);
+  const int max_units = num_sms() / cl;
+  const int grid = (units < max_units ? units : max_units) * cl;
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 16 && !attr_done[dev]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         TcSmem<BN, ZIN>::kBytes);
-    attr_done[dev] = true;
+  const int di = dev < 16 ? dev : 0;
+  cudaError_t e;
+  if (cl == 2) {
+    static bool done[16] = {};
+    auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 2>;
+    set_smem_attr(kern, TcSmem<BN, ZIN>::kBytes, done[di]);
+    e = launch_tc(kern, grid, tc_threads(false), TcSmem<BN, ZIN>::kBytes, st, 2, ta, tb, s, epi);
+  } else {
+    static bool done[16] = {};
+    auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 1>;
+    set_smem_attr(kern, TcSmem<BN, ZIN>::kBytes, done[di]);
+    e = launch_tc(kern, grid, tc_threads(false), TcSmem<BN, ZIN>::kBytes, st, 1, ta, tb, s, epi);
   }
-  kern<<<grid, tc_threads(false), TcSmem<BN, ZIN>::kBytes, st>>>(ta, tb, s, epi);
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_tc_gemm<zin> launch: ") + cudaGetErrorString(e));
     return EDPC_ERR_CUDA;
