@@ -639,11 +639,13 @@ inline int num_sms() {
   return dev < 16 && n[dev] ? n[dev] : 148;
 }
 
+// 2-CTA multicast clusters: correct, but measured slower on these shapes
+// (the GEMMs are not L2-bandwidth bound), so opt-in via EDPC_CLUSTER=1.
 inline bool cluster_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("EDPC_CLUSTER");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
 }
