@@ -200,6 +200,7 @@ struct EpiBias {
 
 // C = acc + bias + resid (MBRB out-projection + residual, model.py:102)
 struct EpiBiasResid {
+  static constexpr bool kTransposed = true;
   float* C;
   int64_t ldc;
   const float* bias;

@@ -183,6 +183,7 @@ struct EpiBranchAct {
 // g_H_z = g_ff * D_z with D_z = GeLU'(prod) * prod_{j != z} H_j stored by
 // the forward (k_mbrb_act / EpiBranchAct) in place of H_z.
 struct EpiBwdAct {
+  static constexpr bool kTransposed = true;
   const float* H;  // holds D_z
   float* GH;
   int K;

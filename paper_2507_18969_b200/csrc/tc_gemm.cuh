@@ -27,6 +27,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -216,12 +217,24 @@ struct TcShape {
 constexpr int kTcEpiWarpsC = 8;
 constexpr int kTcTileFloats = 32 * 33;
 
-template <int BN, int ZIN = 1>
+// Epilogue functors that read extra inputs (residual, product-rule factors)
+// set kTransposed and get the smem transpose; store-only epilogues keep the
+// shared memory for one more pipeline stage.
+template <class Epi, class = void>
+struct EpiTransposed {
+  static constexpr bool value = false;
+};
+template <class Epi>
+struct EpiTransposed<Epi, std::void_t<decltype(Epi::kTransposed)>> {
+  static constexpr bool value = Epi::kTransposed;
+};
+
+template <int BN, int ZIN = 1, bool TR = true>
 struct TcSmem {
   static constexpr int kABytes = kTcBM * kTcBK * 4;  // 16 KB
   static constexpr int kBBytes = BN * kTcBK * 4;
   static constexpr int kStageBytes = kABytes + ZIN * kBBytes;
-  static constexpr int kEpiBytes = kTcEpiWarpsC * ZIN * kTcTileFloats * 4;
+  static constexpr int kEpiBytes = TR ? kTcEpiWarpsC * ZIN * kTcTileFloats * 4 : 0;
   static constexpr int kFixed = 1024 /*align*/ + 256 /*barriers*/ + kEpiBytes;
   static constexpr int kStages = (4 * kStageBytes + kFixed <= 232448) ? 4 : 3;
   static constexpr int kEpiOffset = kStages * kStageBytes;
@@ -266,8 +279,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   static_assert(!BIAS || BMN, "fused bias sums read an MN-major B tile");
   static_assert(ZIN == 1 || !BIAS, "multi-branch tiles have no fused bias");
   static_assert(TcSmem<BN, ZIN>::kCols <= 512, "TMEM holds 512 columns");
+  constexpr bool TR = ZIN > 1 || EpiTransposed<Epi>::value;
   extern __shared__ uint8_t smem_raw[];
-  using SM = TcSmem<BN, ZIN>;
+  using SM = TcSmem<BN, ZIN, TR>;
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr int kStages = SM::kStages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::kBarOffset);
@@ -446,13 +460,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       const int m_base = tm * kTcBM + quad * 32;
 #pragma unroll 1
       for (int c = half * 32; c < BN; c += 64) {
-#pragma unroll
-        for (int zi = 0; zi < ZIN; ++zi) {
+        if constexpr (!TR) {
           float v[32];
           if (any) {
-            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) +
-                          (uint32_t)((acc * ZIN + zi) * BN + c),
-                      v);
+            tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(acc * BN + c), v);
           } else {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0.f;
@@ -461,17 +472,35 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = (float)(m * 1000 + n0 + c + j);
           }
+          if (m < s.M) epi.row32(zb, zg, m, n0 + c, v);
+        } else {
 #pragma unroll
-          for (int j = 0; j < 32; ++j) T[zi * kTcTileFloats + lane * 33 + j] = v[j];
+          for (int zi = 0; zi < ZIN; ++zi) {
+            float v[32];
+            if (any) {
+              tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) +
+                            (uint32_t)((acc * ZIN + zi) * BN + c),
+                        v);
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = 0.f;
+            }
+            if (s.dbg == 1) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = (float)(m * 1000 + n0 + c + j);
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) T[zi * kTcTileFloats + lane * 33 + j] = v[j];
+          }
+          __syncwarp();
+          if (m_base < s.M) {
+            if constexpr (ZIN == 1)
+              epi.tile(T, zb, zg, m_base, n0 + c, s.M);
+            else
+              epi.tile_z(T, m_base, n0 + c, s.M);
+          }
+          __syncwarp();
         }
-        __syncwarp();
-        if (m_base < s.M) {
-          if constexpr (ZIN == 1)
-            epi.tile(T, zb, zg, m_base, n0 + c, s.M);
-          else
-            epi.tile_z(T, m_base, n0 + c, s.M);
-        }
-        __syncwarp();
       }
       tc_fence_before();
       __syncwarp();
@@ -680,6 +709,7 @@ inline void set_smem_attr(Kern kern, int bytes, bool& done) {
 template <int BN, bool AMN, bool BMN, class Epi>
 inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, const Epi& epi,
                      cudaStream_t st) {
+  constexpr int kSmem = TcSmem<BN, 1, EpiTransposed<Epi>::value>::kBytes;
   const int n_tm = cdiv(s.M, kTcBM);
   const int cl = (cluster_enabled() && n_tm % 2 == 0) ? 2 : 1;
   CUtensorMap ta, tb;
@@ -714,13 +744,13 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
       if (cl == 2) {
         static bool done[16] = {};
         auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi, 1, 2>;
-        set_smem_attr(kern, TcSmem<BN>::kBytes, done[di]);
-        e = launch_tc(kern, grid, tc_threads(true), TcSmem<BN>::kBytes, st, 2, ta, tb, s, epi);
+        set_smem_attr(kern, kSmem, done[di]);
+        e = launch_tc(kern, grid, tc_threads(true), kSmem, st, 2, ta, tb, s, epi);
       } else {
         static bool done[16] = {};
         auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi, 1, 1>;
-        set_smem_attr(kern, TcSmem<BN>::kBytes, done[di]);
-        e = launch_tc(kern, grid, tc_threads(true), TcSmem<BN>::kBytes, st, 1, ta, tb, s, epi);
+        set_smem_attr(kern, kSmem, done[di]);
+        e = launch_tc(kern, grid, tc_threads(true), kSmem, st, 1, ta, tb, s, epi);
       }
       launched = true;
     }
@@ -729,13 +759,13 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
     if (cl == 2) {
       static bool done[16] = {};
       auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi, 1, 2>;
-      set_smem_attr(kern, TcSmem<BN>::kBytes, done[di]);
-      e = launch_tc(kern, grid, tc_threads(false), TcSmem<BN>::kBytes, st, 2, ta, tb, s, epi);
+      set_smem_attr(kern, kSmem, done[di]);
+      e = launch_tc(kern, grid, tc_threads(false), kSmem, st, 2, ta, tb, s, epi);
     } else {
       static bool done[16] = {};
       auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi, 1, 1>;
-      set_smem_attr(kern, TcSmem<BN>::kBytes, done[di]);
-      e = launch_tc(kern, grid, tc_threads(false), TcSmem<BN>::kBytes, st, 1, ta, tb, s, epi);
+      set_smem_attr(kern, kSmem, done[di]);
+      e = launch_tc(kern, grid, tc_threads(false), kSmem, st, 1, ta, tb, s, epi);
     }
   }
   if (e == cudaSuccess) e = cudaGetLastError();
