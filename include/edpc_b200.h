@@ -168,6 +168,9 @@ int edpc_sync(edpc_ctx* ctx);
  * 5 local branch outputs [k][B][h_l], 6 global branch outputs, 7 d(embedded
  * context), 8 logits.  count must equal the buffer's element count. */
 int edpc_debug_read(edpc_ctx* ctx, int32_t which, float* out, int64_t count);
+/* bare tcgen05 GEMM microbenchmark on device operands (avg ms per launch) */
+int edpc_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn, int32_t nsplit,
+                    int32_t iters, double* ms);
 /* one GEMM through the tcgen05 path on host arrays (tests):
  * C[M][N] = A . B, A [M][K] (a_mn 0) or [K][M] (a_mn 1), B [N][K] (b_mn 0)
  * or [K][N] (b_mn 1) */

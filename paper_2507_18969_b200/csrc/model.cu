@@ -1577,6 +1577,59 @@ int edpc_debug_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn,
   return EDPC_OK;
 }
 
+__global__ void k_fill_rand(float* p, int64_t n, uint32_t seed) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u ^ seed;
+    h ^= h >> 15;
+    h *= 2246822519u;
+    h ^= h >> 13;
+    p[i] = (float)(h & 0xffff) / 65536.0f - 0.5f;
+  }
+}
+
+// Microbenchmark of the bare tcgen05 GEMM (store-only epilogue) on device
+// operands: average ms over iters launches (CUDA events).  kmode 2 splits K.
+int edpc_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn, int32_t nsplit,
+                    int32_t iters, double* ms) {
+  EDPC_CHECK_ARG(ms && M > 0 && N > 0 && K > 0 && iters > 0 && nsplit >= 1, "bad arguments");
+  EDPC_CHECK_ARG(tc_shape_ok(N, K / nsplit), "shape not supported by the tcgen05 path");
+  float *dA, *dB, *dC;
+  EDPC_CUDA_TRY(cudaMalloc(&dA, (size_t)M * K * 4));
+  EDPC_CUDA_TRY(cudaMalloc(&dB, (size_t)N * K * 4));
+  EDPC_CUDA_TRY(cudaMalloc(&dC, (size_t)nsplit * M * N * 4));
+  k_fill_rand<<<1024, 256>>>(dA, (int64_t)M * K, 1u);
+  k_fill_rand<<<1024, 256>>>(dB, (int64_t)N * K, 2u);
+  TcShape s{M, N, K, 1, 1, kBatchNone, kBatchNone, nsplit > 1 ? 2 : 0, nsplit, 0, 0, 0};
+  TcOperand a{dA, a_mn ? M : K, 0, 1}, b{dB, b_mn ? N : K, 0, 1};
+  EpiSplit e{dC, N, (int64_t)M * N};
+  auto run = [&]() {
+    if (!a_mn && !b_mn) return tc_gemm<false, false>(s, a, b, e, 0);
+    if (!a_mn && b_mn) return tc_gemm<false, true>(s, a, b, e, 0);
+    if (a_mn && !b_mn) return tc_gemm<true, false>(s, a, b, e, 0);
+    return tc_gemm<true, true>(s, a, b, e, 0);
+  };
+  int st = run();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, 0);
+  for (int i = 0; i < iters && st == EDPC_OK; ++i) st = run();
+  cudaEventRecord(e1, 0);
+  cudaError_t ce = cudaEventSynchronize(e1);
+  float t = 0.f;
+  cudaEventElapsedTime(&t, e0, e1);
+  *ms = t / iters;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dC);
+  if (st != EDPC_OK) return st;
+  EDPC_CUDA_TRY(ce);
+  return EDPC_OK;
+}
+
 int edpc_debug_read(edpc_ctx* c, int32_t which, float* out, int64_t count) {
   EDPC_CHECK_ARG(c && out, "null argument");
   EDPC_CUDA_TRY(cudaSetDevice(c->device));
