@@ -156,7 +156,8 @@ def test_ratio_within_half_percent_of_oracle_desk_dims():
     assert abs(r_gpu / r_ref - 1) <= RATIO_TOL, (r_gpu, r_ref)
 
 
-@pytest.mark.parametrize("name", ["desk_text_256k", "c2mini_text_4m", "c1_text_1m"])
+@pytest.mark.parametrize("name", ["desk_text_256k", "c2mini_text_4m", "c1_text_1m",
+                                  "c1_text_1m_s1", "c1_text_1m_s2"])
 def test_ratio_within_half_percent_of_reference_run(name):
     """Anchored on a run of the unmodified reference (tests/golden/ref_ratio_*.json)."""
     path = os.path.join(os.path.dirname(__file__), "golden", f"ref_ratio_{name}.json")
