@@ -127,7 +127,7 @@ class Clocks:
 
 # --------------------------------------------------------------- CPU oracle
 
-def cpu_sample(wl, min_seconds: float, max_steps: int, warm: int = 1):
+def cpu_sample(wl, min_seconds: float, max_steps: int, warm: int = 1, exact: bool = False):
     """Step-sampled CPU oracle at the workload's exact (B, dims)."""
     from oracle import coder as oc
     from oracle.model import OracleModel
@@ -155,7 +155,7 @@ def cpu_sample(wl, min_seconds: float, max_steps: int, warm: int = 1):
         i += 1
     t0 = time.perf_counter()
     n = 0
-    while n < max_steps and (n < 2 or time.perf_counter() - t0 < min_seconds):
+    while n < max_steps and (n < 2 or exact or time.perf_counter() - t0 < min_seconds):
         step(i)
         i += 1
         n += 1
@@ -177,7 +177,7 @@ def run_reference(args, wl):
     if rank != 0:
         return
     B = wl["lanes"]
-    r = cpu_sample(wl, min_seconds=0.0, max_steps=args.steps, warm=args.warmup)
+    r = cpu_sample(wl, min_seconds=0.0, max_steps=args.steps, warm=args.warmup, exact=True)
     # treat each model step as one bench step (a bounded sample of the workload)
     line = dict(metric=METRIC, value=r["value"], unit="MB/s", n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=r["seconds_per_step"] * 1e3,

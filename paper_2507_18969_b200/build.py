@@ -69,7 +69,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             f.write(log)
     objs = [o for o, _ in results]
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lnccl"]
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

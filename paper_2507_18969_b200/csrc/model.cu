@@ -17,6 +17,7 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
 #include <nccl.h>
 
 #include "common.cuh"
@@ -25,6 +26,41 @@
 #include "tc_gemm.cuh"
 
 namespace edpc {
+
+// NCCL is resolved at run time (dlopen of whatever libnccl.so.2 the process
+// already has -- e.g. torch's -- or the system one), only when a context joins
+// a communicator, so the library never drags an NCCL into processes that do
+// not use multi-GPU and never conflicts with torch's bundled NCCL.
+struct NcclApi {
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char* (*getErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy &&
+               api.getErrorString;
+    }
+  }
+  return api;
+}
+
 
 struct MbrbOffs {
   int64_t ln_g, ln_b, w0, b0, wstride, out_w, out_b;
@@ -227,7 +263,7 @@ struct edpc_ctx {
     prof.release();
     for (auto& g : graph)
       if (g) cudaGraphExecDestroy(g);
-    if (comm) ncclCommDestroy(comm);
+    if (comm) nccl().commDestroy(comm);
     for (void* p : allocs) cudaFree(p);
     if (ev) cudaEventDestroy(ev);
     if (t0) cudaEventDestroy(t0);
@@ -763,10 +799,10 @@ static int adam_shared(edpc_ctx* c) {
 static int exchange_partials(edpc_ctx* c) {
   if (!c->comm || c->nranks < 2) return EDPC_OK;
   const size_t cnt = (size_t)c->g_count * c->lay.n_shared;
-  ncclResult_t r = ncclAllGather(c->Gp + (size_t)c->g_first * c->lay.n_shared, c->Gp, cnt,
-                                 ncclFloat, c->comm, c->st);
+  ncclResult_t r = nccl().allGather(c->Gp + (size_t)c->g_first * c->lay.n_shared, c->Gp, cnt,
+                                    ncclFloat, c->comm, c->st);
   if (r != ncclSuccess) {
-    set_error(std::string("ncclAllGather: ") + ncclGetErrorString(r));
+    set_error(std::string("ncclAllGather: ") + nccl().getErrorString(r));
     return EDPC_ERR_CUDA;
   }
   return EDPC_OK;
@@ -1458,10 +1494,14 @@ int edpc_ctx_groups(edpc_ctx* c, int32_t* g_first, int32_t* g_count) {
 
 int edpc_nccl_unique_id(uint8_t* out, int32_t cap) {
   EDPC_CHECK_ARG(out && cap >= (int32_t)sizeof(ncclUniqueId), "buffer too small");
+  if (!nccl().ok) {
+    set_error("libnccl.so.2 not loadable");
+    return EDPC_ERR_CUDA;
+  }
   ncclUniqueId id;
-  ncclResult_t r = ncclGetUniqueId(&id);
+  ncclResult_t r = nccl().getUniqueId(&id);
   if (r != ncclSuccess) {
-    set_error(std::string("ncclGetUniqueId: ") + ncclGetErrorString(r));
+    set_error(std::string("ncclGetUniqueId: ") + nccl().getErrorString(r));
     return EDPC_ERR_CUDA;
   }
   memcpy(out, &id, sizeof(id));
@@ -1482,13 +1522,17 @@ int edpc_ctx_set_comm(edpc_ctx* c, const uint8_t* id, int32_t nranks, int32_t ra
   EDPC_CUDA_TRY(cudaSetDevice(c->device));
   ncclUniqueId uid;
   memcpy(&uid, id, sizeof(uid));
-  ncclComm_t comm;
-  ncclResult_t r = ncclCommInitRank(&comm, nranks, uid, rank);
-  if (r != ncclSuccess) {
-    set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+  if (!nccl().ok) {
+    set_error("libnccl.so.2 not loadable");
     return EDPC_ERR_CUDA;
   }
-  if (c->comm) ncclCommDestroy(c->comm);
+  ncclComm_t comm;
+  ncclResult_t r = nccl().commInitRank(&comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    set_error(std::string("ncclCommInitRank: ") + nccl().getErrorString(r));
+    return EDPC_ERR_CUDA;
+  }
+  if (c->comm) nccl().commDestroy(c->comm);
   c->comm = comm;
   c->nranks = nranks;
   c->rank = rank;

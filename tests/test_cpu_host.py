@@ -207,3 +207,14 @@ def test_product_package_never_imports_oracle():
         if fn.endswith(".py"):
             src = open(os.path.join(pkg, fn)).read()
             assert "import oracle" not in src and "from oracle" not in src, fn
+
+
+def test_library_does_not_preload_a_conflicting_nccl():
+    """torch must still import after the library is loaded (NCCL is dlopen'ed
+    lazily, only for multi-GPU, so torch's bundled NCCL wins)."""
+    import subprocess
+    import sys
+    code = ("import sys; sys.path.insert(0, %r); from paper_2507_18969_b200 import _lib; "
+            "_lib.load(); import torch; print('ok')" % ROOT)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
