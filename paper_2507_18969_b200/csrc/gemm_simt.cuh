@@ -161,7 +161,7 @@ __device__ __forceinline__ void store32(float* dst, const float (&v)[32]) {
 }
 
 // tcgen05 epilogues see a 32x32 block transposed into shared memory:
-// T[r * 33 + j] = D(m_base + r, n0 + j); lane j walks the 32 rows of column
+// T[r * 32 + (j ^ r)] = D(m_base + r, n0 + j); lane j walks the 32 rows of column
 // n0 + j, so each warp access is one coalesced 128-byte row segment.
 #define EDPC_TILE_ROWS(BODY)                                  \
   {                                                           \
@@ -169,7 +169,7 @@ __device__ __forceinline__ void store32(float* dst, const float (&v)[32]) {
     _Pragma("unroll 4") for (int r = 0; r < 32; ++r) {        \
       const int m = m_base + r;                               \
       if (m >= M) break;                                      \
-      const float acc = T[r * 33 + lane_];                    \
+      const float acc = T[r * 32 + (lane_ ^ r)];              \
       BODY                                                    \
     }                                                         \
   }
@@ -229,7 +229,7 @@ struct EpiBiasResid {
       rv[r] = m_base + r < M ? R[(int64_t)(m_base + r) * ldr + n] : 0.f;
 #pragma unroll
     for (int r = 0; r < 32; ++r)
-      if (m_base + r < M) O[(int64_t)(m_base + r) * ldc + n] = (T[r * 33 + lane] + b) + rv[r];
+      if (m_base + r < M) O[(int64_t)(m_base + r) * ldc + n] = (T[r * 32 + (lane ^ r)] + b) + rv[r];
   }
 };
 

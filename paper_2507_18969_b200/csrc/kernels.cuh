@@ -74,7 +74,7 @@ k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE,
 constexpr int kMaxBranches = 8;
 
 __device__ __forceinline__ float gelu_dcdf(float p, float cdf) {
-  return cdf + p * (0.39894228040143267794f * expf(-0.5f * p * p));
+  return cdf + p * (0.39894228040143267794f * __expf(-0.5f * p * p));
 }
 
 // ff = GeLU(prod_z H_z) (model.py:98-101, _kernels.py:35-42).  H_z is then
@@ -161,7 +161,7 @@ struct EpiBranchAct {
       float p = 0.f;
 #pragma unroll
       for (int z = 0; z < ZIN; ++z) {
-        h[z] = T[z * 32 * 33 + r * 33 + lane] + b[z];
+        h[z] = T[z * 1024 + r * 32 + (lane ^ r)] + b[z];
         p = z == 0 ? h[0] : p * h[z];
       }
       const float cdf = gelu_cdf(p);
@@ -219,7 +219,7 @@ struct EpiBwdAct {
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
         const int64_t e = (int64_t)(m_base + r) * ld + n;
-        const float a = T[r * 33 + lane];
+        const float a = T[r * 32 + (lane ^ r)];
         Gw[e] = a * d0[r];
         Gw[plane + e] = a * d1[r];
       }
@@ -232,7 +232,7 @@ struct EpiBwdAct {
         d[r] = m_base + r < M ? Dr[z * plane + (int64_t)(m_base + r) * ld + n] : 0.f;
 #pragma unroll
       for (int r = 0; r < 32; ++r)
-        if (m_base + r < M) Gw[z * plane + (int64_t)(m_base + r) * ld + n] = T[r * 33 + lane] * d[r];
+        if (m_base + r < M) Gw[z * plane + (int64_t)(m_base + r) * ld + n] = T[r * 32 + (lane ^ r)] * d[r];
     }
   }
 };

@@ -214,8 +214,9 @@ struct TcShape {
 // Epilogue warps transpose each 32x32 accumulator block through shared
 // memory (padded rows of 33) so that every global load/store of the
 // epilogue is a coalesced 128-byte row segment.
-constexpr int kTcEpiWarpsC = 8;
-constexpr int kTcTileFloats = 32 * 33;
+// 32x32 transpose scratch, XOR-swizzled (element (r, c) at r*32 + (c ^ r)):
+// conflict-free row writes and column reads without padding
+constexpr int kTcTileFloats = 32 * 32;
 
 // Epilogue functors that read extra inputs (residual, product-rule factors)
 // set kTransposed and get the smem transpose; store-only epilogues keep the
@@ -229,14 +230,16 @@ struct EpiTransposed<Epi, std::void_t<decltype(Epi::kTransposed)>> {
   static constexpr bool value = Epi::kTransposed;
 };
 
-template <int BN, int ZIN = 1, bool TR = true>
+template <int BN, int ZIN = 1, bool TR = true, int EW = 8>
 struct TcSmem {
   static constexpr int kABytes = kTcBM * kTcBK * 4;  // 16 KB
   static constexpr int kBBytes = BN * kTcBK * 4;
   static constexpr int kStageBytes = kABytes + ZIN * kBBytes;
-  static constexpr int kEpiBytes = TR ? kTcEpiWarpsC * ZIN * kTcTileFloats * 4 : 0;
+  static constexpr int kEpiBytes = TR ? EW * ZIN * kTcTileFloats * 4 : 0;
   static constexpr int kFixed = 1024 /*align*/ + 256 /*barriers*/ + kEpiBytes;
-  static constexpr int kStages = (4 * kStageBytes + kFixed <= 232448) ? 4 : 3;
+  static constexpr int kStages = (4 * kStageBytes + kFixed <= 232448)   ? 4
+                                 : (3 * kStageBytes + kFixed <= 232448) ? 3
+                                                                        : 2;
   static constexpr int kEpiOffset = kStages * kStageBytes;
   static constexpr int kBarOffset = kEpiOffset + kEpiBytes;
   static constexpr int kBytes = kStages * kStageBytes + kFixed;
@@ -245,10 +248,9 @@ struct TcSmem {
       kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
 };
 
-constexpr int kTcEpiWarps = 8;
 constexpr int kTcBiasWarps = 4;
-__host__ __device__ constexpr int tc_threads(bool bias) {
-  return 32 * (2 + kTcEpiWarps + (bias ? kTcBiasWarps : 0));
+__host__ __device__ constexpr int tc_threads(bool bias, int ew = 8) {
+  return 32 * (2 + ew + (bias ? kTcBiasWarps : 0));
 }
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -272,16 +274,18 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 // same (tn, z); each CTA TMA-multicasts one half of the shared B tile to
 // both, so per-SM operand traffic per k-block drops from A+B to A+B/2.
 // Stage reuse then needs both CTAs' MMA commits (and bias reads).
-template <int BN, bool AMN, bool BMN, bool BIAS, class Epi, int ZIN = 1, int CL = 1>
-__global__ void __launch_bounds__(tc_threads(BIAS), 1)
+template <int BN, bool AMN, bool BMN, bool BIAS, class Epi, int ZIN = 1, int CL = 1, int EW = 8>
+__global__ void __launch_bounds__(tc_threads(BIAS, EW), 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
           TcShape s, Epi epi) {
   static_assert(!BIAS || BMN, "fused bias sums read an MN-major B tile");
   static_assert(ZIN == 1 || !BIAS, "multi-branch tiles have no fused bias");
   static_assert(TcSmem<BN, ZIN>::kCols <= 512, "TMEM holds 512 columns");
   constexpr bool TR = ZIN > 1 || EpiTransposed<Epi>::value;
+  constexpr int kTcEpiWarps = EW;  // epilogue warps: EW / 4 per TMEM lane quadrant
+  static_assert(EW % 4 == 0, "whole TMEM lane quadrants per epilogue warp group");
   extern __shared__ uint8_t smem_raw[];
-  using SM = TcSmem<BN, ZIN, TR>;
+  using SM = TcSmem<BN, ZIN, TR, EW>;
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr int kStages = SM::kStages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::kBarOffset);
@@ -445,7 +449,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   } else if (warp < 2 + kTcEpiWarps) {
     // ---------------- epilogue warps (TMEM lane quadrant = warp % 4)
     const int quad = warp & 3;
-    const int half = (warp - 2) >> 2;
+    const int half = (warp - 2) >> 2;  // which of the EW/4 warps of this quadrant
     int lt = 0;
     for (int t = u0; t < n_tiles; t += ustride, ++lt) {
       int tn, tm, zb, zg, kb0, nkb;
@@ -459,7 +463,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       float* T = reinterpret_cast<float*>(smem + SM::kEpiOffset) + (warp - 2) * ZIN * kTcTileFloats;
       const int m_base = tm * kTcBM + quad * 32;
 #pragma unroll 1
-      for (int c = half * 32; c < BN; c += 64) {
+      for (int c = half * 32; c < BN; c += 32 * (EW / 4)) {
         if constexpr (!TR) {
           float v[32];
           if (any) {
@@ -490,7 +494,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
               for (int j = 0; j < 32; ++j) v[j] = (float)(m * 1000 + n0 + c + j);
             }
 #pragma unroll
-            for (int j = 0; j < 32; ++j) T[zi * kTcTileFloats + lane * 33 + j] = v[j];
+            for (int j = 0; j < 32; ++j) T[zi * kTcTileFloats + lane * 32 + (j ^ lane)] = v[j];
           }
           __syncwarp();
           if (m_base < s.M) {
@@ -780,6 +784,8 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
 template <int BN, int ZIN, bool BMN, class Epi>
 inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& B,
                          const Epi& epi, cudaStream_t st) {
+  // the fused GeLU epilogue is issue-bound: 16 epilogue warps (4 per quadrant)
+  constexpr int kZinEW = (BN % 128 == 0) ? 16 : 8;
   const int n_tm = cdiv(s.M, kTcBM);
   const int cl = (cluster_enabled() && n_tm % 2 == 0) ? 2 : 1;
   CUtensorMap ta, tb;
@@ -802,14 +808,14 @@ inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& 
   cudaError_t e;
   if (cl == 2) {
     static bool done[16] = {};
-    auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 2>;
-    set_smem_attr(kern, TcSmem<BN, ZIN>::kBytes, done[di]);
-    e = launch_tc(kern, grid, tc_threads(false), TcSmem<BN, ZIN>::kBytes, st, 2, ta, tb, s, epi);
+    auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 2, kZinEW>;
+    set_smem_attr(kern, TcSmem<BN, ZIN, true, kZinEW>::kBytes, done[di]);
+    e = launch_tc(kern, grid, tc_threads(false, kZinEW), TcSmem<BN, ZIN, true, kZinEW>::kBytes, st, 2, ta, tb, s, epi);
   } else {
     static bool done[16] = {};
-    auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 1>;
-    set_smem_attr(kern, TcSmem<BN, ZIN>::kBytes, done[di]);
-    e = launch_tc(kern, grid, tc_threads(false), TcSmem<BN, ZIN>::kBytes, st, 1, ta, tb, s, epi);
+    auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 1, kZinEW>;
+    set_smem_attr(kern, TcSmem<BN, ZIN, true, kZinEW>::kBytes, done[di]);
+    e = launch_tc(kern, grid, tc_threads(false, kZinEW), TcSmem<BN, ZIN, true, kZinEW>::kBytes, st, 1, ta, tb, s, epi);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
