@@ -826,10 +826,22 @@ inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& 
 }
 
 // BN dispatch: the widest tile <= 256 that divides N
+inline int bn_cap() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EDPC_BN_MAX");  // tuning knob (tests / microbenchmarks)
+    v = e ? atoi(e) : 256;
+  }
+  return v;
+}
+
 template <bool AMN, bool BMN, class Epi>
 inline int tc_gemm(const TcShape& s, const TcOperand& A, const TcOperand& B, const Epi& epi,
                    cudaStream_t st) {
-  if (s.N % 256 == 0) return tc_launch<256, AMN, BMN>(s, A, B, epi, st);
+  const int cap = bn_cap();
+  if (cap >= 256 && s.N % 256 == 0) return tc_launch<256, AMN, BMN>(s, A, B, epi, st);
+  if (cap >= 128 && s.N % 128 == 0) return tc_launch<128, AMN, BMN>(s, A, B, epi, st);
+  if (cap >= 64 && s.N % 64 == 0) return tc_launch<64, AMN, BMN>(s, A, B, epi, st);
   if (s.N == 128) return tc_launch<128, AMN, BMN>(s, A, B, epi, st);
   if (s.N == 64) return tc_launch<64, AMN, BMN>(s, A, B, epi, st);
   if (s.N == 32) return tc_launch<32, AMN, BMN>(s, A, B, epi, st);
