@@ -17,6 +17,7 @@
 #include <stdint.h>
 
 #include "common.cuh"
+#include "tc_types.cuh"
 
 namespace edpc {
 
@@ -176,10 +177,24 @@ __device__ __forceinline__ void store32(float* dst, const float (&v)[32]) {
 
 // C[zb] = acc + bias[zb] (row-broadcast); ldc row stride, sC batch stride
 struct EpiBias {
+  static constexpr bool kTmaStore = true;
   float* C;
   int64_t ldc, sC;
   const float* bias;
   int64_t sBias;
+  bool store_maps(const TcShape& s, TcStoreMap& c, TcStoreMap&) const {
+    c = TcStoreMap{C, {(uint64_t)s.N, (uint64_t)s.M, (uint64_t)s.nzb, 1},
+                   {(uint64_t)ldc, (uint64_t)sC, 0}};
+    return true;
+  }
+  template <class IO>
+  __device__ void ts_chunk(IO& io, int zb, int, int, int n0, float (&v)[1][32]) const {
+    float b[32];
+    load32(bias + zb * sBias + n0, b);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[0][j] = v[0][j] + b[j];
+    io.put(0, v[0], zb, 0);
+  }
   __device__ void operator()(int zb, int, int m, int n, float acc) const {
     C[zb * sC + (int64_t)m * ldc + n] = acc + bias[zb * sBias + n];
   }
@@ -235,8 +250,17 @@ struct EpiBiasResid {
 
 // plain store (dgrad outputs)
 struct EpiStore {
+  static constexpr bool kTmaStore = true;
   float* C;
   int64_t ldc;
+  bool store_maps(const TcShape& s, TcStoreMap& c, TcStoreMap&) const {
+    c = TcStoreMap{C, {(uint64_t)s.N, (uint64_t)s.M, 1, 1}, {(uint64_t)ldc, 0, 0}};
+    return true;
+  }
+  template <class IO>
+  __device__ void ts_chunk(IO& io, int, int, int, int, float (&v)[1][32]) const {
+    io.put(0, v[0], 0, 0);
+  }
   __device__ void operator()(int, int, int m, int n, float acc) const {
     C[(int64_t)m * ldc + n] = acc;
   }
@@ -251,11 +275,21 @@ struct EpiStore {
 
 // weight-gradient partial of lane group (g0 + zg) at param offset (+ zb*sOff)
 struct EpiPartial {
+  static constexpr bool kTmaStore = true;
   float* partials;     // [8][n_shared]
   int64_t n_shared;
   int64_t off, sOff;   // parameter offset in the shared flat layout, batch stride
   int64_t ldw;         // row stride of the weight (its N)
   int g0;
+  bool store_maps(const TcShape& s, TcStoreMap& c, TcStoreMap&) const {
+    c = TcStoreMap{partials + off, {(uint64_t)s.N, (uint64_t)s.M, (uint64_t)s.nzb, (uint64_t)kNumGroups},
+                   {(uint64_t)ldw, (uint64_t)sOff, (uint64_t)n_shared}};
+    return true;
+  }
+  template <class IO>
+  __device__ void ts_chunk(IO& io, int zb, int zg, int, int, float (&v)[1][32]) const {
+    io.put(0, v[0], zb, g0 + zg);
+  }
   __device__ void operator()(int zb, int zg, int m, int n, float acc) const {
     partials[(int64_t)(g0 + zg) * n_shared + off + zb * sOff + (int64_t)m * ldw + n] = acc;
   }

@@ -105,10 +105,53 @@ __global__ void k_mbrb_act(float* __restrict__ H, int K, int64_t plane, float* _
 // acc_z + b_z (kept for the backward product rule), ff = GeLU(prod_z H_z).
 template <int ZIN>
 struct EpiBranchAct {
+  static constexpr bool kTmaStore = true;
+  static constexpr int kTsSlots = 2;  // ff and the D_z leave through a 2-box ring
   float* H;         // [ZIN][M][N]
   float* ff;        // [M][N]
   const float* b0;  // bias of branch 0; branch z at b0 + z*sBias
   int64_t sBias, N, plane;
+  // map 0: D_z as (n, m, z); map 1: ff
+  bool store_maps(const TcShape& s, TcStoreMap& c, TcStoreMap& d) const {
+    c = TcStoreMap{H, {(uint64_t)N, (uint64_t)s.M, (uint64_t)ZIN, 1}, {(uint64_t)N, (uint64_t)plane, 0}};
+    d = TcStoreMap{ff, {(uint64_t)N, (uint64_t)s.M, 1, 1}, {(uint64_t)N, 0, 0}};
+    return true;
+  }
+  template <class IO>
+  __device__ void ts_chunk(IO& io, int, int, int, int n0, float (&v)[ZIN][32]) const {
+    float p[32];
+#pragma unroll
+    for (int z = 0; z < ZIN; ++z) {
+      float b[32];
+      load32(b0 + z * sBias + n0, b);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[z][j] = v[z][j] + b[j];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) p[j] = z == 0 ? v[0][j] : p[j] * v[z][j];
+    }
+    {
+      float f[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const float cdf = gelu_cdf(p[j]);
+        f[j] = p[j] * cdf;
+        p[j] = gelu_dcdf(p[j], cdf);
+      }
+      io.put(1, f, 0, 0);
+    }
+#pragma unroll
+    for (int z = 0; z < ZIN; ++z) {
+      float d[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        d[j] = p[j];
+#pragma unroll
+        for (int y = 0; y < ZIN; ++y)
+          if (y != z) d[j] = d[j] * v[y][j];
+      }
+      io.put(0, d, z, 0);
+    }
+  }
   __device__ void rowz(int m, int n0, float (&v)[ZIN][32]) const {
     float p[32];
 #pragma unroll
@@ -183,11 +226,32 @@ struct EpiBranchAct {
 // g_H_z = g_ff * D_z with D_z = GeLU'(prod) * prod_{j != z} H_j stored by
 // the forward (k_mbrb_act / EpiBranchAct) in place of H_z.
 struct EpiBwdAct {
-  static constexpr bool kTransposed = true;
+  static constexpr bool kTransposed = true;  // fallback (K != 2)
+  static constexpr bool kTmaStore = true;
+  static constexpr int kTsSlots = 2, kTsIn = 2;  // D_0, D_1 boxes, overwritten by g_H_0, g_H_1
   const float* H;  // holds D_z
   float* GH;
   int K;
   int64_t plane, ld;
+  // map 0: g_H as (n, m, z); map 1: D as (n, m, z) -- TMA-loaded
+  bool store_maps(const TcShape& s, TcStoreMap& c, TcStoreMap& d) const {
+    if (K != kTsIn) return false;
+    c = TcStoreMap{GH, {(uint64_t)s.N, (uint64_t)s.M, (uint64_t)K, 1}, {(uint64_t)ld, (uint64_t)plane, 0}};
+    d = TcStoreMap{H, {(uint64_t)s.N, (uint64_t)s.M, (uint64_t)K, 1}, {(uint64_t)ld, (uint64_t)plane, 0}};
+    return true;
+  }
+  __device__ void ts_in(int i, int, int, int& c2, int& c3) const { c2 = i; c3 = 0; }
+  template <class IO>
+  __device__ void ts_chunk(IO& io, int, int, int, int, float (&v)[1][32]) const {
+#pragma unroll
+    for (int z = 0; z < kTsIn; ++z) {
+      float d[32];
+      io.in(z, d);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) d[j] = v[0][j] * d[j];
+      io.put_at(z, 0, d, z, 0);
+    }
+  }
   __device__ void operator()(int, int, int m, int n, float acc) const {
     const int64_t e = (int64_t)m * ld + n;
     for (int z = 0; z < K; ++z) GH[z * plane + e] = acc * H[z * plane + e];
@@ -967,8 +1031,18 @@ __global__ void k_decode_column(uint8_t* __restrict__ mat, int64_t L, StepIdx si
 
 // Split-K epilogue: tile partial of K chunk zg into the workspace.
 struct EpiSplit {
+  static constexpr bool kTmaStore = true;
   float* ws;
   int64_t ld, plane;
+  bool store_maps(const TcShape& s, TcStoreMap& c, TcStoreMap&) const {
+    c = TcStoreMap{ws, {(uint64_t)s.N, (uint64_t)s.M, (uint64_t)s.nsplit, 1},
+                   {(uint64_t)ld, (uint64_t)plane, 0}};
+    return true;
+  }
+  template <class IO>
+  __device__ void ts_chunk(IO& io, int, int zg, int, int, float (&v)[1][32]) const {
+    io.put(0, v[0], zg, 0);
+  }
   __device__ void operator()(int, int zg, int m, int n, float acc) const {
     ws[zg * plane + (int64_t)m * ld + n] = acc;
   }

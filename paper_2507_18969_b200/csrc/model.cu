@@ -1664,6 +1664,7 @@ int edpc_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn,
   k_fill_rand<<<1024, 256>>>(dB, (int64_t)N * K, 2u);
   TcShape s{M, N, K, 1, 1, kBatchNone, kBatchNone, nsplit > 1 ? 2 : 0, nsplit, 0, 0, 0};
   TcOperand a{dA, a_mn ? M : K, 0, 1}, b{dB, b_mn ? N : K, 0, 1};
+  if (const char* d = getenv("EDPC_GEMM_DBG")) s.dbg = atoi(d);
   EpiSplit e{dC, N, (int64_t)M * N};
   auto run = [&]() {
     if (!a_mn && !b_mn) return tc_gemm<false, false>(s, a, b, e, 0);

@@ -30,6 +30,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "tc_types.cuh"
 
 namespace edpc {
 
@@ -78,6 +79,27 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
       "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+
+// TMA bulk-tensor store of a 4D box from shared memory (bulk-group tracked)
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1,
+                                             int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the smem sources of all but the newest N committed groups may be reused
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// generic-proxy smem writes -> visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 // TMA load multicast to the CTAs of the cluster in cta_mask (same smem offset
@@ -187,25 +209,6 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_
 
 // ------------------------------------------------------------------ shapes
 
-// Where an operand's batch coordinate comes from.
-enum TcBatch { kBatchNone = 0, kBatchZ = 1, kBatchSum = 2 };
-
-struct TcShape {
-  int M, N, K;       // K per summed sub-problem (before any K split)
-  int nzb;           // output batches
-  int nsum;          // sub-problems accumulated into one tile
-  int a_batch, b_batch;
-  // K split, one output per split index zg:
-  //   kmode 0: none; 1: lane groups [g0+zg] of B_global lanes (minus lane0);
-  //   2: nsplit equal K chunks
-  int kmode, nsplit, g0, B_global, lane0;
-  int dbg = 0;  // tests only: 1 = epilogue writes m*1000+n
-  // fused column sums of B over K (weight-gradient GEMMs: the bias gradient
-  // of lane group g0+zg); needs MN-major B
-  float* bias_part = nullptr;
-  int64_t bias_gstride = 0, bias_off = 0, bias_zstride = 0;
-};
-
 // ------------------------------------------------------------------ kernel
 
 // ZIN > 1: ZIN batches (the MBRB branches) are computed by the same CTA for
@@ -230,13 +233,56 @@ struct EpiTransposed<Epi, std::void_t<decltype(Epi::kTransposed)>> {
   static constexpr bool value = Epi::kTransposed;
 };
 
-template <int BN, int ZIN = 1, bool TR = true, int EW = 8>
+// TMA-store epilogues (Epi::kTmaStore).  Each epilogue warp owns kTsSlots
+// 4 KB boxes of shared memory; a box holds one 32x32 block in the row-per-
+// thread layout of tcgen05.ld (row = TMEM lane), 128B-swizzled, and leaves
+// through a TMA bulk-tensor store.  ncu on the row-per-thread global stores
+// showed the K=256 GEMMs bound by the LSU (each warp-wide STG.128 touches 32
+// rows: ~256 L1 wavefronts per block, the store-free ablation ran 1.9x
+// faster); a box costs 32 wavefronts of STS.128 and the copy engine writes
+// whole lines.  Epilogues that read a second operand (kTsIn boxes per block,
+// e.g. the stored GeLU' factors) get it TMA-loaded into slots 0..kTsIn-1
+// before their tcgen05.ld and overwrite the slots in place.  The functor:
+//   host:   bool store_maps(const TcShape&, TcStoreMap& c, TcStoreMap& d) const
+//           (maps 0 and 1; false -> the kernel uses its non-TMA path)
+//   device: template <class IO, int Z>
+//           void ts_chunk(IO&, zb, zg, m, n0, float (&v)[Z][32]) const
+//           void ts_in(i, zb, zg, int& c2, int& c3) const   (kTsIn > 0)
+template <class Epi, class = void>
+struct EpiTmaStore {
+  static constexpr bool value = false;
+};
+template <class Epi>
+struct EpiTmaStore<Epi, std::void_t<decltype(Epi::kTmaStore)>> {
+  static constexpr bool value = Epi::kTmaStore;
+};
+template <class Epi, class = void>
+struct EpiTsSlots {
+  static constexpr int value = 1;
+};
+template <class Epi>
+struct EpiTsSlots<Epi, std::void_t<decltype(Epi::kTsSlots)>> {
+  static constexpr int value = Epi::kTsSlots;
+};
+template <class Epi, class = void>
+struct EpiTsIn {
+  static constexpr int value = 0;
+};
+template <class Epi>
+struct EpiTsIn<Epi, std::void_t<decltype(Epi::kTsIn)>> {
+  static constexpr int value = Epi::kTsIn;
+};
+constexpr int kTsBoxBytes = 32 * 32 * 4;
+
+template <int BN, int ZIN = 1, bool TR = true, int EW = 8, int TSLOTS = 0>
 struct TcSmem {
   static constexpr int kABytes = kTcBM * kTcBK * 4;  // 16 KB
   static constexpr int kBBytes = BN * kTcBK * 4;
   static constexpr int kStageBytes = kABytes + ZIN * kBBytes;
-  static constexpr int kEpiBytes = TR ? EW * ZIN * kTcTileFloats * 4 : 0;
-  static constexpr int kFixed = 1024 /*align*/ + 256 /*barriers*/ + kEpiBytes;
+  static constexpr int kTrBytes = TR ? EW * ZIN * kTcTileFloats * 4 : 0;
+  static constexpr int kTsBytes = EW * TSLOTS * kTsBoxBytes;
+  static constexpr int kEpiBytes = kTrBytes > kTsBytes ? kTrBytes : kTsBytes;
+  static constexpr int kFixed = 1024 /*align*/ + 512 /*barriers*/ + kEpiBytes;
   static constexpr int kStages = (4 * kStageBytes + kFixed <= 232448)   ? 4
                                  : (3 * kStageBytes + kFixed <= 232448) ? 3
                                                                         : 2;
@@ -247,6 +293,64 @@ struct TcSmem {
   static constexpr uint32_t kTmemCols =
       kCols <= 32 ? 32 : kCols <= 64 ? 64 : kCols <= 128 ? 128 : kCols <= 256 ? 256 : 512;
 };
+
+// Per-warp box writer of a TMA-store epilogue (see EpiTmaStore).
+template <int NS>
+struct TsIo {
+  float* slots;  // NS boxes of 32x32 floats
+  const CUtensorMap* maps[2];
+  int n0, m0;    // box origin (columns, rows)
+  int* next;     // ring position (persists across blocks)
+  // row `lane` of box `slot`: 16-byte chunk j at j ^ (lane & 7) (SWIZZLE_128B)
+  __device__ __forceinline__ void write_row(int slot, const float (&v)[32]) const {
+    const int lane = threadIdx.x & 31;
+    float* box = slots + slot * 1024 + lane * 32;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<float4*>(box + ((j ^ (lane & 7)) << 2)) =
+          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+  }
+  __device__ __forceinline__ void in(int slot, float (&v)[32]) const {
+    const int lane = threadIdx.x & 31;
+    const float* box = slots + slot * 1024 + lane * 32;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float4 q = *reinterpret_cast<const float4*>(box + ((j ^ (lane & 7)) << 2));
+      v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
+    }
+  }
+  __device__ __forceinline__ void issue(int slot, int map, int c2, int c3) const {
+    fence_async_smem();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) {
+      tma_store_4d(maps[map], slots + slot * 1024, n0, m0, c2, c3);  // rows past M are clipped
+      bulk_commit();
+    }
+  }
+  // store v (this thread's row) to map at (n0, m0, c2, c3) through the ring
+  __device__ __forceinline__ void put(int map, const float (&v)[32], int c2, int c3) {
+    const int slot = *next;
+    *next = slot + 1 == NS ? 0 : slot + 1;
+    if ((threadIdx.x & 31) == 0) bulk_wait_read<NS - 1>();
+    __syncwarp();
+    write_row(slot, v);
+    issue(slot, map, c2, c3);
+  }
+  // store v through input slot `slot` (already consumed by this thread's row)
+  __device__ __forceinline__ void put_at(int slot, int map, const float (&v)[32], int c2, int c3) {
+    write_row(slot, v);
+    issue(slot, map, c2, c3);
+  }
+};
+
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
 
 constexpr int kTcBiasWarps = 4;
 __host__ __device__ constexpr int tc_threads(bool bias, int ew = 8) {
@@ -277,15 +381,20 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 template <int BN, bool AMN, bool BMN, bool BIAS, class Epi, int ZIN = 1, int CL = 1, int EW = 8>
 __global__ void __launch_bounds__(tc_threads(BIAS, EW), 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+          const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_d,
           TcShape s, Epi epi) {
   static_assert(!BIAS || BMN, "fused bias sums read an MN-major B tile");
   static_assert(ZIN == 1 || !BIAS, "multi-branch tiles have no fused bias");
   static_assert(TcSmem<BN, ZIN>::kCols <= 512, "TMEM holds 512 columns");
-  constexpr bool TR = ZIN > 1 || EpiTransposed<Epi>::value;
+  constexpr bool TS = EpiTmaStore<Epi>::value;
+  constexpr int kTsSlots = TS ? EpiTsSlots<Epi>::value : 0;
+  constexpr int kTsIn = EpiTsIn<Epi>::value;
+  static_assert(kTsIn <= kTsSlots, "input boxes live in the TMA-store slots");
+  constexpr bool TR = ZIN > 1 || EpiTransposed<Epi>::value;  // also the !s.ts fallback
   constexpr int kTcEpiWarps = EW;  // epilogue warps: EW / 4 per TMEM lane quadrant
   static_assert(EW % 4 == 0, "whole TMEM lane quadrants per epilogue warp group");
   extern __shared__ uint8_t smem_raw[];
-  using SM = TcSmem<BN, ZIN, TR, EW>;
+  using SM = TcSmem<BN, ZIN, TR, EW, kTsSlots>;
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr int kStages = SM::kStages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::kBarOffset);
@@ -293,6 +402,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* wbar = tempty + 4;  // per epilogue warp: its TMA-loaded input boxes
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -335,6 +445,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kTcEpiWarps);
     }
+    if constexpr (kTsIn > 0)
+      for (int w = 0; w < kTcEpiWarps; ++w) mbar_init(&wbar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -451,6 +563,8 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;  // which of the EW/4 warps of this quadrant
     int lt = 0;
+    int ts_next = 0;       // TMA-store box ring position
+    uint32_t ts_wph = 0;   // phase of this warp's input-box barrier
     for (int t = u0; t < n_tiles; t += ustride, ++lt) {
       int tn, tm, zb, zg, kb0, nkb;
       tile_coords(t, tn, tm, zb, zg, kb0, nkb);
@@ -464,6 +578,49 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       const int m_base = tm * kTcBM + quad * 32;
 #pragma unroll 1
       for (int c = half * 32; c < BN; c += 32 * (EW / 4)) {
+        if (s.dbg == 3) continue;  // microbenchmark ablation: no epilogue at all
+        if constexpr (TS) {
+          if (s.ts) {
+            float* slots = reinterpret_cast<float*>(smem + SM::kEpiOffset) +
+                           (warp - 2) * kTsSlots * (kTsBoxBytes / 4);
+            if constexpr (kTsIn > 0) {
+              if (lane == 0) {
+                bulk_wait_read<0>();  // the slots' previous stores have read them
+                mbar_expect_tx(&wbar[warp - 2], kTsIn * kTsBoxBytes);
+#pragma unroll
+                for (int i = 0; i < kTsIn; ++i) {
+                  int c2, c3;
+                  epi.ts_in(i, zb, zg, c2, c3);
+                  tma_load_4d(slots + i * (kTsBoxBytes / 4), &tma_d, &wbar[warp - 2], n0 + c,
+                              m_base, c2, c3);
+                }
+              }
+            }
+            float v[ZIN][32];
+#pragma unroll
+            for (int zi = 0; zi < ZIN; ++zi) {
+              if (any) {
+                tmem_ld32(tmem + ((uint32_t)(quad * 32) << 16) +
+                              (uint32_t)((acc * ZIN + zi) * BN + c),
+                          v[zi]);
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[zi][j] = 0.f;
+              }
+              if (s.dbg == 1) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[zi][j] = (float)(m * 1000 + n0 + c + j);
+              }
+            }
+            if constexpr (kTsIn > 0) {
+              mbar_wait(&wbar[warp - 2], ts_wph);
+              ts_wph ^= 1u;
+            }
+            TsIo<kTsSlots> io{slots, {&tma_c, &tma_d}, n0 + c, m_base, &ts_next};
+            epi.ts_chunk(io, zb, zg, m, n0 + c, v);
+            continue;
+          }
+        }
         if constexpr (!TR) {
           float v[32];
           if (any) {
@@ -475,6 +632,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
           if (s.dbg == 1) {
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = (float)(m * 1000 + n0 + c + j);
+          }
+          if (s.dbg == 2) {  // microbenchmark ablation: TMEM loads only
+            float x = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) x += v[j];
+            if (x == 12345.678f) epi.row32(zb, zg, m, n0 + c, v);
+            continue;
           }
           if (m < s.M) epi.row32(zb, zg, m, n0 + c, v);
         } else {
@@ -509,6 +673,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+    }
+    if constexpr (TS) {
+      if (s.ts && lane == 0) bulk_wait_all();
     }
   } else if (BIAS) {
     // ---------------- bias warps: column sums of B over this tile's K range
@@ -620,6 +787,66 @@ inline int make_tmap(CUtensorMap* map, const float* base, uint64_t inner, uint64
   return EDPC_OK;
 }
 
+// Output map of a TMA-store epilogue: 4D fp32, box 32 x 32 x 1 x 1, 128B
+// swizzle.  False when TMA cannot address it (16-byte alignment of the base
+// and of every stride); the kernel then stores with row32.
+inline bool make_store_tmap(CUtensorMap* map, const TcStoreMap& d) {
+  if (((uintptr_t)d.base & 15) != 0 || d.dims[0] < 32) return false;
+  cuuint64_t dims[4] = {d.dims[0], d.dims[1], d.dims[2] ? d.dims[2] : 1, d.dims[3] ? d.dims[3] : 1};
+  cuuint64_t strides[3];
+  uint64_t prev = d.dims[0];
+  for (int i = 0; i < 3; ++i) {
+    uint64_t st = d.strides[i];
+    if (dims[i + 1] == 1 || st == 0) st = prev;  // unused dimension: any valid stride
+    if ((st * 4) % 16 != 0 || st * 4 >= (1ull << 40)) return false;
+    strides[i] = st * 4;
+    prev = st * dims[i + 1];
+  }
+  cuuint32_t box[4] = {32, 32, 1, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  PfnEncodeTiled enc = encode_tiled_fn();
+  if (!enc) return false;
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)d.base, dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct StoreTmapCache {
+  std::mutex mu;
+  std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t,
+                      uint64_t>,
+           std::pair<bool, CUtensorMap>>
+      maps;
+  bool get(CUtensorMap* out, const TcStoreMap& d) {
+    auto key = std::make_tuple((const void*)d.base, d.dims[0], d.dims[1], d.dims[2], d.dims[3],
+                               d.strides[0], d.strides[1], d.strides[2]);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = maps.find(key);
+    if (it == maps.end()) {
+      CUtensorMap m{};
+      bool ok = make_store_tmap(&m, d);
+      it = maps.emplace(key, std::make_pair(ok, m)).first;
+    }
+    *out = it->second.second;
+    return it->second.first;
+  }
+};
+
+inline StoreTmapCache& store_tmap_cache() {
+  static StoreTmapCache c;
+  return c;
+}
+
+// Both maps of a TMA-store epilogue (a null base = unused); 1 if usable.
+template <class Epi>
+inline int ts_maps(const Epi& epi, const TcShape& s, CUtensorMap& tc, CUtensorMap& td) {
+  TcStoreMap c{}, d{};
+  if (!epi.store_maps(s, c, d)) return 0;
+  if (!store_tmap_cache().get(&tc, c)) return 0;
+  if (d.base && !store_tmap_cache().get(&td, d)) return 0;
+  return 1;
+}
+
 // An operand as stored in global memory: row-major [rows][inner] (+ batch).
 struct TcOperand {
   const float* ptr;
@@ -685,8 +912,8 @@ inline bool cluster_enabled() {
 
 template <typename Kern, typename Epi>
 inline cudaError_t launch_tc(Kern kern, int grid, int threads, int smem, cudaStream_t st, int cl,
-                             const CUtensorMap& ta, const CUtensorMap& tb, const TcShape& s,
-                             const Epi& epi) {
+                             const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc,
+                             const CUtensorMap& td, const TcShape& s, const Epi& epi) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3((unsigned)threads);
@@ -699,7 +926,7 @@ inline cudaError_t launch_tc(Kern kern, int grid, int threads, int smem, cudaStr
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, ta, tb, s, epi);
+  return cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, td, s, epi);
 }
 
 template <typename Kern>
@@ -713,10 +940,14 @@ inline void set_smem_attr(Kern kern, int bytes, bool& done) {
 template <int BN, bool AMN, bool BMN, class Epi>
 inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, const Epi& epi,
                      cudaStream_t st) {
-  constexpr int kSmem = TcSmem<BN, 1, EpiTransposed<Epi>::value>::kBytes;
+  constexpr bool kTS = EpiTmaStore<Epi>::value;
+  constexpr int kSmem =
+      TcSmem<BN, 1, EpiTransposed<Epi>::value, 8, kTS ? EpiTsSlots<Epi>::value : 0>::kBytes;
   const int n_tm = cdiv(s.M, kTcBM);
   const int cl = (cluster_enabled() && n_tm % 2 == 0) ? 2 : 1;
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tc{}, td{};
+  TcShape s2 = s;
+  if constexpr (kTS) s2.ts = ts_maps(epi, s, tc, td);
   int r;
   // A: K-major -> [M rows][K inner]; MN-major -> [K rows][M inner]
   if (AMN)
@@ -749,12 +980,12 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
         static bool done[16] = {};
         auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi, 1, 2>;
         set_smem_attr(kern, kSmem, done[di]);
-        e = launch_tc(kern, grid, tc_threads(true), kSmem, st, 2, ta, tb, s, epi);
+        e = launch_tc(kern, grid, tc_threads(true), kSmem, st, 2, ta, tb, tc, td, s2, epi);
       } else {
         static bool done[16] = {};
         auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi, 1, 1>;
         set_smem_attr(kern, kSmem, done[di]);
-        e = launch_tc(kern, grid, tc_threads(true), kSmem, st, 1, ta, tb, s, epi);
+        e = launch_tc(kern, grid, tc_threads(true), kSmem, st, 1, ta, tb, tc, td, s2, epi);
       }
       launched = true;
     }
@@ -764,12 +995,12 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
       static bool done[16] = {};
       auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi, 1, 2>;
       set_smem_attr(kern, kSmem, done[di]);
-      e = launch_tc(kern, grid, tc_threads(false), kSmem, st, 2, ta, tb, s, epi);
+      e = launch_tc(kern, grid, tc_threads(false), kSmem, st, 2, ta, tb, tc, td, s2, epi);
     } else {
       static bool done[16] = {};
       auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi, 1, 1>;
       set_smem_attr(kern, kSmem, done[di]);
-      e = launch_tc(kern, grid, tc_threads(false), kSmem, st, 1, ta, tb, s, epi);
+      e = launch_tc(kern, grid, tc_threads(false), kSmem, st, 1, ta, tb, tc, td, s2, epi);
     }
   }
   if (e == cudaSuccess) e = cudaGetLastError();
@@ -784,8 +1015,11 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
 template <int BN, int ZIN, bool BMN, class Epi>
 inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& B,
                          const Epi& epi, cudaStream_t st) {
-  // the fused GeLU epilogue is issue-bound: 16 epilogue warps (4 per quadrant)
-  constexpr int kZinEW = (BN % 128 == 0) ? 16 : 8;
+  // the transposed fused-GeLU epilogue is issue-bound (16 epilogue warps);
+  // the TMA-store form keeps its registers with 8
+  constexpr bool kTS = EpiTmaStore<Epi>::value;
+  constexpr int kZinEW = (!kTS && BN % 128 == 0) ? 16 : 8;
+  constexpr int kSmem = TcSmem<BN, ZIN, true, kZinEW, kTS ? EpiTsSlots<Epi>::value : 0>::kBytes;
   const int n_tm = cdiv(s.M, kTcBM);
   const int cl = (cluster_enabled() && n_tm % 2 == 0) ? 2 : 1;
   CUtensorMap ta, tb;
@@ -799,6 +1033,9 @@ inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& 
     r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.K, (uint64_t)s.N, (uint64_t)B.nbatch,
                          (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN / cl, false);
   if (r != EDPC_OK) return r;
+  CUtensorMap tc{}, td{};
+  TcShape s2 = s;
+  if constexpr (kTS) s2.ts = ts_maps(epi, s, tc, td);
   const int units = (s.N / BN) * (n_tm / cl);
   const int max_units = num_sms() / cl;
   const int grid = (units < max_units ? units : max_units) * cl;
@@ -809,13 +1046,13 @@ inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& 
   if (cl == 2) {
     static bool done[16] = {};
     auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 2, kZinEW>;
-    set_smem_attr(kern, TcSmem<BN, ZIN, true, kZinEW>::kBytes, done[di]);
-    e = launch_tc(kern, grid, tc_threads(false, kZinEW), TcSmem<BN, ZIN, true, kZinEW>::kBytes, st, 2, ta, tb, s, epi);
+    set_smem_attr(kern, kSmem, done[di]);
+    e = launch_tc(kern, grid, tc_threads(false, kZinEW), kSmem, st, 2, ta, tb, tc, td, s2, epi);
   } else {
     static bool done[16] = {};
     auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 1, kZinEW>;
-    set_smem_attr(kern, TcSmem<BN, ZIN, true, kZinEW>::kBytes, done[di]);
-    e = launch_tc(kern, grid, tc_threads(false, kZinEW), TcSmem<BN, ZIN, true, kZinEW>::kBytes, st, 1, ta, tb, s, epi);
+    set_smem_attr(kern, kSmem, done[di]);
+    e = launch_tc(kern, grid, tc_threads(false, kZinEW), kSmem, st, 1, ta, tb, tc, td, s2, epi);
   }
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
