@@ -426,6 +426,7 @@ k_ln_bwd_fused(const float* __restrict__ gx0, const float* __restrict__ xhat,
   const float* all = scratch + (int64_t)blockIdx.y * nchunk * 2 * F;
   for (int f = threadIdx.x; f < F; f += blockDim.x) {
     float a = all[f], c = all[F + f];
+#pragma unroll 8  // the loads are independent: keep 8 in flight (this tail is L2-latency bound)
     for (int k = 1; k < nchunk; ++k) {
       a += all[(int64_t)k * 2 * F + f];
       c += all[(int64_t)k * 2 * F + F + f];
@@ -630,7 +631,11 @@ k_fdm_fwd_v(const float* __restrict__ down, const float* __restrict__ U, float* 
   for (int v = 0; v < G::kNV; ++v) out[v * G::kTPR + t] = acc[v];
 }
 
-template <int FP>
+// GX: g_down_b = U_b g_b with the old U (nn.py:177-179); ADAM: U_b's
+// gradient d_b (x) g_b and its Adam step.  Both in one pass (U read once),
+// or split so that the Adam half -- ~6 B/param of HBM traffic, off the
+// critical path -- runs on the side stream after the GX half.
+template <int FP, bool GX = true, bool ADAM = true>
 __global__ void __launch_bounds__(256)
 k_fdm_bwd_adam_v(const float* __restrict__ down, const float* __restrict__ gmix,
                  float* __restrict__ U, float* __restrict__ Um, float* __restrict__ Uv,
@@ -643,8 +648,8 @@ k_fdm_bwd_adam_v(const float* __restrict__ down, const float* __restrict__ gmix,
   const int t = lane % G::kTPR;
   const bool live = b < Bl;
   const int bb = live ? b : 0;
-  float bc1, bc2;
-  adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
+  float bc1 = 0.f, bc2 = 0.f;
+  if (ADAM) adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
   const float* d = down + (int64_t)bb * FP;
   const float4* gm4 = reinterpret_cast<const float4*>(gmix + (int64_t)bb * FP);
   float4 g[G::kNV];
@@ -665,37 +670,46 @@ k_fdm_bwd_adam_v(const float* __restrict__ down, const float* __restrict__ gmix,
       for (int v = 0; v < G::kNV; ++v) {
         const int e = ((i0 + r) * FP) / 4 + v * G::kTPR + t;
         w[r][v] = u4[e];
-        m[r][v] = m4[e];
-        q[r][v] = v4[e];
+        if (ADAM) {
+          m[r][v] = m4[e];
+          q[r][v] = v4[e];
+        }
       }
     float part[kR];
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
-      const float di = d[i0 + r];
+      const float di = ADAM ? d[i0 + r] : 0.f;
       part[r] = 0.f;
 #pragma unroll
       for (int v = 0; v < G::kNV; ++v) {
-        part[r] = fmaf(g[v].x, w[r][v].x, part[r]);
-        part[r] = fmaf(g[v].y, w[r][v].y, part[r]);
-        part[r] = fmaf(g[v].z, w[r][v].z, part[r]);
-        part[r] = fmaf(g[v].w, w[r][v].w, part[r]);
-        adam_elem(w[r][v].x, m[r][v].x, q[r][v].x, di * g[v].x, c, bc1, bc2);
-        adam_elem(w[r][v].y, m[r][v].y, q[r][v].y, di * g[v].y, c, bc1, bc2);
-        adam_elem(w[r][v].z, m[r][v].z, q[r][v].z, di * g[v].z, c, bc1, bc2);
-        adam_elem(w[r][v].w, m[r][v].w, q[r][v].w, di * g[v].w, c, bc1, bc2);
-        if (live) {
-          const int e = ((i0 + r) * FP) / 4 + v * G::kTPR + t;
-          u4[e] = w[r][v];
-          m4[e] = m[r][v];
-          v4[e] = q[r][v];
+        if (GX) {
+          part[r] = fmaf(g[v].x, w[r][v].x, part[r]);
+          part[r] = fmaf(g[v].y, w[r][v].y, part[r]);
+          part[r] = fmaf(g[v].z, w[r][v].z, part[r]);
+          part[r] = fmaf(g[v].w, w[r][v].w, part[r]);
+        }
+        if (ADAM) {
+          adam_elem(w[r][v].x, m[r][v].x, q[r][v].x, di * g[v].x, c, bc1, bc2);
+          adam_elem(w[r][v].y, m[r][v].y, q[r][v].y, di * g[v].y, c, bc1, bc2);
+          adam_elem(w[r][v].z, m[r][v].z, q[r][v].z, di * g[v].z, c, bc1, bc2);
+          adam_elem(w[r][v].w, m[r][v].w, q[r][v].w, di * g[v].w, c, bc1, bc2);
+          if (live) {
+            const int e = ((i0 + r) * FP) / 4 + v * G::kTPR + t;
+            u4[e] = w[r][v];
+            m4[e] = m[r][v];
+            v4[e] = q[r][v];
+          }
         }
       }
     }
+    if (GX) {
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
+      for (int r = 0; r < kR; ++r) {
 #pragma unroll
-      for (int o = G::kTPR / 2; o > 0; o >>= 1) part[r] += __shfl_xor_sync(0xffffffffu, part[r], o);
-      if (live && t == 0) gdown[(int64_t)b * FP + i0 + r] = part[r];
+        for (int o = G::kTPR / 2; o > 0; o >>= 1)
+          part[r] += __shfl_xor_sync(0xffffffffu, part[r], o);
+        if (live && t == 0) gdown[(int64_t)b * FP + i0 + r] = part[r];
+      }
     }
   }
 }
@@ -784,24 +798,24 @@ k_embed_grad_chunks(ByteCols src, StepIdx si, int T, int DE, int F,
     }
     __syncthreads();
   }
-  const int c = tid;
-  const int o0 = off[c], o1 = off[c] + hist[c];
-  for (int d0 = 0; d0 < DE; d0 += 16) {
-    float acc[16];
-#pragma unroll
-    for (int d = 0; d < 16; ++d) acc[d] = 0.f;
-    for (int q = o0; q < o1; ++q) {
-      const int e = order[q];
-      const int bl = e / T, p = e - bl * T;
-      const float* g = staged ? grows + bl * F + p * DE + d0
-                              : gx + (int64_t)(lb + bl) * F + p * DE + d0;
-#pragma unroll
-      for (int d = 0; d < 16; ++d)
-        if (d0 + d < DE) acc[d] += g[d];
+  // half-warp per byte value, thread = embedding dimension: the 16 threads
+  // read one row's 16 consecutive floats (conflict-free; a thread per byte
+  // value reading whole rows hit 2 banks, ~16-way conflicts) and sum the
+  // byte's entries in their sorted (= sequential scan) order
+  const int hw = tid >> 4, dl = tid & 15;
+  for (int c = hw; c < 256; c += 16) {
+    const int o0 = off[c], o1 = off[c] + hist[c];
+    for (int d = dl; d < ((DE + 15) & ~15); d += 16) {
+      float acc = 0.f;
+      if (d < DE) {
+        for (int q = o0; q < o1; ++q) {
+          const int e = order[q];
+          const int bl = e / T, p = e - bl * T;
+          acc += staged ? grows[bl * F + p * DE + d] : gx[(int64_t)(lb + bl) * F + p * DE + d];
+        }
+        sub[((int64_t)k * 256 + c) * DE + d] = acc;
+      }
     }
-#pragma unroll
-    for (int d = 0; d < 16; ++d)
-      if (d0 + d < DE) sub[((int64_t)k * 256 + c) * DE + d0 + d] = acc[d];
   }
 }
 
@@ -814,6 +828,7 @@ __global__ void k_embed_grad_reduce(const float* __restrict__ sub, const int* __
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= 256 * DE) return;
   float acc = 0.f;
+#pragma unroll 8
   for (int k = k0; k < k1; ++k) acc += sub[(int64_t)k * 256 * DE + e];
   partials[(int64_t)gg * n_shared + off + e] = acc;
 }

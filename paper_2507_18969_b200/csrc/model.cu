@@ -731,25 +731,46 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   CK(fork_aux(c));
   CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
   CK(dgrad(c, c->g_lte, F, 1, 0, c->W + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
-  // per-lane FDM: g_down with the old U, then U's Adam step (fused)
+  // per-lane FDM: g_down with the old U, then U's Adam step (fused: U read once)
   {
-    Scope sc_(c, kRegFdmBwd, c->st);
     if (FP == 64 || FP == 128 || FP == 256) {
       const int lpw = 32 / std::min(32, FP / 4);
       const unsigned blocks = (unsigned)cdiv(cdiv(Bl, lpw), 8);
-      if (FP == 64)
-        k_fdm_bwd_adam_v<64><<<blocks, 256, 0, c->st>>>(c->down, c->gmix, c->U, c->Um, c->Uv,
-                                                        c->gdown, Bl, c->si(), c->adam,
-                                                        c->cfg.beta1, c->cfg.beta2);
-      else if (FP == 128)
-        k_fdm_bwd_adam_v<128><<<blocks, 256, 0, c->st>>>(c->down, c->gmix, c->U, c->Um, c->Uv,
-                                                         c->gdown, Bl, c->si(), c->adam,
-                                                         c->cfg.beta1, c->cfg.beta2);
-      else
-        k_fdm_bwd_adam_v<256><<<blocks, 256, 0, c->st>>>(c->down, c->gmix, c->U, c->Um, c->Uv,
-                                                         c->gdown, Bl, c->si(), c->adam,
-                                                         c->cfg.beta1, c->cfg.beta2);
+      auto run = [&](auto kern, cudaStream_t st) {
+        Scope sc_(c, kRegFdmBwd, st);
+        kern<<<blocks, 256, 0, st>>>(c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, Bl, c->si(),
+                                     c->adam, c->cfg.beta1, c->cfg.beta2);
+      };
+      // split measured 1% slower at C2: the persistent GEMMs own whole SMs,
+      // so the side-stream Adam pass barely overlaps and U is read twice
+      const bool split = false;
+      if (FP == 64) {
+        if (split) {
+          run(k_fdm_bwd_adam_v<64, true, false>, c->st);
+          CK(fork_aux(c));
+          run(k_fdm_bwd_adam_v<64, false, true>, c->st_aux);
+        } else {
+          run(k_fdm_bwd_adam_v<64>, c->st);
+        }
+      } else if (FP == 128) {
+        if (split) {
+          run(k_fdm_bwd_adam_v<128, true, false>, c->st);
+          CK(fork_aux(c));
+          run(k_fdm_bwd_adam_v<128, false, true>, c->st_aux);
+        } else {
+          run(k_fdm_bwd_adam_v<128>, c->st);
+        }
+      } else {
+        if (split) {
+          run(k_fdm_bwd_adam_v<256, true, false>, c->st);
+          CK(fork_aux(c));
+          run(k_fdm_bwd_adam_v<256, false, true>, c->st_aux);
+        } else {
+          run(k_fdm_bwd_adam_v<256>, c->st);
+        }
+      }
     } else {
+      Scope sc_(c, kRegFdmBwd, c->st);
       k_fdm_bwd_adam<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(
           c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, FP, Bl, c->si(), c->adam,
           c->cfg.beta1, c->cfg.beta2);

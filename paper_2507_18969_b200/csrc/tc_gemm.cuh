@@ -1075,13 +1075,26 @@ inline int bn_cap() {
 template <bool AMN, bool BMN, class Epi>
 inline int tc_gemm(const TcShape& s, const TcOperand& A, const TcOperand& B, const Epi& epi,
                    cudaStream_t st) {
+  // Tile width: the widest BN whose tile count still fills 3/4 of the SMs;
+  // small GEMMs (head, LTE projections, their weight gradients: 8-32 tiles
+  // at BN 256) are bound by per-SM TMA bandwidth and latency, so they trade
+  // MMA width for CTAs.
   const int cap = bn_cap();
-  if (cap >= 256 && s.N % 256 == 0) return tc_launch<256, AMN, BMN>(s, A, B, epi, st);
-  if (cap >= 128 && s.N % 128 == 0) return tc_launch<128, AMN, BMN>(s, A, B, epi, st);
-  if (cap >= 64 && s.N % 64 == 0) return tc_launch<64, AMN, BMN>(s, A, B, epi, st);
-  if (s.N == 128) return tc_launch<128, AMN, BMN>(s, A, B, epi, st);
-  if (s.N == 64) return tc_launch<64, AMN, BMN>(s, A, B, epi, st);
-  if (s.N == 32) return tc_launch<32, AMN, BMN>(s, A, B, epi, st);
+  const int nz = s.nzb * (s.kmode == 0 ? 1 : s.nsplit);
+  const int n_tm = cdiv(s.M, kTcBM);
+  const int want = num_sms() * 3 / 4;
+  int bn = 0;
+  for (int c : {256, 128, 64, 32}) {
+    if (c > cap || s.N % c != 0) continue;
+    bn = c;
+    if ((s.N / c) * n_tm * nz >= want) break;
+  }
+  switch (bn) {
+    case 256: return tc_launch<256, AMN, BMN>(s, A, B, epi, st);
+    case 128: return tc_launch<128, AMN, BMN>(s, A, B, epi, st);
+    case 64: return tc_launch<64, AMN, BMN>(s, A, B, epi, st);
+    case 32: return tc_launch<32, AMN, BMN>(s, A, B, epi, st);
+  }
   set_error("tc_gemm: unsupported N");
   return EDPC_ERR_INVALID;
 }
