@@ -370,31 +370,38 @@ k_ln_bwd_fused(const float* __restrict__ gx0, const float* __restrict__ xhat,
   float sg[kJ], sb[kJ];
 #pragma unroll
   for (int j = 0; j < kJ; ++j) sg[j] = sb[j] = 0.f;
+  float gn[kJ];
+#pragma unroll
+  for (int j = 0; j < kJ; ++j) gn[j] = lane + 32 * j < F ? gain[lane + 32 * j] : 0.f;
   for (int b = lb + warp; b < le; b += 8) {
     const int64_t o = (int64_t)b * F;
-    float s1 = 0.f, s2 = 0.f;
+    // the row's loads all in flight first, kept in registers for both passes
+    float gxv[kJ], xhv[kJ], upv[kJ];
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
       const int f = lane + 32 * j;
-      if (f < F) {
-        const float gx = gx0[o + f], xh = xhat[o + f];
-        const float g = gx * gain[f];
+      gxv[j] = f < F ? gx0[o + f] : 0.f;
+      xhv[j] = f < F ? xhat[o + f] : 0.f;
+      upv[j] = f < F ? up[o + f] : 0.f;
+    }
+    const float r = rstd[b];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      if (lane + 32 * j < F) {
+        const float g = gxv[j] * gn[j];
         s1 += g;
-        s2 += g * xh;
-        sg[j] += gx * xh;
-        sb[j] += gx;
+        s2 += g * xhv[j];
+        sg[j] += gxv[j] * xhv[j];
+        sb[j] += gxv[j];
       }
     }
     const float gm = warp_sum(s1) / (float)F;
     const float gxm = warp_sum(s2) / (float)F;
-    const float r = rstd[b];
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
       const int f = lane + 32 * j;
-      if (f < F) {
-        const float g = gx0[o + f] * gain[f];
-        out[o + f] = (g - gm - xhat[o + f] * gxm) * r + up[o + f];
-      }
+      if (f < F) out[o + f] = (gxv[j] * gn[j] - gm - xhv[j] * gxm) * r + upv[j];
     }
   }
 #pragma unroll
@@ -749,9 +756,23 @@ k_embed_grad_chunks(ByteCols src, StepIdx si, int T, int DE, int F,
     cbytes[e] = src.base[(int64_t)(lb + bl) * src.ld + col0 + p];
   }
   const bool staged = nl * F <= kEmbSmemFloats;
-  if (staged) {
-    const float* g0 = gx + (int64_t)lb * F;
-    for (int e = tid; e < nl * F; e += blockDim.x) grows[e] = g0[e];
+  if (staged) {  // float4, 4 loads in flight per thread (an LDG->STS chain was latency bound)
+    const float4* g0 = reinterpret_cast<const float4*>(gx + (int64_t)lb * F);
+    float4* gr = reinterpret_cast<float4*>(grows);
+    const int n4 = (nl * F) >> 2;
+    if (((nl * F) & 3) == 0 && (((uintptr_t)g0) & 15) == 0) {
+      for (int e0 = tid; e0 < n4; e0 += 4 * blockDim.x) {
+        float4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e0 + u * (int)blockDim.x < n4) q[u] = g0[e0 + u * blockDim.x];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (e0 + u * (int)blockDim.x < n4) gr[e0 + u * blockDim.x] = q[u];
+      }
+    } else {
+      for (int e = tid; e < nl * F; e += blockDim.x) grows[e] = gx[(int64_t)lb * F + e];
+    }
   }
   hist[tid] = 0;
   __syncthreads();
