@@ -247,7 +247,9 @@ struct EpiBranchAct {
 struct EpiBwdAct {
   static constexpr bool kTransposed = true;  // fallback (K != 2)
   static constexpr bool kTmaStore = true;
-  static constexpr int kTsSlots = 2, kTsIn = 2;  // D_0, D_1 boxes, overwritten by g_H_0, g_H_1
+  // D_0, D_1 boxes (double-buffered: the next block's load in flight),
+  // overwritten in place by g_H_0, g_H_1
+  static constexpr int kTsSlots = 4, kTsIn = 2;
   const float* H;  // holds D_z
   float* GH;
   int K;

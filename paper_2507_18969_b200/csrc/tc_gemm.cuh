@@ -273,6 +273,7 @@ struct EpiTsIn<Epi, std::void_t<decltype(Epi::kTsIn)>> {
   static constexpr int value = Epi::kTsIn;
 };
 constexpr int kTsBoxBytes = 32 * 32 * 4;
+constexpr int kStagesMax = 4;
 
 template <int BN, int ZIN = 1, bool TR = true, int EW = 8, int TSLOTS = 0>
 struct TcSmem {
@@ -301,6 +302,7 @@ struct TsIo {
   const CUtensorMap* maps[2];
   int n0, m0;    // box origin (columns, rows)
   int* next;     // ring position (persists across blocks)
+  int ib;        // first slot of this block's input boxes (in / put_at)
   // row `lane` of box `slot`: 16-byte chunk j at j ^ (lane & 7) (SWIZZLE_128B)
   __device__ __forceinline__ void write_row(int slot, const float (&v)[32]) const {
     const int lane = threadIdx.x & 31;
@@ -312,7 +314,7 @@ struct TsIo {
   }
   __device__ __forceinline__ void in(int slot, float (&v)[32]) const {
     const int lane = threadIdx.x & 31;
-    const float* box = slots + slot * 1024 + lane * 32;
+    const float* box = slots + (ib + slot) * 1024 + lane * 32;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float4 q = *reinterpret_cast<const float4*>(box + ((j ^ (lane & 7)) << 2));
@@ -338,8 +340,8 @@ struct TsIo {
   }
   // store v through input slot `slot` (already consumed by this thread's row)
   __device__ __forceinline__ void put_at(int slot, int map, const float (&v)[32], int c2, int c3) {
-    write_row(slot, v);
-    issue(slot, map, c2, c3);
+    write_row(ib + slot, v);
+    issue(ib + slot, map, c2, c3);
   }
 };
 
@@ -389,7 +391,9 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   constexpr bool TS = EpiTmaStore<Epi>::value;
   constexpr int kTsSlots = TS ? EpiTsSlots<Epi>::value : 0;
   constexpr int kTsIn = EpiTsIn<Epi>::value;
-  static_assert(kTsIn <= kTsSlots, "input boxes live in the TMA-store slots");
+  static_assert(kTsIn == 0 || 2 * kTsIn == kTsSlots,
+                "input boxes are double-buffered in the TMA-store slots");
+  static_assert(2 * (kStagesMax + 2 + 2 + EW) * 8 <= 512, "barrier area");
   constexpr bool TR = ZIN > 1 || EpiTransposed<Epi>::value;  // also the !s.ts fallback
   constexpr int kTcEpiWarps = EW;  // epilogue warps: EW / 4 per TMEM lane quadrant
   static_assert(EW % 4 == 0, "whole TMEM lane quadrants per epilogue warp group");
@@ -402,7 +406,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  uint64_t* wbar = tempty + 4;  // per epilogue warp: its TMA-loaded input boxes
+  uint64_t* wbar = tempty + 4;  // 2 per epilogue warp: its double-buffered TMA-loaded input boxes
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -446,7 +450,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       mbar_init(&tempty[a], kTcEpiWarps);
     }
     if constexpr (kTsIn > 0)
-      for (int w = 0; w < kTcEpiWarps; ++w) mbar_init(&wbar[w], 1);
+      for (int w = 0; w < 2 * kTcEpiWarps; ++w) mbar_init(&wbar[w], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -564,7 +568,29 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
     const int half = (warp - 2) >> 2;  // which of the EW/4 warps of this quadrant
     int lt = 0;
     int ts_next = 0;       // TMA-store box ring position
-    uint32_t ts_wph = 0;   // phase of this warp's input-box barrier
+    uint32_t ts_wph = 0;   // phases of this warp's two input-box barriers (bit = slot pair)
+    int ts_pair = 0;       // slot pair holding the current block's input boxes
+    float* const ts_slots = reinterpret_cast<float*>(smem + SM::kEpiOffset) +
+                            (warp - 2) * (kTsSlots > 0 ? kTsSlots : 1) * (kTsBoxBytes / 4);
+    // TMA loads of the input boxes of block (tile tq, column cq) into slot pair `pair`
+    auto ts_issue = [&](int tq, int cq, int pair) {
+      if constexpr (kTsIn > 0) {
+        int tn, tm, zb, zg, kb0, nkb;
+        tile_coords(tq, tn, tm, zb, zg, kb0, nkb);
+        uint64_t* bar = &wbar[(warp - 2) * 2 + pair];
+        mbar_expect_tx(bar, kTsIn * kTsBoxBytes);
+#pragma unroll
+        for (int i = 0; i < kTsIn; ++i) {
+          int c2, c3;
+          epi.ts_in(i, zb, zg, c2, c3);
+          tma_load_4d(ts_slots + (pair * kTsIn + i) * (kTsBoxBytes / 4), &tma_d, bar,
+                      tn * BN + cq, tm * kTcBM + quad * 32, c2, c3);
+        }
+      }
+    };
+    if constexpr (TS && kTsIn > 0) {
+      if (s.ts && lane == 0 && u0 < n_tiles) ts_issue(u0, half * 32, 0);
+    }
     for (int t = u0; t < n_tiles; t += ustride, ++lt) {
       int tn, tm, zb, zg, kb0, nkb;
       tile_coords(t, tn, tm, zb, zg, kb0, nkb);
@@ -581,19 +607,19 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
         if (s.dbg == 3) continue;  // microbenchmark ablation: no epilogue at all
         if constexpr (TS) {
           if (s.ts) {
-            float* slots = reinterpret_cast<float*>(smem + SM::kEpiOffset) +
-                           (warp - 2) * kTsSlots * (kTsBoxBytes / 4);
+            float* slots = ts_slots;
             if constexpr (kTsIn > 0) {
+              // this block's inputs were issued one block ahead; now issue the
+              // next block's (this warp's next column, or its next tile's first)
+              // into the other slot pair, whose stores must have read it
+              int tq = t, cq = c + 32 * (EW / 4);
+              if (cq >= BN) {
+                tq = t + ustride;
+                cq = half * 32;
+              }
               if (lane == 0) {
-                bulk_wait_read<0>();  // the slots' previous stores have read them
-                mbar_expect_tx(&wbar[warp - 2], kTsIn * kTsBoxBytes);
-#pragma unroll
-                for (int i = 0; i < kTsIn; ++i) {
-                  int c2, c3;
-                  epi.ts_in(i, zb, zg, c2, c3);
-                  tma_load_4d(slots + i * (kTsBoxBytes / 4), &tma_d, &wbar[warp - 2], n0 + c,
-                              m_base, c2, c3);
-                }
+                bulk_wait_read<0>();
+                if (tq < n_tiles) ts_issue(tq, cq, ts_pair ^ 1);
               }
             }
             float v[ZIN][32];
@@ -612,11 +638,14 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
                 for (int j = 0; j < 32; ++j) v[zi][j] = (float)(m * 1000 + n0 + c + j);
               }
             }
+            int ib = 0;
             if constexpr (kTsIn > 0) {
-              mbar_wait(&wbar[warp - 2], ts_wph);
-              ts_wph ^= 1u;
+              mbar_wait(&wbar[(warp - 2) * 2 + ts_pair], (ts_wph >> ts_pair) & 1u);
+              ts_wph ^= 1u << ts_pair;
+              ib = ts_pair * kTsIn;
+              ts_pair ^= 1;
             }
-            TsIo<kTsSlots> io{slots, {&tma_c, &tma_d}, n0 + c, m_base, &ts_next};
+            TsIo<kTsSlots> io{slots, {&tma_c, &tma_d}, n0 + c, m_base, &ts_next, ib};
             epi.ts_chunk(io, zb, zg, m, n0 + c, v);
             continue;
           }
