@@ -174,6 +174,10 @@ int edpc_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn,
 /* one GEMM through the tcgen05 path on host arrays (tests):
  * C[M][N] = A . B, A [M][K] (a_mn 0) or [K][M] (a_mn 1), B [N][K] (b_mn 0)
  * or [K][N] (b_mn 1) */
+/* Tests: the fp16-operand tcgen05 GEMM (A, B as IEEE half bits; lbo/sbo
+ * override the MN-major descriptor strides, 0 = default). */
+int edpc_debug_gemm_h(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn,
+                      const uint16_t* A, const uint16_t* B, float* C, int32_t lbo, int32_t sbo);
 int edpc_debug_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn, const float* A,
                     const float* B, float* C, int32_t dbg);
 

@@ -1671,6 +1671,42 @@ __global__ void k_fill_rand(float* p, int64_t n, uint32_t seed) {
   }
 }
 
+// fp16-operand GEMM of host matrices (tests): A, B as IEEE half bits;
+// lbo/sbo override the MN-major descriptor strides (0 = default).
+int edpc_debug_gemm_h(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn,
+                      const uint16_t* A, const uint16_t* B, float* C, int32_t lbo, int32_t sbo) {
+  EDPC_CHECK_ARG(A && B && C && M > 0 && N > 0 && K > 0, "bad arguments");
+  EDPC_CHECK_ARG(N % 64 == 0 && K % tc_bk<true>() == 0 && (N <= 256 || N % 256 == 0),
+                 "shape not supported by the fp16 tcgen05 path");
+  uint16_t *dA, *dB;
+  float* dC;
+  EDPC_CUDA_TRY(cudaMalloc(&dA, (size_t)M * K * 2));
+  EDPC_CUDA_TRY(cudaMalloc(&dB, (size_t)N * K * 2));
+  EDPC_CUDA_TRY(cudaMalloc(&dC, (size_t)M * N * 4));
+  EDPC_CUDA_TRY(cudaMemcpy(dA, A, (size_t)M * K * 2, cudaMemcpyHostToDevice));
+  EDPC_CUDA_TRY(cudaMemcpy(dB, B, (size_t)N * K * 2, cudaMemcpyHostToDevice));
+  EDPC_CUDA_TRY(cudaMemset(dC, 0, (size_t)M * N * 4));
+  TcShape s{M, N, K, 1, 1, kBatchNone, kBatchNone, 0, 1, 0, 0, 0};
+  s.mn_lbo = lbo;
+  s.mn_sbo = sbo;
+  TcOperand a{dA, a_mn ? M : K, 0, 1}, b{dB, b_mn ? N : K, 0, 1};
+  EpiStore e{dC, N};
+  int st;
+  if (!a_mn && !b_mn) st = tc_gemm<false, false, true>(s, a, b, e, 0);
+  else if (!a_mn && b_mn) st = tc_gemm<false, true, true>(s, a, b, e, 0);
+  else if (a_mn && !b_mn) st = tc_gemm<true, false, true>(s, a, b, e, 0);
+  else st = tc_gemm<true, true, true>(s, a, b, e, 0);
+  cudaError_t ce = cudaDeviceSynchronize();
+  if (st == EDPC_OK && ce == cudaSuccess)
+    ce = cudaMemcpy(C, dC, (size_t)M * N * 4, cudaMemcpyDeviceToHost);
+  cudaFree(dA);
+  cudaFree(dB);
+  cudaFree(dC);
+  if (st != EDPC_OK) return st;
+  EDPC_CUDA_TRY(ce);
+  return EDPC_OK;
+}
+
 // Microbenchmark of the bare tcgen05 GEMM (store-only epilogue) on device
 // operands: average ms over iters launches (CUDA events).  kmode 2 splits K.
 int edpc_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn, int32_t nsplit,
@@ -1687,7 +1723,15 @@ int edpc_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn,
   TcOperand a{dA, a_mn ? M : K, 0, 1}, b{dB, b_mn ? N : K, 0, 1};
   if (const char* d = getenv("EDPC_GEMM_DBG")) s.dbg = atoi(d);
   EpiSplit e{dC, N, (int64_t)M * N};
+  const char* hf = getenv("EDPC_GEMM_F16");  // fp16 operands (timing only: the fp32
+  const bool h = hf && hf[0] == '1';          // random bits are read as halves)
   auto run = [&]() {
+    if (h) {
+      if (!a_mn && !b_mn) return tc_gemm<false, false, true>(s, a, b, e, 0);
+      if (!a_mn && b_mn) return tc_gemm<false, true, true>(s, a, b, e, 0);
+      if (a_mn && !b_mn) return tc_gemm<true, false, true>(s, a, b, e, 0);
+      return tc_gemm<true, true, true>(s, a, b, e, 0);
+    }
     if (!a_mn && !b_mn) return tc_gemm<false, false>(s, a, b, e, 0);
     if (!a_mn && b_mn) return tc_gemm<false, true>(s, a, b, e, 0);
     if (a_mn && !b_mn) return tc_gemm<true, false>(s, a, b, e, 0);

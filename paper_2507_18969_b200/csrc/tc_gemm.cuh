@@ -163,6 +163,16 @@ __device__ __forceinline__ void tc_mma_tf32(uint32_t tmem_d, uint64_t adesc, uin
       : "memory");
 }
 
+__device__ __forceinline__ void tc_mma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 // 32 lanes x 32 consecutive fp32 columns -> 32 registers per thread
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   uint32_t r[32];
@@ -201,11 +211,26 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 }
 constexpr uint32_t kLayoutSW128 = 2, kLayoutSW128Base32B = 1;
 
-// instruction descriptor: D f32, A/B tf32, majors, N>>3, M>>4
+// instruction descriptor: D f32, A/B tf32 (format 2) or f16 (format 0),
+// majors, N>>3, M>>4
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int a_mn, int b_mn) {
   return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+__host__ __device__ constexpr uint32_t idesc_f16(int M, int N, int a_mn, int b_mn) {
+  return (1u << 4) | ((uint32_t)a_mn << 15) | ((uint32_t)b_mn << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// fp16 operands (H): 128-byte smem rows hold 64 elements of K (K-major) or of
+// M/N (MN-major, the standard SWIZZLE_128B layout: 64-wide MN atoms of 8
+// K-rows, one TMA box of 64 x 64 per atom column); 4 MMAs of K = 16 per
+// k-block, as the tf32 path's 4 of K = 8 -- same smem bytes per stage.
+template <bool H>
+__host__ __device__ constexpr int tc_bk() {
+  return H ? 64 : 32;
+}
+constexpr uint32_t kMnH_LBO = 8192, kMnH_SBO = 1024;
 
 // ------------------------------------------------------------------ shapes
 
@@ -380,12 +405,16 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 // same (tn, z); each CTA TMA-multicasts one half of the shared B tile to
 // both, so per-SM operand traffic per k-block drops from A+B to A+B/2.
 // Stage reuse then needs both CTAs' MMA commits (and bias reads).
-template <int BN, bool AMN, bool BMN, bool BIAS, class Epi, int ZIN = 1, int CL = 1, int EW = 8>
+template <int BN, bool AMN, bool BMN, bool BIAS, class Epi, int ZIN = 1, int CL = 1, int EW = 8,
+          bool H = false>
 __global__ void __launch_bounds__(tc_threads(BIAS, EW), 1)
 k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
           const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_d,
           TcShape s, Epi epi) {
   static_assert(!BIAS || BMN, "fused bias sums read an MN-major B tile");
+  static_assert(!BIAS || !H, "fused bias sums read fp32 B tiles");
+  static_assert(!H || !BMN || BN % 64 == 0, "fp16 MN-major B boxes are 64 wide");
+  constexpr int BK = tc_bk<H>();
   static_assert(ZIN == 1 || !BIAS, "multi-branch tiles have no fused bias");
   static_assert(TcSmem<BN, ZIN>::kCols <= 512, "TMEM holds 512 columns");
   constexpr bool TS = EpiTmaStore<Epi>::value;
@@ -437,7 +466,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       k_end = k_begin + chunk;
     }
     kb0 = k_begin;
-    nkb = (k_end - k_begin) / kTcBK;
+    nkb = (k_end - k_begin) / BK;
   };
 
   if (warp == 0 && lane == 0) {
@@ -479,16 +508,17 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
           const uint32_t ph = (uint32_t)(it / kStages) & 1u;
           mbar_wait(&empty[st], ph ^ 1u);
           const int sub = q / nkb;
-          const int k = kb0 + (q - sub * nkb) * kTcBK;
+          const int k = kb0 + (q - sub * nkb) * BK;
           const int az = s.a_batch == kBatchZ ? zb : (s.a_batch == kBatchSum ? sub : 0);
           const int bz = s.b_batch == kBatchZ ? zb : (s.b_batch == kBatchSum ? sub : 0);
           uint8_t* sa = smem + st * SM::kStageBytes;
           uint8_t* sb = sa + SM::kABytes;
           mbar_expect_tx(&full[st], SM::kStageBytes);
           if (AMN) {
+            constexpr int kW = H ? 64 : 32;  // MN width of one box
 #pragma unroll
-            for (int j = 0; j < kTcBM / 32; ++j)
-              tma_load_3d(sa + j * 4096, &tma_a, &full[st], m0 + 32 * j, k, az);
+            for (int j = 0; j < kTcBM / kW; ++j)
+              tma_load_3d(sa + j * kW * 128, &tma_a, &full[st], m0 + kW * j, k, az);
           } else {
             tma_load_3d(sa, &tma_a, &full[st], k, m0, az);
           }
@@ -496,22 +526,24 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
           for (int zi = 0; zi < ZIN; ++zi) {
             const int bzz = ZIN > 1 ? zi : bz;
             uint8_t* sbz = sb + zi * SM::kBBytes;
+            constexpr int kW = H ? 64 : 32;
             if constexpr (CL == 1) {
               if (BMN) {
 #pragma unroll
-                for (int j = 0; j < BN / 32; ++j)
-                  tma_load_3d(sbz + j * 4096, &tma_b, &full[st], n0 + 32 * j, k, bzz);
+                for (int j = 0; j < BN / kW; ++j)
+                  tma_load_3d(sbz + j * kW * 128, &tma_b, &full[st], n0 + kW * j, k, bzz);
               } else {
                 tma_load_3d(sbz, &tma_b, &full[st], k, n0, bzz);
               }
             } else {
               // this CTA's half of B, multicast into both CTAs of the pair
               if (BMN) {
-                constexpr int nb = BN / 32 / CL;
+                constexpr int nb = BN / kW / CL > 0 ? BN / kW / CL : 1;
 #pragma unroll
                 for (int jj = 0; jj < nb; ++jj) {
                   const int j = crank * nb + jj;
-                  tma_load_3d_mc(sbz + j * 4096, &tma_b, &full[st], n0 + 32 * j, k, bzz, kMask);
+                  tma_load_3d_mc(sbz + j * kW * 128, &tma_b, &full[st], n0 + kW * j, k, bzz,
+                                 kMask);
                 }
               } else {
                 constexpr int rows = BN / CL;
@@ -526,7 +558,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer
-      constexpr uint32_t idesc = idesc_tf32(kTcBM, BN, AMN ? 1 : 0, BMN ? 1 : 0);
+      constexpr uint32_t idesc = H ? idesc_f16(kTcBM, BN, AMN ? 1 : 0, BMN ? 1 : 0)
+                                   : idesc_tf32(kTcBM, BN, AMN ? 1 : 0, BMN ? 1 : 0);
+      const uint32_t mlbo = s.mn_lbo ? (uint32_t)s.mn_lbo : kMnH_LBO;
+      const uint32_t msbo = s.mn_sbo ? (uint32_t)s.mn_sbo : kMnH_SBO;
       int it = 0, lt = 0;
       for (int t = u0; t < n_tiles; t += ustride, ++lt) {
         int tn, tm, zb, zg, kb0, nkb;
@@ -546,12 +581,21 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
           for (int zi = 0; zi < ZIN; ++zi) {
             const uint32_t sb = sa + SM::kABytes + zi * SM::kBBytes;
 #pragma unroll
-            for (int kk = 0; kk < kTcBK / 8; ++kk) {
-              const uint64_t ad = AMN ? sdesc(sa + kk * 1024, 4096, 512, kLayoutSW128Base32B)
-                                      : sdesc(sa + kk * 32, 16, 1024, kLayoutSW128);
-              const uint64_t bd = BMN ? sdesc(sb + kk * 1024, 4096, 512, kLayoutSW128Base32B)
-                                      : sdesc(sb + kk * 32, 16, 1024, kLayoutSW128);
-              tc_mma_tf32(dtm + (uint32_t)(zi * BN), ad, bd, idesc, (q > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < 4; ++kk) {
+              if constexpr (H) {
+                const uint64_t ad = AMN ? sdesc(sa + kk * 2048, mlbo, msbo, kLayoutSW128)
+                                        : sdesc(sa + kk * 32, 16, 1024, kLayoutSW128);
+                const uint64_t bd = BMN ? sdesc(sb + kk * 2048, mlbo, msbo, kLayoutSW128)
+                                        : sdesc(sb + kk * 32, 16, 1024, kLayoutSW128);
+                tc_mma_f16(dtm + (uint32_t)(zi * BN), ad, bd, idesc, (q > 0 || kk > 0) ? 1u : 0u);
+              } else {
+                const uint64_t ad = AMN ? sdesc(sa + kk * 1024, 4096, 512, kLayoutSW128Base32B)
+                                        : sdesc(sa + kk * 32, 16, 1024, kLayoutSW128);
+                const uint64_t bd = BMN ? sdesc(sb + kk * 1024, 4096, 512, kLayoutSW128Base32B)
+                                        : sdesc(sb + kk * 32, 16, 1024, kLayoutSW128);
+                tc_mma_tf32(dtm + (uint32_t)(zi * BN), ad, bd, idesc,
+                            (q > 0 || kk > 0) ? 1u : 0u);
+              }
             }
           }
           if constexpr (CL == 1)
@@ -791,11 +835,14 @@ inline PfnEncodeTiled encode_tiled_fn() {
 }
 
 // 3-D fp32 tensor map: dims {inner, rows, batch}; strides in elements.
-inline int make_tmap(CUtensorMap* map, const float* base, uint64_t inner, uint64_t rows,
+// kind: bit 0 = MN-major, bit 1 = fp16 elements
+inline int make_tmap(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,
                      uint64_t batch, uint64_t row_stride, uint64_t batch_stride, uint32_t box_inner,
-                     uint32_t box_rows, bool mn_major) {
+                     uint32_t box_rows, int kind) {
+  const bool mn_major = kind & 1, half = kind & 2;
+  const uint64_t es = half ? 2 : 4;
   cuuint64_t dims[3] = {inner, rows, batch < 1 ? 1 : batch};
-  cuuint64_t strides[2] = {row_stride * 4, (batch_stride ? batch_stride : row_stride * rows) * 4};
+  cuuint64_t strides[2] = {row_stride * es, (batch_stride ? batch_stride : row_stride * rows) * es};
   cuuint32_t box[3] = {box_inner, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   PfnEncodeTiled enc = encode_tiled_fn();
@@ -803,10 +850,10 @@ inline int make_tmap(CUtensorMap* map, const float* base, uint64_t inner, uint64
     set_error("cuTensorMapEncodeTiled entry point unavailable");
     return EDPC_ERR_CUDA;
   }
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims,
-                                      strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                      mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
-                                               : CU_TENSOR_MAP_SWIZZLE_128B,
+  CUresult r = enc(map, half ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                   3, (void*)base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   (mn_major && !half) ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B
+                                       : CU_TENSOR_MAP_SWIZZLE_128B,
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
@@ -878,7 +925,7 @@ inline int ts_maps(const Epi& epi, const TcShape& s, CUtensorMap& tc, CUtensorMa
 
 // An operand as stored in global memory: row-major [rows][inner] (+ batch).
 struct TcOperand {
-  const float* ptr;
+  const void* ptr;  // fp32, or fp16 on the H path
   int64_t ld;      // row stride (elements)
   int64_t sbatch;  // batch stride (elements), 0 if no batch
   int nbatch;
@@ -887,11 +934,11 @@ struct TcOperand {
 struct TmapCache {
   std::mutex mu;
   std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint32_t,
-                      uint32_t, bool>,
+                      uint32_t, int>,
            CUtensorMap>
       maps;
-  int get(CUtensorMap* out, const float* base, uint64_t inner, uint64_t rows, uint64_t batch,
-          uint64_t ld, uint64_t sb, uint32_t bi, uint32_t br, bool mn) {
+  int get(CUtensorMap* out, const void* base, uint64_t inner, uint64_t rows, uint64_t batch,
+          uint64_t ld, uint64_t sb, uint32_t bi, uint32_t br, int mn) {
     auto key = std::make_tuple((const void*)base, inner, rows, batch, ld, sb, bi, br, mn);
     std::lock_guard<std::mutex> g(mu);
     auto it = maps.find(key);
@@ -966,7 +1013,33 @@ inline void set_smem_attr(Kern kern, int bytes, bool& done) {
   }
 }
 
-template <int BN, bool AMN, bool BMN, class Epi>
+// TMA maps of the two operands.  A: K-major -> [M rows][K inner]; MN-major ->
+// [K rows][M inner].  B: K-major -> [N rows][K inner] (box BN/cl rows);
+// MN-major -> [K rows][N inner].  fp32 boxes are 32 elements (128 B) wide,
+// fp16 boxes 64; MN-major boxes are square.
+template <int BN, bool AMN, bool BMN, bool H>
+inline int tc_operand_maps(const TcShape& s, const TcOperand& A, const TcOperand& B, int cl,
+                           CUtensorMap& ta, CUtensorMap& tb) {
+  constexpr uint32_t W = tc_bk<H>();
+  constexpr int kh = H ? 2 : 0;
+  int r;
+  if (AMN)
+    r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.M, (uint64_t)s.K, (uint64_t)A.nbatch,
+                         (uint64_t)A.ld, (uint64_t)A.sbatch, W, W, 1 | kh);
+  else
+    r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.K, (uint64_t)s.M, (uint64_t)A.nbatch,
+                         (uint64_t)A.ld, (uint64_t)A.sbatch, W, kTcBM, kh);
+  if (r != EDPC_OK) return r;
+  if (BMN)
+    r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.N, (uint64_t)s.K, (uint64_t)B.nbatch,
+                         (uint64_t)B.ld, (uint64_t)B.sbatch, W, W, 1 | kh);
+  else
+    r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.K, (uint64_t)s.N, (uint64_t)B.nbatch,
+                         (uint64_t)B.ld, (uint64_t)B.sbatch, W, BN / cl, kh);
+  return r;
+}
+
+template <int BN, bool AMN, bool BMN, bool H = false, class Epi>
 inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, const Epi& epi,
                      cudaStream_t st) {
   constexpr bool kTS = EpiTmaStore<Epi>::value;
@@ -978,21 +1051,7 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
   TcShape s2 = s;
   if constexpr (kTS) s2.ts = ts_maps(epi, s, tc, td);
   int r;
-  // A: K-major -> [M rows][K inner]; MN-major -> [K rows][M inner]
-  if (AMN)
-    r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.M, (uint64_t)s.K, (uint64_t)A.nbatch,
-                         (uint64_t)A.ld, (uint64_t)A.sbatch, 32, 32, true);
-  else
-    r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.K, (uint64_t)s.M, (uint64_t)A.nbatch,
-                         (uint64_t)A.ld, (uint64_t)A.sbatch, 32, kTcBM, false);
-  if (r != EDPC_OK) return r;
-  // B: K-major -> [N rows][K inner] (box BN/cl rows); MN-major -> [K rows][N inner]
-  if (BMN)
-    r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.N, (uint64_t)s.K, (uint64_t)B.nbatch,
-                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, 32, true);
-  else
-    r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.K, (uint64_t)s.N, (uint64_t)B.nbatch,
-                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN / cl, false);
+  r = tc_operand_maps<BN, AMN, BMN, H>(s, A, B, cl, ta, tb);
   if (r != EDPC_OK) return r;
   const int nz = s.nzb * (s.kmode == 0 ? 1 : s.nsplit);
   const int units = (s.N / BN) * (n_tm / cl) * nz;
@@ -1003,16 +1062,16 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
   const int di = dev < 16 ? dev : 0;
   cudaError_t e = cudaSuccess;
   bool launched = false;
-  if constexpr (BMN) {
+  if constexpr (BMN && !H) {
     if (s.bias_part) {
       if (cl == 2) {
         static bool done[16] = {};
-        auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi, 1, 2>;
+        auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi, 1, 2, 8, H>;
         set_smem_attr(kern, kSmem, done[di]);
         e = launch_tc(kern, grid, tc_threads(true), kSmem, st, 2, ta, tb, tc, td, s2, epi);
       } else {
         static bool done[16] = {};
-        auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi, 1, 1>;
+        auto kern = k_tc_gemm<BN, AMN, BMN, true, Epi, 1, 1, 8, H>;
         set_smem_attr(kern, kSmem, done[di]);
         e = launch_tc(kern, grid, tc_threads(true), kSmem, st, 1, ta, tb, tc, td, s2, epi);
       }
@@ -1022,12 +1081,12 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
   if (!launched) {
     if (cl == 2) {
       static bool done[16] = {};
-      auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi, 1, 2>;
+      auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi, 1, 2, 8, H>;
       set_smem_attr(kern, kSmem, done[di]);
       e = launch_tc(kern, grid, tc_threads(false), kSmem, st, 2, ta, tb, tc, td, s2, epi);
     } else {
       static bool done[16] = {};
-      auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi, 1, 1>;
+      auto kern = k_tc_gemm<BN, AMN, BMN, false, Epi, 1, 1, 8, H>;
       set_smem_attr(kern, kSmem, done[di]);
       e = launch_tc(kern, grid, tc_threads(false), kSmem, st, 1, ta, tb, tc, td, s2, epi);
     }
@@ -1041,7 +1100,7 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
 }
 
 // Multi-branch launch: ZIN branch GEMMs sharing A, one CTA per (tm, tn).
-template <int BN, int ZIN, bool BMN, class Epi>
+template <int BN, int ZIN, bool BMN, bool H = false, class Epi>
 inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& B,
                          const Epi& epi, cudaStream_t st) {
   // the transposed fused-GeLU epilogue is issue-bound (16 epilogue warps);
@@ -1052,15 +1111,7 @@ inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& 
   const int n_tm = cdiv(s.M, kTcBM);
   const int cl = (cluster_enabled() && n_tm % 2 == 0) ? 2 : 1;
   CUtensorMap ta, tb;
-  int r = tmap_cache().get(&ta, A.ptr, (uint64_t)s.K, (uint64_t)s.M, (uint64_t)A.nbatch,
-                           (uint64_t)A.ld, (uint64_t)A.sbatch, 32, kTcBM, false);
-  if (r != EDPC_OK) return r;
-  if (BMN)
-    r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.N, (uint64_t)s.K, (uint64_t)B.nbatch,
-                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, 32, true);
-  else
-    r = tmap_cache().get(&tb, B.ptr, (uint64_t)s.K, (uint64_t)s.N, (uint64_t)B.nbatch,
-                         (uint64_t)B.ld, (uint64_t)B.sbatch, 32, BN / cl, false);
+  int r = tc_operand_maps<BN, false, BMN, H>(s, A, B, cl, ta, tb);
   if (r != EDPC_OK) return r;
   CUtensorMap tc{}, td{};
   TcShape s2 = s;
@@ -1074,12 +1125,12 @@ inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& 
   cudaError_t e;
   if (cl == 2) {
     static bool done[16] = {};
-    auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 2, kZinEW>;
+    auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 2, kZinEW, H>;
     set_smem_attr(kern, kSmem, done[di]);
     e = launch_tc(kern, grid, tc_threads(false, kZinEW), kSmem, st, 2, ta, tb, tc, td, s2, epi);
   } else {
     static bool done[16] = {};
-    auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 1, kZinEW>;
+    auto kern = k_tc_gemm<BN, false, BMN, false, Epi, ZIN, 1, kZinEW, H>;
     set_smem_attr(kern, kSmem, done[di]);
     e = launch_tc(kern, grid, tc_threads(false, kZinEW), kSmem, st, 1, ta, tb, tc, td, s2, epi);
   }
@@ -1101,7 +1152,7 @@ inline int bn_cap() {
   return v;
 }
 
-template <bool AMN, bool BMN, class Epi>
+template <bool AMN, bool BMN, bool H = false, class Epi>
 inline int tc_gemm(const TcShape& s, const TcOperand& A, const TcOperand& B, const Epi& epi,
                    cudaStream_t st) {
   // Tile width: the widest BN whose tile count still fills 3/4 of the SMs;
@@ -1114,15 +1165,17 @@ inline int tc_gemm(const TcShape& s, const TcOperand& A, const TcOperand& B, con
   const int want = num_sms() * 3 / 4;
   int bn = 0;
   for (int c : {256, 128, 64, 32}) {
-    if (c > cap || s.N % c != 0) continue;
+    if (c > cap || s.N % c != 0 || (H && BMN && c < 64)) continue;
     bn = c;
     if ((s.N / c) * n_tm * nz >= want) break;
   }
   switch (bn) {
-    case 256: return tc_launch<256, AMN, BMN>(s, A, B, epi, st);
-    case 128: return tc_launch<128, AMN, BMN>(s, A, B, epi, st);
-    case 64: return tc_launch<64, AMN, BMN>(s, A, B, epi, st);
-    case 32: return tc_launch<32, AMN, BMN>(s, A, B, epi, st);
+    case 256: return tc_launch<256, AMN, BMN, H>(s, A, B, epi, st);
+    case 128: return tc_launch<128, AMN, BMN, H>(s, A, B, epi, st);
+    case 64: return tc_launch<64, AMN, BMN, H>(s, A, B, epi, st);
+    case 32:
+      if constexpr (!(H && BMN)) return tc_launch<32, AMN, BMN, H>(s, A, B, epi, st);
+      break;
   }
   set_error("tc_gemm: unsupported N");
   return EDPC_ERR_INVALID;

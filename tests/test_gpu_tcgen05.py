@@ -100,3 +100,24 @@ def test_tc_gemm_unit(M, N, K, a_mn, b_mn):
     ref = A.astype(np.float64) @ B.astype(np.float64)
     err = np.abs(C - ref).max() / np.abs(ref).max()
     assert err < 3e-3, (err, C[:2, :4], ref[:2, :4])
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 64, 64), (128, 256, 128), (256, 512, 256), (200, 128, 192)])
+@pytest.mark.parametrize("a_mn", [0, 1])
+@pytest.mark.parametrize("b_mn", [0, 1])
+def test_tc_gemm_f16_unit(M, N, K, a_mn, b_mn):
+    """fp16-operand tcgen05 GEMM (kind::f16, fp32 accumulate) vs float64 numpy
+    on the same fp16 values: products are exact, only the fp32 sums round."""
+    if not _lib.load().edpc_has_tcgen05():
+        pytest.skip("tcgen05 path not compiled")
+    rng = np.random.default_rng(7 * M + N + K)
+    A = rng.normal(size=(M, K)).astype(np.float16)
+    B = rng.normal(size=(K, N)).astype(np.float16)
+    Ah = np.ascontiguousarray(A.T) if a_mn else A
+    Bh = B if b_mn else np.ascontiguousarray(B.T)
+    C = np.empty((M, N), dtype=np.float32)
+    _lib.check(_lib.load().edpc_debug_gemm_h(M, N, K, a_mn, b_mn, Ah.ctypes.data,
+                                             Bh.ctypes.data, C.ctypes.data, 0, 0))
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    err = np.abs(C - ref).max() / np.abs(ref).max()
+    assert err < 1e-5, (err, C[:2, :4], ref[:2, :4])
