@@ -99,6 +99,10 @@ int edpc_decode_rows(int device, int64_t* dec_state, const uint8_t* data, int64_
 int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_len,
                     int32_t device, int32_t lane_begin, int32_t lane_count, edpc_ctx** out);
 int edpc_ctx_destroy(edpc_ctx* ctx);
+/* Numerics the context runs (a function of the config, part of the format):
+ * bit 0 = tcgen05 tensor-core GEMMs (tf32), bit 1 = fp16 operands for the
+ * MBRB branch / out-projection GEMMs. */
+int edpc_ctx_numerics(edpc_ctx* ctx, int32_t* flags);
 int edpc_ctx_info(edpc_ctx* ctx, int64_t* lane_len, int64_t* n_params, int64_t* n_shared);
 
 /* fp32 parameters in the reference parameters() order (model.py:237-239),

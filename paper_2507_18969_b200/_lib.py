@@ -87,6 +87,7 @@ _SIGS = {
     "edpc_ctx_set_comm": ([_P, _P, _I32, _I32], ctypes.c_int),
     "edpc_sync": ([_P], ctypes.c_int),
     "edpc_debug_read": ([_P, _I32, _P, _I64], ctypes.c_int),
+    "edpc_ctx_numerics": ([_P, _P], ctypes.c_int),
     "edpc_debug_gemm": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _I32], ctypes.c_int),
     "edpc_debug_gemm_h": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _I32, _I32], ctypes.c_int),
     "edpc_bench_gemm": ([_I32, _I32, _I32, _I32, _I32, _I32, _I32, _P], ctypes.c_int),

@@ -1,6 +1,7 @@
 // Shared helpers for the EDPC B200 kernels: status plumbing, warp reductions.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 

@@ -63,7 +63,8 @@ template <bool kGather>
 __global__ void __launch_bounds__(256)
 k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE, int F, int Bl,
            float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
-           float* __restrict__ xhat, float* __restrict__ rstd, float* __restrict__ x0) {
+           float* __restrict__ xhat, float* __restrict__ rstd, float* __restrict__ x0,
+           __half* __restrict__ x0h) {
   const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= Bl) return;
@@ -92,7 +93,11 @@ k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE,
   for (int f = lane; f < F; f += 32) {
     float h = (xr[f] - mean) * r;
     xhat[(int64_t)b * F + f] = h;
-    x0[(int64_t)b * F + f] = h * gain[f] + bias[f];
+    const float v = h * gain[f] + bias[f];
+    if (x0h)  // fp16 GEMM path: x0 only feeds the branch GEMM and its weight gradient
+      x0h[(int64_t)b * F + f] = __float2half_rn(v);
+    else
+      x0[(int64_t)b * F + f] = v;
   }
   if (lane == 0) rstd[b] = r;
 }
@@ -322,6 +327,90 @@ struct EpiBwdAct {
   }
 };
 
+
+// fp16 forms of the two fused MBRB epilogues (the fp16 GEMM path): the same
+// math in fp32 registers, ff / D_z / g_H stored as fp16 through 64B-swizzled
+// TMA boxes (half the bytes of the fp32 path; 10-bit mantissa = the tf32
+// operand precision these values feed).  TMA-only: a launch whose tensor
+// maps cannot be built fails instead of taking a fallback.
+template <int ZIN>
+struct EpiBranchActH {
+  static constexpr bool kTmaStore = true, kRequireTs = true;
+  static constexpr int kTsSlots = 2;
+  __half* H;        // D_z [ZIN][M][N]
+  __half* ff;       // [M][N]
+  const float* b0;  // bias of branch 0; branch z at b0 + z*sBias
+  int64_t sBias, N, plane;
+  bool store_maps(const TcShape& s, TcStoreMap& c, TcStoreMap& d) const {
+    c = TcStoreMap{H, {(uint64_t)N, (uint64_t)s.M, (uint64_t)ZIN, 1}, {(uint64_t)N, (uint64_t)plane, 0}, 1};
+    d = TcStoreMap{ff, {(uint64_t)N, (uint64_t)s.M, 1, 1}, {(uint64_t)N, 0, 0}, 1};
+    return true;
+  }
+  template <class IO>
+  __device__ void ts_chunk(IO& io, int, int, int, int n0, float (&v)[ZIN][32]) const {
+    float p[32];
+#pragma unroll
+    for (int z = 0; z < ZIN; ++z) {
+      float b[32];
+      load32(b0 + z * sBias + n0, b);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) v[z][j] = v[z][j] + b[j];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) p[j] = z == 0 ? v[0][j] : p[j] * v[z][j];
+    }
+    {
+      float f[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) gelu_pair(p[j], f[j], p[j]);
+      io.put_h(1, f, 0, 0);
+    }
+#pragma unroll
+    for (int z = 0; z < ZIN; ++z) {
+      float d[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        d[j] = p[j];
+#pragma unroll
+        for (int y = 0; y < ZIN; ++y)
+          if (y != z) d[j] = d[j] * v[y][j];
+      }
+      io.put_h(0, d, z, 0);
+    }
+  }
+  __device__ void row32(int, int, int, int, float (&)[32]) const { __trap(); }
+  __device__ void tile(const float*, int, int, int, int, int) const { __trap(); }
+  __device__ void tile_z(const float*, int, int, int) const { __trap(); }
+};
+
+struct EpiBwdActH {
+  static constexpr bool kTmaStore = true, kRequireTs = true;
+  static constexpr int kTsSlots = 4, kTsIn = 2, kTsInBytes = 32 * 32 * 2;
+  const __half* H;  // D_z
+  __half* GH;
+  int K;
+  int64_t plane, ld;
+  bool store_maps(const TcShape& s, TcStoreMap& c, TcStoreMap& d) const {
+    if (K != kTsIn) return false;
+    c = TcStoreMap{GH, {(uint64_t)s.N, (uint64_t)s.M, (uint64_t)K, 1}, {(uint64_t)ld, (uint64_t)plane, 0}, 1};
+    d = TcStoreMap{H, {(uint64_t)s.N, (uint64_t)s.M, (uint64_t)K, 1}, {(uint64_t)ld, (uint64_t)plane, 0}, 1};
+    return true;
+  }
+  __device__ void ts_in(int i, int, int, int& c2, int& c3) const { c2 = i; c3 = 0; }
+  template <class IO>
+  __device__ void ts_chunk(IO& io, int, int, int, int, float (&v)[1][32]) const {
+#pragma unroll
+    for (int z = 0; z < kTsIn; ++z) {
+      float d[32];
+      io.in_h(z, d);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) d[j] = v[0][j] * d[j];
+      io.put_at_h(z, 0, d, z, 0);
+    }
+  }
+  __device__ void operator()(int, int, int, int, float) const { __trap(); }
+  __device__ void row32(int, int, int, int, float (&)[32]) const { __trap(); }
+  __device__ void tile(const float*, int, int, int, int, int) const { __trap(); }
+};
 
 // LN backward + residual (nn.py:116-125, model.py:120-121); one warp per lane
 __global__ void __launch_bounds__(256)
@@ -568,7 +657,7 @@ __global__ void __launch_bounds__(256)
 k_fdm_bwd_adam(const float* __restrict__ down, const float* __restrict__ gmix,
                float* __restrict__ U, float* __restrict__ Um, float* __restrict__ Uv,
                float* __restrict__ gdown, int FP, int Bl, StepIdx si, AdamConsts c, double b1d,
-               double b2d) {
+               double b2d, float ginv) {
   const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= Bl) return;
@@ -579,7 +668,7 @@ k_fdm_bwd_adam(const float* __restrict__ down, const float* __restrict__ gmix,
   const int64_t base = (int64_t)b * FP * FP;
   for (int i = 0; i < FP; ++i) {
     float acc = 0.f;
-    const float di = d[i];
+    const float di = d[i] * ginv;  // gradient scale removed exactly (see k_dlogits)
     for (int j = lane; j < FP; j += 32) {
       const int64_t e = base + (int64_t)i * FP + j;
       float w = U[e], m = Um[e], v = Uv[e];
@@ -649,7 +738,7 @@ __global__ void __launch_bounds__(256)
 k_fdm_bwd_adam_v(const float* __restrict__ down, const float* __restrict__ gmix,
                  float* __restrict__ U, float* __restrict__ Um, float* __restrict__ Uv,
                  float* __restrict__ gdown, int Bl, StepIdx si, AdamConsts c, double b1d,
-                 double b2d) {
+                 double b2d, float ginv) {
   using G = FdmGeo<FP>;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -687,7 +776,7 @@ k_fdm_bwd_adam_v(const float* __restrict__ down, const float* __restrict__ gmix,
     float part[kR];
 #pragma unroll
     for (int r = 0; r < kR; ++r) {
-      const float di = ADAM ? d[i0 + r] : 0.f;
+      const float di = ADAM ? d[i0 + r] * ginv : 0.f;  // (d ginv) g == d (g ginv): exact
       part[r] = 0.f;
 #pragma unroll
       for (int v = 0; v < G::kNV; ++v) {
@@ -856,13 +945,62 @@ __global__ void k_embed_grad_reduce(const float* __restrict__ sub, const int* __
   partials[(int64_t)gg * n_shared + off + e] = acc;
 }
 
+// ------------------------------------------------------- fp16 helpers
+
+__global__ void k_to_half(const float* __restrict__ src, __half* __restrict__ dst, int64_t n) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = __float2half_rn(src[e]);
+}
+
+// k_colsum_groups over an fp16 source (the fp16 branch-output gradients):
+// per lane group, column sums in fp32, same fixed order (warp-strided lanes,
+// then the 8 warps in order).  4 columns per thread.
+__global__ void __launch_bounds__(256)
+k_colsum_groups_h(const __half* __restrict__ src, int64_t ld, int64_t sz, int N,
+                  float* __restrict__ partials, int64_t n_shared, int64_t off, int64_t sOff,
+                  int g0, int B_global, int lane0) {
+  __shared__ float4 red[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n = blockIdx.x * 128 + lane * 4;
+  const int z = blockIdx.y;
+  const int gg = g0 + blockIdx.z;
+  const int b0 = group_begin(gg, B_global) - lane0, b1 = group_begin(gg + 1, B_global) - lane0;
+  const __half* s = src + z * sz;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (n < N) {
+#pragma unroll 4
+    for (int b = b0 + warp; b < b1; b += 8) {
+      const uint2 q = *reinterpret_cast<const uint2*>(s + (int64_t)b * ld + n);
+      const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&q.x));
+      const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&q.y));
+      acc.x += lo.x; acc.y += lo.y; acc.z += hi.x; acc.w += hi.y;
+    }
+  }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && n < N) {
+    float4 t = red[0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      const float4 u = red[w][lane];
+      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
+    }
+    float* dst = partials + (int64_t)gg * n_shared + off + z * sOff + n;
+    dst[0] = t.x;
+    dst[1] = t.y;
+    dst[2] = t.z;
+    dst[3] = t.w;
+  }
+}
+
 // ------------------------------------------------------- Adam (shared)
 
 // grad = ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)) -- the canonical G-invariant
 // tree over the 8 lane groups -- then fused Adam (_kernels.py:18-32).
 __global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, float* __restrict__ V,
                               const float* __restrict__ P, int64_t n, StepIdx si, AdamConsts c,
-                              double b1d, double b2d) {
+                              double b1d, double b2d, float ginv, __half* __restrict__ Wh) {
   float bc1, bc2;
   adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
@@ -870,10 +1008,11 @@ __global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, floa
     float q[8];
 #pragma unroll
     for (int g = 0; g < 8; ++g) q[g] = P[g * n + e];
-    const float grad = ((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]));
+    const float grad = (((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]))) * ginv;
     float w = W[e], m = M[e], v = V[e];
     adam_elem(w, m, v, grad, c, bc1, bc2);
     W[e] = w;
+    if (Wh) Wh[e] = __float2half_rn(w);  // fp16 shadow for the fp16 GEMMs
     M[e] = m;
     V[e] = v;
   }
@@ -951,8 +1090,12 @@ k_softmax_quant(const float* __restrict__ logits, float* __restrict__ probs, int
 }
 
 // dlogits = (probs - onehot(target)) / B (nn.py:204-210); nll for the loss
+// The gradient leaves scaled by gscale = 2^k (k = floor(log2 B)): |g| <= 1,
+// so fp16 GEMM operands do not underflow; every backward op is linear in g
+// and power-of-two scaling commutes with fp32 rounding, and the Adam kernels
+// multiply by 1/gscale, so the fp32 trajectory is bit-identical to unscaled.
 __global__ void k_dlogits(const float* __restrict__ probs, ByteCols src, StepIdx si, int Bl,
-                          float Bf, float* __restrict__ g, float* __restrict__ nll) {
+                          float Bf, float gscale, float* __restrict__ g, float* __restrict__ nll) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)Bl * 256) return;
   const int b = (int)(e >> 8), v = (int)(e & 255);
@@ -962,7 +1105,7 @@ __global__ void k_dlogits(const float* __restrict__ probs, ByteCols src, StepIdx
     if (nll) nll[b] = -logf(p);
     p = p - 1.0f;
   }
-  g[e] = p / Bf;
+  g[e] = (p / Bf) * gscale;
 }
 
 // --------------------------------------------------------------- coder

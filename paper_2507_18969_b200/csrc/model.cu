@@ -209,6 +209,11 @@ struct edpc_ctx {
   int64_t n = 0, L = 0;
   int g_first = 0, g_count = 0;  // local lane groups
   bool use_tc = false;
+  // fp16 GEMM path for the MBRB branch / out-projection GEMMs (see ctx_create)
+  bool h16 = false;
+  int gs_log2 = 0;                                  // gradient scale 2^gs_log2 (k_dlogits)
+  __half* Wh = nullptr;                             // fp16 shadow of the shared weights
+  __half *guph_l = nullptr, *guph_g = nullptr;      // fp16 copies of g_up per MBRB
   cudaStream_t st = nullptr, st_enc = nullptr;
   cudaStream_t st_aux = nullptr;  // weight-gradient GEMMs run here, joined before Adam
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -569,6 +574,86 @@ static cudaError_t dgrad(edpc_ctx* c, const float* G, int Kd, int nsum, int64_t 
   return gemm_simt<false, true>(g, epi, c->st);
 }
 
+// ---------------------------------------------------- fp16 GEMM path
+//
+// The MBRB branch and out-projection GEMMs (>90% of the step's FLOPs) take
+// fp16 operands (kind::f16: 2x the tf32 MMA rate, half the operand bytes):
+// x0, ff, D_z and g_H are stored as fp16 by the kernels that produce them,
+// the weights come from an fp16 shadow refreshed by Adam, g_up gets an fp16
+// copy.  fp16 has tf32's 10-bit mantissa (rounded, not truncated); range is
+// handled by the power-of-two gradient scale (k_dlogits).
+
+static cudaError_t fwd_linear_h(edpc_ctx* c, const __half* A, int Kd, const __half* w, int N,
+                                float* out, const float* bias, const float* resid) {
+  const int M = c->Bl;
+  TcOperand a{A, Kd, 0, 1}, b{w, N, 0, 1};
+  if (N <= 256 && N % 4 == 0 && Kd >= 1024 && Kd % (kSplitK * tc_bk<true>()) == 0) {
+    TcShape s{M, N, Kd, 1, 1, kBatchNone, kBatchNone, 2, kSplitK, 0, 0, 0};
+    {
+      Scope sc(c, kRegGemm, c->st);
+      int st = tc_gemm<false, true, true>(s, a, b, EpiSplit{c->ws, N, (int64_t)M * N}, c->st);
+      if (st != EDPC_OK) return cudaErrorUnknown;
+    }
+    return splitk_reduce(c, N, bias, resid, out);
+  }
+  Scope sc(c, kRegGemm, c->st);
+  TcShape s{M, N, Kd, 1, 1, kBatchNone, kBatchNone, 0, 1, 0, 0, 0};
+  if (resid)
+    return as_cuda(tc_gemm<false, true, true>(s, a, b, EpiBiasResid{out, N, bias, resid, N}, c->st));
+  return as_cuda(tc_gemm<false, true, true>(s, a, b, EpiBias{out, N, 0, bias, 0}, c->st));
+}
+
+// out[Bl][N] = sum_s G_s[Bl][Kd] . W_s^T, W_s fp16 [N][Kd]
+static cudaError_t dgrad_h(edpc_ctx* c, const __half* G, int Kd, int nsum, int64_t sG_sum,
+                           const __half* w, int64_t sW_sum, int N, float* out) {
+  TcOperand a{G, Kd, sG_sum, nsum}, b{w, Kd, sW_sum, nsum};
+  const TcBatch bt = nsum > 1 ? kBatchSum : kBatchNone;
+  if (N <= 256 && N % 4 == 0 && (int64_t)Kd * nsum >= 1024 &&
+      Kd % (kSplitK * tc_bk<true>()) == 0) {
+    TcShape s{c->Bl, N, Kd, 1, nsum, bt, bt, 2, kSplitK, 0, 0, 0};
+    {
+      Scope sc(c, kRegGemm, c->st);
+      int st = tc_gemm<false, false, true>(s, a, b, EpiSplit{c->ws, N, (int64_t)c->Bl * N}, c->st);
+      if (st != EDPC_OK) return cudaErrorUnknown;
+    }
+    return splitk_reduce(c, N, nullptr, nullptr, out);
+  }
+  Scope sc(c, kRegGemm, c->st);
+  TcShape s{c->Bl, N, Kd, 1, nsum, bt, bt, 0, 1, 0, 0, 0};
+  return as_cuda(tc_gemm<false, false, true>(s, a, b, EpiStore{out, N}, c->st));
+}
+
+// weight-gradient partials from fp16 X [lanes][Mw] and G [nzb][lanes][N]
+// (both MN-major operands: K = lanes, split into the lane groups)
+static cudaError_t wgrad_h(edpc_ctx* c, const __half* X, int Mw, const __half* G, int N, int nzb,
+                           int64_t sG, int64_t off, int64_t sOff) {
+  EpiPartial e{c->Gp, c->lay.n_shared, off, sOff, N, c->g_first};
+  cudaStream_t ws = wst(c);
+  Scope sc(c, kRegGemm, ws);
+  TcShape s{Mw, N, c->Bl, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 1,
+            c->g_count, c->g_first, c->lay.B, c->lane0};
+  TcOperand a{X, Mw, 0, 1}, b{G, N, sG, nzb};
+  return as_cuda(tc_gemm<true, true, true>(s, a, b, e, ws));
+}
+
+// bias-gradient partials (column sums per lane group) of an fp16 source
+static cudaError_t colsum_h(edpc_ctx* c, const __half* src, int N, int nz, int64_t sz,
+                            int64_t off, int64_t sOff, cudaStream_t st) {
+  if (c->g_count == 0) return cudaSuccess;
+  dim3 grid((unsigned)cdiv(N, 128), (unsigned)nz, (unsigned)c->g_count);
+  Scope sc(c, kRegColsum, st);
+  k_colsum_groups_h<<<grid, 256, 0, st>>>(src, N, sz, N, c->Gp, c->lay.n_shared, off, sOff,
+                                          c->g_first, c->lay.B, c->lane0);
+  return cudaGetLastError();
+}
+
+static cudaError_t to_half(edpc_ctx* c, const float* src, __half* dst, int64_t n, cudaStream_t st) {
+  Scope sc(c, kRegElem, st);
+  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 8);
+  k_to_half<<<blocks, 256, 0, st>>>(src, dst, n);
+  return cudaGetLastError();
+}
+
 #define CK(expr)                                                        \
   do {                                                                  \
     cudaError_t _e = (expr);                                            \
@@ -591,15 +676,33 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
   dim3 g8((unsigned)cdiv(Bl, 8));
   {
     Scope sc_ln(c, kRegElem, c->st);
+    __half* x0h = c->h16 ? reinterpret_cast<__half*>(b.x0) : nullptr;
     if (gather)
       k_embed_ln<true><<<g8, 256, 0, c->st>>>(src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
-                                              c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0);
+                                              c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0,
+                                              x0h);
     else
       k_embed_ln<false><<<g8, 256, 0, c->st>>>(src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
-                                               c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0);
+                                               c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0,
+                                               x0h);
     CK(cudaGetLastError());
   }
   const int64_t plane = (int64_t)Bl * H;
+  if (c->h16) {  // fp16 operands; x0, ff and D_z live in their buffers as fp16
+    __half* x0h = reinterpret_cast<__half*>(b.x0);
+    __half* ffh = reinterpret_cast<__half*>(b.ff);
+    __half* Dh = reinterpret_cast<__half*>(b.H);
+    {
+      Scope sc(c, kRegGemm, c->st);
+      TcShape s{Bl, H, F, 2, 1, kBatchNone, kBatchZ, 0, 1, 0, 0, 0};
+      TcOperand a{x0h, F, 0, 1}, bw{c->Wh + o.w0, H, o.wstride, 2};
+      const int st = tc_launch_zin<128, 2, true, true>(
+          s, a, bw, EpiBranchActH<2>{Dh, ffh, c->W + o.b0, o.wstride, H, plane}, c->st);
+      if (st != EDPC_OK) return st;
+    }
+    CK(fwd_linear_h(c, ffh, H, c->Wh + o.out_w, F, b.out, c->W + o.out_b, b.x));
+    return EDPC_OK;
+  }
   // branch GEMMs with the product + GeLU fused into the epilogue when all
   // branches of a tile fit one CTA's TMEM (k = 2, 3); else GEMM + k_mbrb_act
   if ((L.K == 2 || L.K == 3) && H % 128 == 0 &&
@@ -677,10 +780,33 @@ static int softmax_quant(edpc_ctx* c, int mode, ByteCols src) {
 // g_up: gradient w.r.t. the block output [Bl][F]; writes the gradient w.r.t.
 // the block input into g_in
 static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, const float* g_up,
-                         float* g_in, float* GH) {
+                         float* g_in, float* GH, __half* guph) {
   const Layout& L = c->lay;
   const int Bl = c->Bl, F = L.F, H = o.H, K = L.K;
   const int64_t plane = (int64_t)Bl * H;
+  if (c->h16) {
+    const __half* x0h = reinterpret_cast<const __half*>(b.x0);
+    const __half* ffh = reinterpret_cast<const __half*>(b.ff);
+    const __half* Dh = reinterpret_cast<const __half*>(b.H);
+    __half* GHh = reinterpret_cast<__half*>(GH);
+    CK(to_half(c, g_up, guph, (int64_t)Bl * F, c->st));
+    // g_ff = g_up . out_w^T (out_w [H][F] = K-major B), epilogue -> g_H[z]
+    {
+      Scope sc(c, kRegGemm, c->st);
+      TcShape s{Bl, H, F, 1, 1, kBatchNone, kBatchNone, 0, 1, 0, 0, 0};
+      TcOperand a{guph, F, 0, 1}, bw{c->Wh + o.out_w, F, 0, 1};
+      const int st = tc_gemm<false, false, true>(s, a, bw, EpiBwdActH{Dh, GHh, K, plane, H}, c->st);
+      if (st != EDPC_OK) return st;
+    }
+    // weight gradients (and bias sums from fp32 g_up / fp16 g_H) on the side stream
+    CK(fork_aux(c));
+    CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0));
+    CK(colsum(c, g_up, F, 1, 0, nullptr, o.out_b, 0, wst(c)));
+    CK(wgrad_h(c, x0h, F, GHh, H, K, plane, o.w0, o.wstride));
+    CK(colsum_h(c, GHh, H, K, plane, o.b0, o.wstride, wst(c)));
+    // g_x0 = sum_z g_H[z] . W_z^T (W_z [F][H] = K-major B)
+    CK(dgrad_h(c, GHh, H, K, plane, c->Wh + o.w0, o.wstride, F, c->gx0));
+  } else {
   // g_ff = g_up . out_w^T, epilogue -> GH[z] (product rule + GeLU')
   CK(dgrad(c, g_up, F, 1, 0, c->W + o.out_w, 0, H, EpiBwdAct{b.H, GH, K, plane, H}));
   // weight gradients on the side stream: out_w/out_b, branch weights/biases
@@ -689,6 +815,7 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
   CK(wgrad(c, b.x0, F, GH, H, K, plane, o.w0, o.wstride, o.b0));
   // g_x0 = sum_z GH[z] . W_z^T
   CK(dgrad(c, GH, H, K, plane, c->W + o.w0, o.wstride, F, EpiStore{c->gx0, F}));
+  }
   // LN backward + residual, with the LN gain / bias gradient partials
   if (F <= kLnMaxF && c->g_count > 0) {
     int maxg = 0;
@@ -717,7 +844,7 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   {
     Scope sc_(c, kRegElem, c->st);
     k_dlogits<<<(unsigned)cdiv((int64_t)Bl * 256, 256), 256, 0, c->st>>>(
-        c->probs, src, c->si(), Bl, (float)L.B, c->gl, nll);
+        c->probs, src, c->si(), Bl, (float)L.B, ldexpf(1.0f, c->gs_log2), c->gl, nll);
   }
   CK(cudaGetLastError());
   // head
@@ -726,7 +853,7 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   CK(dgrad(c, c->gl, 256, 1, 0, c->W + L.head_w, 0, F, EpiStore{c->g_head, F}));
   // global MBRB: d(x_global) -> d(x_lte)
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
-  EDPC_TRY(mbrb_backward(c, L.glo, gb, c->g_head, c->g_lte, c->GH_g));
+  EDPC_TRY(mbrb_backward(c, L.glo, gb, c->g_head, c->g_lte, c->GH_g, c->guph_g));
   // LTE up
   CK(fork_aux(c));
   CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
@@ -739,7 +866,8 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
       auto run = [&](auto kern, cudaStream_t st) {
         Scope sc_(c, kRegFdmBwd, st);
         kern<<<blocks, 256, 0, st>>>(c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, Bl, c->si(),
-                                     c->adam, c->cfg.beta1, c->cfg.beta2);
+                                     c->adam, c->cfg.beta1, c->cfg.beta2,
+                                     ldexpf(1.0f, -c->gs_log2));
       };
       // split measured 1% slower at C2: the persistent GEMMs own whole SMs,
       // so the side-stream Adam pass barely overlaps and U is read twice
@@ -773,7 +901,7 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
       Scope sc_(c, kRegFdmBwd, c->st);
       k_fdm_bwd_adam<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(
           c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, FP, Bl, c->si(), c->adam,
-          c->cfg.beta1, c->cfg.beta2);
+          c->cfg.beta1, c->cfg.beta2, ldexpf(1.0f, -c->gs_log2));
     }
   }
   CK(cudaGetLastError());
@@ -783,7 +911,7 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore{c->g_loc, F}));
   // local MBRB: d(x_local) -> d(x_emb) (gradient w.r.t. the embedded context)
   MbrbBufs lb{c->x_emb, c->l_xhat, c->l_rstd, c->l_x0, c->l_H, c->l_ff, c->x_local};
-  EDPC_TRY(mbrb_backward(c, L.loc, lb, c->g_loc, c->g_emb, c->GH_l));
+  EDPC_TRY(mbrb_backward(c, L.loc, lb, c->g_loc, c->g_emb, c->GH_l, c->guph_l));
   // embedding scatter-add as per-group partials
   if (c->n_chunks > 0) {
     {
@@ -809,7 +937,8 @@ static int adam_shared(edpc_ctx* c) {
   {
     Scope sc_(c, kRegAdam, c->st);
     k_adam_shared<<<blocks, 256, 0, c->st>>>(c->W, c->M, c->V, c->Gp, c->lay.n_shared, c->si(),
-                                             c->adam, c->cfg.beta1, c->cfg.beta2);
+                                             c->adam, c->cfg.beta1, c->cfg.beta2,
+                                             ldexpf(1.0f, -c->gs_log2), c->h16 ? c->Wh : nullptr);
   }
   CK(cudaGetLastError());
   return EDPC_OK;
@@ -993,6 +1122,20 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
     else
       c->use_tc = tc_compiled() && cfg->lanes >= kTf32MinLanes;
   }
+  // fp16 operands for the MBRB GEMMs (part of the same numerics policy):
+  // on the tensor-core path whenever the shapes tile (k = 2, F and the lane
+  // groups multiples of 64 for the fp16 k-blocks, H multiple of 128).
+  // EDPC_F16=0 keeps them tf32 (debugging / A-B runs).
+  {
+    const Layout& L = c->lay;
+    const char* e = getenv("EDPC_F16");
+    const int glanes = L.B / kNumGroups;
+    c->h16 = !(e && e[0] == '0') && c->use_tc && L.K == 2 && L.F % 64 == 0 &&
+             L.HL % 128 == 0 && L.HG % 128 == 0 && L.B % kNumGroups == 0 && glanes % 64 == 0;
+    int k = 0;
+    while ((2 << k) <= L.B) ++k;  // 2^k <= B < 2^(k+1)
+    c->gs_log2 = k;
+  }
 
   auto fail = [&](int code) {
     delete c;
@@ -1052,6 +1195,11 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
   A_(c->g_emb, Bl * F);
   A_(c->GH_g, (int64_t)L.K * Bl * L.HG);
   A_(c->GH_l, (int64_t)L.K * Bl * L.HL);
+  if (c->h16) {
+    A_(c->Wh, L.n_shared);
+    A_(c->guph_l, Bl * F);
+    A_(c->guph_g, Bl * F);
+  }
   A_(c->gx0, Bl * F);
   A_(c->gmix, Bl * FP);
   A_(c->gdown, Bl * FP);
@@ -1134,6 +1282,12 @@ int edpc_ctx_destroy(edpc_ctx* ctx) {
   return EDPC_OK;
 }
 
+int edpc_ctx_numerics(edpc_ctx* c, int32_t* flags) {
+  EDPC_CHECK_ARG(c && flags, "null argument");
+  *flags = (c->use_tc ? 1 : 0) | (c->h16 ? 2 : 0);
+  return EDPC_OK;
+}
+
 int edpc_ctx_info(edpc_ctx* c, int64_t* lane_len, int64_t* n_params, int64_t* n_shared) {
   EDPC_CHECK_ARG(c, "null ctx");
   if (lane_len) *lane_len = c->L;
@@ -1154,6 +1308,12 @@ int edpc_load_params(edpc_ctx* c, const float* params, int64_t count) {
                            (L.n_shared - L.ref_lane_mats) * 4, cudaMemcpyHostToDevice));
   EDPC_CUDA_TRY(cudaMemcpy(c->U, params + L.ref_lane_mats + (int64_t)c->lane0 * L.fdm,
                            (int64_t)c->Bl * L.fdm * 4, cudaMemcpyHostToDevice));
+  if (c->h16) {  // the fp16 weight shadow starts from the loaded weights
+    k_to_half<<<(unsigned)std::min<int64_t>(cdiv(L.n_shared, 256), 148 * 8), 256, 0, c->st>>>(
+        c->W, c->Wh, L.n_shared);
+    EDPC_CUDA_TRY(cudaGetLastError());
+    EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  }
   return EDPC_OK;
 }
 
@@ -1779,7 +1939,17 @@ int edpc_debug_read(edpc_ctx* c, int32_t which, float* out, int64_t count) {
     default: EDPC_CHECK_ARG(false, "unknown debug buffer");
   }
   EDPC_CHECK_ARG(count == n, "debug buffer size mismatch (expected " + std::to_string(n) + ")");
+  if (c->h16 && (which == 5 || which == 6)) {  // D_z stored as fp16 on that path
+    std::vector<__half> h((size_t)n);
+    EDPC_CUDA_TRY(cudaMemcpy(h.data(), src, n * 2, cudaMemcpyDeviceToHost));
+    for (int64_t e = 0; e < n; ++e) out[e] = __half2float(h[(size_t)e]);
+    return EDPC_OK;
+  }
   EDPC_CUDA_TRY(cudaMemcpy(out, src, n * 4, cudaMemcpyDeviceToHost));
+  if (which == 0) {  // partials are kept in gradient-scale units (k_dlogits)
+    const float inv = ldexpf(1.0f, -c->gs_log2);
+    for (int64_t e = 0; e < n; ++e) out[e] *= inv;
+  }
   return EDPC_OK;
 }
 

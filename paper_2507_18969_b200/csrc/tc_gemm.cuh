@@ -290,6 +290,22 @@ struct EpiTsSlots<Epi, std::void_t<decltype(Epi::kTsSlots)>> {
   static constexpr int value = Epi::kTsSlots;
 };
 template <class Epi, class = void>
+struct EpiTsInBytes {
+  static constexpr int value = 32 * 32 * 4;
+};
+template <class Epi>
+struct EpiTsInBytes<Epi, std::void_t<decltype(Epi::kTsInBytes)>> {
+  static constexpr int value = Epi::kTsInBytes;
+};
+template <class Epi, class = void>
+struct EpiRequireTs {
+  static constexpr bool value = false;
+};
+template <class Epi>
+struct EpiRequireTs<Epi, std::void_t<decltype(Epi::kRequireTs)>> {
+  static constexpr bool value = Epi::kRequireTs;
+};
+template <class Epi, class = void>
 struct EpiTsIn {
   static constexpr int value = 0;
 };
@@ -353,6 +369,53 @@ struct TsIo {
       tma_store_4d(maps[map], slots + slot * 1024, n0, m0, c2, c3);  // rows past M are clipped
       bulk_commit();
     }
+  }
+  // fp16 boxes: rows of 64 B (32 halves), SWIZZLE_64B: 16-byte chunk j of
+  // row r at j ^ ((r >> 1) & 3) -- conflict-free for 8 rows per phase
+  __device__ __forceinline__ void write_row_h(int slot, const float (&v)[32]) const {
+    const int lane = threadIdx.x & 31;
+    uint8_t* row = reinterpret_cast<uint8_t*>(slots + slot * 1024) + lane * 64;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint4 q;
+      __half2 h0 = __floats2half2_rn(v[8 * j], v[8 * j + 1]);
+      __half2 h1 = __floats2half2_rn(v[8 * j + 2], v[8 * j + 3]);
+      __half2 h2 = __floats2half2_rn(v[8 * j + 4], v[8 * j + 5]);
+      __half2 h3 = __floats2half2_rn(v[8 * j + 6], v[8 * j + 7]);
+      q.x = *reinterpret_cast<uint32_t*>(&h0);
+      q.y = *reinterpret_cast<uint32_t*>(&h1);
+      q.z = *reinterpret_cast<uint32_t*>(&h2);
+      q.w = *reinterpret_cast<uint32_t*>(&h3);
+      *reinterpret_cast<uint4*>(row + ((j ^ ((lane >> 1) & 3)) << 4)) = q;
+    }
+  }
+  __device__ __forceinline__ void in_h(int slot, float (&v)[32]) const {
+    const int lane = threadIdx.x & 31;
+    const uint8_t* row = reinterpret_cast<const uint8_t*>(slots + (ib + slot) * 1024) + lane * 64;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const uint4 q = *reinterpret_cast<const uint4*>(row + ((j ^ ((lane >> 1) & 3)) << 4));
+      const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w[u]));
+        v[8 * j + 2 * u] = f.x;
+        v[8 * j + 2 * u + 1] = f.y;
+      }
+    }
+  }
+  __device__ __forceinline__ void put_h(int map, const float (&v)[32], int c2, int c3) {
+    const int slot = *next;
+    *next = slot + 1 == NS ? 0 : slot + 1;
+    if ((threadIdx.x & 31) == 0) bulk_wait_read<NS - 1>();
+    __syncwarp();
+    write_row_h(slot, v);
+    issue(slot, map, c2, c3);
+  }
+  __device__ __forceinline__ void put_at_h(int slot, int map, const float (&v)[32], int c2,
+                                           int c3) {
+    write_row_h(ib + slot, v);
+    issue(ib + slot, map, c2, c3);
   }
   // store v (this thread's row) to map at (n0, m0, c2, c3) through the ring
   __device__ __forceinline__ void put(int map, const float (&v)[32], int c2, int c3) {
@@ -622,7 +685,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
         int tn, tm, zb, zg, kb0, nkb;
         tile_coords(tq, tn, tm, zb, zg, kb0, nkb);
         uint64_t* bar = &wbar[(warp - 2) * 2 + pair];
-        mbar_expect_tx(bar, kTsIn * kTsBoxBytes);
+        mbar_expect_tx(bar, kTsIn * EpiTsInBytes<Epi>::value);
 #pragma unroll
         for (int i = 0; i < kTsIn; ++i) {
           int c2, c3;
@@ -868,34 +931,36 @@ inline int make_tmap(CUtensorMap* map, const void* base, uint64_t inner, uint64_
 // and of every stride); the kernel then stores with row32.
 inline bool make_store_tmap(CUtensorMap* map, const TcStoreMap& d) {
   if (((uintptr_t)d.base & 15) != 0 || d.dims[0] < 32) return false;
+  const uint64_t es = d.half ? 2 : 4;
   cuuint64_t dims[4] = {d.dims[0], d.dims[1], d.dims[2] ? d.dims[2] : 1, d.dims[3] ? d.dims[3] : 1};
   cuuint64_t strides[3];
   uint64_t prev = d.dims[0];
   for (int i = 0; i < 3; ++i) {
     uint64_t st = d.strides[i];
     if (dims[i + 1] == 1 || st == 0) st = prev;  // unused dimension: any valid stride
-    if ((st * 4) % 16 != 0 || st * 4 >= (1ull << 40)) return false;
-    strides[i] = st * 4;
+    if ((st * es) % 16 != 0 || st * es >= (1ull << 40)) return false;
+    strides[i] = st * es;
     prev = st * dims[i + 1];
   }
   cuuint32_t box[4] = {32, 32, 1, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   PfnEncodeTiled enc = encode_tiled_fn();
   if (!enc) return false;
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void*)d.base, dims, strides, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  return enc(map, d.half ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+             (void*)d.base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             d.half ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 struct StoreTmapCache {
   std::mutex mu;
   std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t, uint64_t,
-                      uint64_t>,
+                      uint64_t, int>,
            std::pair<bool, CUtensorMap>>
       maps;
   bool get(CUtensorMap* out, const TcStoreMap& d) {
     auto key = std::make_tuple((const void*)d.base, d.dims[0], d.dims[1], d.dims[2], d.dims[3],
-                               d.strides[0], d.strides[1], d.strides[2]);
+                               d.strides[0], d.strides[1], d.strides[2], d.half);
     std::lock_guard<std::mutex> g(mu);
     auto it = maps.find(key);
     if (it == maps.end()) {
@@ -1050,6 +1115,10 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
   CUtensorMap ta, tb, tc{}, td{};
   TcShape s2 = s;
   if constexpr (kTS) s2.ts = ts_maps(epi, s, tc, td);
+  if (EpiRequireTs<Epi>::value && !s2.ts) {
+    set_error("tc_gemm: epilogue output not addressable by TMA (alignment)");
+    return EDPC_ERR_INVALID;
+  }
   int r;
   r = tc_operand_maps<BN, AMN, BMN, H>(s, A, B, cl, ta, tb);
   if (r != EDPC_OK) return r;
@@ -1116,6 +1185,10 @@ inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& 
   CUtensorMap tc{}, td{};
   TcShape s2 = s;
   if constexpr (kTS) s2.ts = ts_maps(epi, s, tc, td);
+  if (EpiRequireTs<Epi>::value && !s2.ts) {
+    set_error("tc_gemm: epilogue output not addressable by TMA (alignment)");
+    return EDPC_ERR_INVALID;
+  }
   const int units = (s.N / BN) * (n_tm / cl);
   const int max_units = num_sms() / cl;
   const int grid = (units < max_units ? units : max_units) * cl;

@@ -29,9 +29,10 @@ struct TcShape {
 
 // Output of a TMA-store epilogue as a 4D fp32 tensor: (n, m, c2, c3).
 struct TcStoreMap {
-  const float* base;
+  const void* base;
   uint64_t dims[4];     // n (inner), m, c2, c3
   uint64_t strides[3];  // elements, of m, c2, c3
+  int half = 0;         // fp16 elements (64B-swizzled 32x32 boxes) instead of fp32
 };
 
 }  // namespace edpc

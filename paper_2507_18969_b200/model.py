@@ -68,6 +68,13 @@ class DeviceContext:
         _lib.check(_lib.load().edpc_get_params(self.h, out.ctypes.data, out.size))
         return out
 
+    def numerics(self) -> dict:
+        """GEMM numerics of this context (fixed by the config): tensor cores
+        (tf32) and fp16 operands for the MBRB branch / out-projection GEMMs."""
+        f = ctypes.c_int32()
+        _lib.check(_lib.load().edpc_ctx_numerics(self.h, ctypes.byref(f)))
+        return {"tcgen05": bool(f.value & 1), "fp16_mbrb": bool(f.value & 2)}
+
     def state_checksum(self) -> str:
         """sha256 over the fp32 parameter bytes (the lockstep probe, `model.py:294-300`)."""
         return hashlib.sha256(self.params_flat().tobytes()).hexdigest()

@@ -19,12 +19,14 @@ pytestmark = pytest.mark.gpu
 REL = 5e-3
 
 
-def _ctx(cfg, tc: bool):
+def _ctx(cfg, tc: bool, f16: bool = False):
     os.environ["EDPC_TCGEN05"] = "1" if tc else "0"
+    os.environ["EDPC_F16"] = "1" if f16 else "0"
     try:
         c = DeviceContext(cfg, 4, 0, 0)
     finally:
         os.environ.pop("EDPC_TCGEN05", None)
+        os.environ.pop("EDPC_F16", None)
     c.load_flat(init_params_f32(cfg))
     return c
 
@@ -44,8 +46,27 @@ def test_tcgen05_matches_simt(lanes, extra):
     if not _lib.load().edpc_has_tcgen05():
         pytest.skip("tcgen05 path not compiled")
     cfg = ModelConfig(**dict(PAPER, **extra), lanes=lanes)
+    _compare(cfg, _ctx(cfg, True), _ctx(cfg, False))
+
+
+@pytest.mark.parametrize("ref", ["fp32", "tf32"])
+def test_f16_matches(ref):
+    """fp16-operand MBRB GEMMs (1024 lanes: lane groups of 128) against the
+    fp32 SIMT path and against the tf32 tensor-core path, same tolerances as
+    tf32 vs fp32 (fp16 keeps tf32's 10-bit mantissa)."""
+    if not _lib.load().edpc_has_tcgen05():
+        pytest.skip("tcgen05 path not compiled")
+    cfg = ModelConfig(**PAPER, lanes=1024)
+    a = _ctx(cfg, True, f16=True)
+    b = _ctx(cfg, ref == "tf32", f16=False)
+    assert a.numerics() == {"tcgen05": True, "fp16_mbrb": True}
+    assert b.numerics() == {"tcgen05": ref == "tf32", "fp16_mbrb": False}
+    _compare(cfg, a, b)
+
+
+def _compare(cfg, a, b):
+    lanes = cfg.lanes
     lib = _lib.load()
-    a, b = _ctx(cfg, True), _ctx(cfg, False)
     rng = np.random.default_rng(0)
     F, T = cfg.feature_dim, cfg.context_len
     sizes = {1: lanes * 256, 2: lanes * F, 3: lanes * F, 4: lanes * F,
