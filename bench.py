@@ -24,7 +24,12 @@ of predict -> quantize -> encode -> backward -> Adam.
                 (tests/golden/ref_ratio_c2mini_text_4m.json).
 * ``roofline``  dominant kernel class (the per-step GEMMs): algorithmic
                 FLOPs (6*(kF h_l + h_l F + 2F F' + kF h_g + h_g F
-                + 256F) per lane-step) / CUDA-event time of those launches.
+                + 256F) per lane-step) / CUDA-event time of those launches,
+                against the FLOP-weighted peak of the numerics the context
+                runs (kind::f16 MBRB GEMMs at the measured dense bf16/fp16
+                rate, kind::tf32 LTE/head GEMMs at half of it); ``traffic`` is
+                the GEMMs' DRAM bytes per model step from the committed ncu
+                capture (profiles/r01_gemm_traffic.json).
 * ``cpu_baseline`` the CPU oracle (numpy fp64 + C coder, restating the
                 reference) step-sampled at the same B and dims on this host.
 
@@ -240,6 +245,7 @@ def run_ours(args, wl):
     # ---- compress (device-resident input)
     ctx = DeviceContext(cfg, S, n, 0)
     ctx.load_flat(params)
+    numerics = ctx.numerics()
     _lib.check(lib.edpc_set_input(ctx.h, buf.ctypes.data, n, 0))
     col = 0
     _lib.check(lib.edpc_compress_steps(ctx.h, 0, T))
@@ -340,12 +346,28 @@ def run_ours(args, wl):
         cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     pk, pk_src = peaks()
-    tc = bool(lib.edpc_has_tcgen05()) and os.environ.get("EDPC_TCGEN05", "1") != "0"
+    tc, f16 = numerics["tcgen05"], numerics["fp16_mbrb"]
     fl_step = gemm_flops_per_lane(wl["model"]) * B  # per model step (lane column)
     steps_total = KP * chunk  # model steps in the profiled pass
     g_ms, g_n = c_regions["gemm"]
     achieved = fl_step * steps_total / (g_ms / 1e3) / 1e12 if g_ms > 0 else 0.0
-    peak_t = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))
+    peak_16 = pk.get("bf16_tflops_sustained", pk.get("bf16_tflops"))  # dense fp16 = bf16 rate
+    # mixed peak: the MBRB GEMMs run kind::f16 (fp16 operands), the LTE / head
+    # GEMMs kind::tf32 at half that rate -> t_min = sum_phase FLOP / peak
+    fl_tf32 = gemm_flops_per_lane(dict(wl["model"], hidden_local=0, hidden_global=0)) * B
+    if f16:
+        peak_t = fl_step / ((fl_step - fl_tf32) / peak_16 + fl_tf32 / (peak_16 / 2))
+        gemm_kind = "tcgen05 kind::f16 (MBRB branch/out-proj) + kind::tf32 (LTE, head)"
+        dtype = "fp16+tf32"
+    elif tc:
+        peak_t, gemm_kind, dtype = peak_16 / 2, "tcgen05 kind::tf32", "tf32"
+    else:
+        peak_t, gemm_kind, dtype = peak_16 / 2, "SIMT fp32", "fp32"
+    traffic, traffic_src = None, None
+    tp = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp))
+        traffic, traffic_src = tj["gemm_dram_bytes_per_step"], tj.get("source", tp)
     m = wl["model"]
     F = m["context_len"] * m["embed_dim"]
     Fp = F // m["lte_ratio"]
@@ -362,7 +384,7 @@ def run_ours(args, wl):
     line = dict(
         metric=METRIC, value=B * chunk * K / (c_ms / 1e3) / 1e6, unit="MB/s", n_gpus=1,
         steps=K, warmup=W, ms_per_step=c_ms / K, higher_is_better=True, scaling="weak",
-        vs_baseline=None, dtype="tf32" if tc else "fp32", data=f"synthetic {wl['kind']}-like (PCG64 seed {wl['seed']},"
+        vs_baseline=None, dtype=dtype, data=f"synthetic {wl['kind']}-like (PCG64 seed {wl['seed']},"
                                               f" sha256 {synth.sha256(data)[:16]})",
         config=dict(workload=wl["desc"], lanes=B, segments=S, columns_per_step=chunk,
                     bytes_per_step=B * chunk, model=wl["model"],
@@ -370,17 +392,20 @@ def run_ours(args, wl):
         decompress_MBps=B * chunk * K / (d_ms / 1e3) / 1e6, lossless_region=lossless,
         region_bits_per_byte=region_bpb, **ratio,
         roofline=dict(bound="tensor",
-                      kernel="per-step GEMMs (" + ("tcgen05 kind::tf32" if tc else "SIMT fp32") + ")",
+                      kernel=f"per-step GEMMs ({gemm_kind})",
                       achieved=achieved,
-                      peak=peak_t, unit="TFLOP/s", frac=achieved / peak_t, traffic=None,
-                      peak_source=f"{pk_src} bf16 dense sustained",
-                      flops_per_step=fl_step),
+                      peak=peak_t, unit="TFLOP/s", frac=achieved / peak_t, traffic=traffic,
+                      peak_source=f"{pk_src} bf16 dense sustained ({peak_16} TFLOP/s) = fp16 rate;"
+                                  f" tf32 at half; weighted by the FLOP mix",
+                      traffic_unit="DRAM bytes per model step, all GEMM launches",
+                      traffic_source=traffic_src, frac_vs_fp16_peak=achieved / peak_16,
+                      flops_per_step=fl_step, gemm_ms_per_model_step=g_ms / steps_total),
         kernels=kernels, kernels_note=f"per-region CUDA events over {KP} extra eager bench steps "
                                       f"({steps_total} model steps); eager ms/step {p_ms / KP:.2f} vs "
                                       f"graph ms/step {c_ms / K:.2f}",
         decode_kernels={k: dict(ms_per_step=v[0] / steps_total) for k, v in d_regions.items() if v[0]},
         cpu_baseline=cpu, e2e=e2e, gpu_launches=int(launches * K // KP),
-        clocks=clocks, tcgen05=tc)
+        clocks=clocks, numerics=numerics)
     print(json.dumps(line), flush=True)
 
 

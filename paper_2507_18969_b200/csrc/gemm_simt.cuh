@@ -273,6 +273,39 @@ struct EpiStore {
   }
 };
 
+// plain store plus an fp16 copy (the gradient entering an MBRB: fp32 for the
+// LN backward's residual, fp16 as an operand of the fp16 GEMMs)
+struct EpiStore2 {
+  static constexpr bool kTmaStore = true;
+  static constexpr int kTsSlots = 2;
+  float* C;
+  __half* Ch;
+  int64_t ldc;
+  bool store_maps(const TcShape& s, TcStoreMap& c, TcStoreMap& d) const {
+    c = TcStoreMap{C, {(uint64_t)s.N, (uint64_t)s.M, 1, 1}, {(uint64_t)ldc, 0, 0}};
+    d = TcStoreMap{Ch, {(uint64_t)s.N, (uint64_t)s.M, 1, 1}, {(uint64_t)ldc, 0, 0}, 1};
+    return true;
+  }
+  template <class IO>
+  __device__ void ts_chunk(IO& io, int, int, int, int, float (&v)[1][32]) const {
+    io.put(0, v[0], 0, 0);
+    io.put_h(1, v[0], 0, 0);
+  }
+  __device__ void operator()(int, int, int m, int n, float acc) const {
+    C[(int64_t)m * ldc + n] = acc;
+    Ch[(int64_t)m * ldc + n] = __float2half_rn(acc);
+  }
+  __device__ void row32(int, int, int m, int n0, float (&v)[32]) const {
+    store32(C + (int64_t)m * ldc + n0, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) Ch[(int64_t)m * ldc + n0 + j] = __float2half_rn(v[j]);
+  }
+  __device__ void tile(const float* T, int, int, int m_base, int n0, int M) const {
+    const int n = n0 + (threadIdx.x & 31);
+    EDPC_TILE_ROWS(C[(int64_t)m * ldc + n] = acc; Ch[(int64_t)m * ldc + n] = __float2half_rn(acc);)
+  }
+};
+
 // weight-gradient partial of lane group (g0 + zg) at param offset (+ zb*sOff)
 struct EpiPartial {
   static constexpr bool kTmaStore = true;

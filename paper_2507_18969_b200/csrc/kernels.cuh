@@ -953,47 +953,6 @@ __global__ void k_to_half(const float* __restrict__ src, __half* __restrict__ ds
     dst[e] = __float2half_rn(src[e]);
 }
 
-// k_colsum_groups over an fp16 source (the fp16 branch-output gradients):
-// per lane group, column sums in fp32, same fixed order (warp-strided lanes,
-// then the 8 warps in order).  4 columns per thread.
-__global__ void __launch_bounds__(256)
-k_colsum_groups_h(const __half* __restrict__ src, int64_t ld, int64_t sz, int N,
-                  float* __restrict__ partials, int64_t n_shared, int64_t off, int64_t sOff,
-                  int g0, int B_global, int lane0) {
-  __shared__ float4 red[8][32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n = blockIdx.x * 128 + lane * 4;
-  const int z = blockIdx.y;
-  const int gg = g0 + blockIdx.z;
-  const int b0 = group_begin(gg, B_global) - lane0, b1 = group_begin(gg + 1, B_global) - lane0;
-  const __half* s = src + z * sz;
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  if (n < N) {
-#pragma unroll 4
-    for (int b = b0 + warp; b < b1; b += 8) {
-      const uint2 q = *reinterpret_cast<const uint2*>(s + (int64_t)b * ld + n);
-      const float2 lo = __half22float2(*reinterpret_cast<const __half2*>(&q.x));
-      const float2 hi = __half22float2(*reinterpret_cast<const __half2*>(&q.y));
-      acc.x += lo.x; acc.y += lo.y; acc.z += hi.x; acc.w += hi.y;
-    }
-  }
-  red[warp][lane] = acc;
-  __syncthreads();
-  if (warp == 0 && n < N) {
-    float4 t = red[0][lane];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) {
-      const float4 u = red[w][lane];
-      t.x += u.x; t.y += u.y; t.z += u.z; t.w += u.w;
-    }
-    float* dst = partials + (int64_t)gg * n_shared + off + z * sOff + n;
-    dst[0] = t.x;
-    dst[1] = t.y;
-    dst[2] = t.z;
-    dst[3] = t.w;
-  }
-}
-
 // ------------------------------------------------------- Adam (shared)
 
 // grad = ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)) -- the canonical G-invariant

@@ -625,34 +625,25 @@ static cudaError_t dgrad_h(edpc_ctx* c, const __half* G, int Kd, int nsum, int64
 
 // weight-gradient partials from fp16 X [lanes][Mw] and G [nzb][lanes][N]
 // (both MN-major operands: K = lanes, split into the lane groups)
+// and (bias_off >= 0) the bias partials = column sums of G over the group's
+// lanes, by the GEMM's bias warps from its own fp16 B tiles in shared memory
 static cudaError_t wgrad_h(edpc_ctx* c, const __half* X, int Mw, const __half* G, int N, int nzb,
-                           int64_t sG, int64_t off, int64_t sOff) {
+                           int64_t sG, int64_t off, int64_t sOff, int64_t bias_off) {
   EpiPartial e{c->Gp, c->lay.n_shared, off, sOff, N, c->g_first};
   cudaStream_t ws = wst(c);
   Scope sc(c, kRegGemm, ws);
   TcShape s{Mw, N, c->Bl, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 1,
             c->g_count, c->g_first, c->lay.B, c->lane0};
+  if (bias_off >= 0) {
+    s.bias_part = c->Gp;
+    s.bias_gstride = c->lay.n_shared;
+    s.bias_off = bias_off;
+    s.bias_zstride = sOff;
+  }
   TcOperand a{X, Mw, 0, 1}, b{G, N, sG, nzb};
   return as_cuda(tc_gemm<true, true, true>(s, a, b, e, ws));
 }
 
-// bias-gradient partials (column sums per lane group) of an fp16 source
-static cudaError_t colsum_h(edpc_ctx* c, const __half* src, int N, int nz, int64_t sz,
-                            int64_t off, int64_t sOff, cudaStream_t st) {
-  if (c->g_count == 0) return cudaSuccess;
-  dim3 grid((unsigned)cdiv(N, 128), (unsigned)nz, (unsigned)c->g_count);
-  Scope sc(c, kRegColsum, st);
-  k_colsum_groups_h<<<grid, 256, 0, st>>>(src, N, sz, N, c->Gp, c->lay.n_shared, off, sOff,
-                                          c->g_first, c->lay.B, c->lane0);
-  return cudaGetLastError();
-}
-
-static cudaError_t to_half(edpc_ctx* c, const float* src, __half* dst, int64_t n, cudaStream_t st) {
-  Scope sc(c, kRegElem, st);
-  const unsigned blocks = (unsigned)std::min<int64_t>(cdiv(n, 256), 148 * 8);
-  k_to_half<<<blocks, 256, 0, st>>>(src, dst, n);
-  return cudaGetLastError();
-}
 
 #define CK(expr)                                                        \
   do {                                                                  \
@@ -789,7 +780,7 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
     const __half* ffh = reinterpret_cast<const __half*>(b.ff);
     const __half* Dh = reinterpret_cast<const __half*>(b.H);
     __half* GHh = reinterpret_cast<__half*>(GH);
-    CK(to_half(c, g_up, guph, (int64_t)Bl * F, c->st));
+    // guph: the fp16 copy of g_up, written by the dgrad that produced g_up (EpiStore2)
     // g_ff = g_up . out_w^T (out_w [H][F] = K-major B), epilogue -> g_H[z]
     {
       Scope sc(c, kRegGemm, c->st);
@@ -800,10 +791,8 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
     }
     // weight gradients (and bias sums from fp32 g_up / fp16 g_H) on the side stream
     CK(fork_aux(c));
-    CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0));
-    CK(colsum(c, g_up, F, 1, 0, nullptr, o.out_b, 0, wst(c)));
-    CK(wgrad_h(c, x0h, F, GHh, H, K, plane, o.w0, o.wstride));
-    CK(colsum_h(c, GHh, H, K, plane, o.b0, o.wstride, wst(c)));
+    CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0, o.out_b));
+    CK(wgrad_h(c, x0h, F, GHh, H, K, plane, o.w0, o.wstride, o.b0));
     // g_x0 = sum_z g_H[z] . W_z^T (W_z [F][H] = K-major B)
     CK(dgrad_h(c, GHh, H, K, plane, c->Wh + o.w0, o.wstride, F, c->gx0));
   } else {
@@ -850,7 +839,10 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   // head
   CK(fork_aux(c));
   CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0, L.head_b));
-  CK(dgrad(c, c->gl, 256, 1, 0, c->W + L.head_w, 0, F, EpiStore{c->g_head, F}));
+  if (c->h16)
+    CK(dgrad(c, c->gl, 256, 1, 0, c->W + L.head_w, 0, F, EpiStore2{c->g_head, c->guph_g, F}));
+  else
+    CK(dgrad(c, c->gl, 256, 1, 0, c->W + L.head_w, 0, F, EpiStore{c->g_head, F}));
   // global MBRB: d(x_global) -> d(x_lte)
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
   EDPC_TRY(mbrb_backward(c, L.glo, gb, c->g_head, c->g_lte, c->GH_g, c->guph_g));
@@ -908,7 +900,10 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   // LTE down
   CK(fork_aux(c));
   CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
-  CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore{c->g_loc, F}));
+  if (c->h16)
+    CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore2{c->g_loc, c->guph_l, F}));
+  else
+    CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore{c->g_loc, F}));
   // local MBRB: d(x_local) -> d(x_emb) (gradient w.r.t. the embedded context)
   MbrbBufs lb{c->x_emb, c->l_xhat, c->l_rstd, c->l_x0, c->l_H, c->l_ff, c->x_local};
   EDPC_TRY(mbrb_backward(c, L.loc, lb, c->g_loc, c->g_emb, c->GH_l, c->guph_l));

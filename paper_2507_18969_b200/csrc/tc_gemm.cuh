@@ -475,7 +475,6 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
           const __grid_constant__ CUtensorMap tma_c, const __grid_constant__ CUtensorMap tma_d,
           TcShape s, Epi epi) {
   static_assert(!BIAS || BMN, "fused bias sums read an MN-major B tile");
-  static_assert(!BIAS || !H, "fused bias sums read fp32 B tiles");
   static_assert(!H || !BMN || BN % 64 == 0, "fp16 MN-major B boxes are 64 wide");
   constexpr int BK = tc_bk<H>();
   static_assert(ZIN == 1 || !BIAS, "multi-branch tiles have no fused bias");
@@ -816,15 +815,20 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   } else if (BIAS) {
     // ---------------- bias warps: column sums of B over this tile's K range
     const int bt = threadIdx.x - 32 * (2 + kTcEpiWarps);  // 0..127
-    constexpr int kCols = BN / (32 * kTcBiasWarps) > 0 ? BN / (32 * kTcBiasWarps) : 1;
+    // columns per thread (fp16: column pairs)
+    constexpr int kCols = (H ? BN / 2 : BN) / (32 * kTcBiasWarps) > 0
+                              ? (H ? BN / 2 : BN) / (32 * kTcBiasWarps)
+                              : 1;
+    auto bias_col = [&](int j) { return H ? 2 * (bt + j * 32 * kTcBiasWarps)
+                                          : bt + j * 32 * kTcBiasWarps; };
     int it = 0;
     for (int t = u0; t < n_tiles; t += ustride) {
       int tn, tm, zb, zg, kb0, nkb;
       tile_coords(t, tn, tm, zb, zg, kb0, nkb);
       const bool do_sum = tm == 0 && s.bias_part != nullptr;
-      float sum[kCols];
+      float sum[kCols], sum2[kCols];  // sum2: second column of an fp16 pair
 #pragma unroll
-      for (int j = 0; j < kCols; ++j) sum[j] = 0.f;
+      for (int j = 0; j < kCols; ++j) sum[j] = sum2[j] = 0.f;
       const int nq = nkb * s.nsum;
       for (int q = 0; q < nq; ++q, ++it) {
         const int st = it % kStages;
@@ -834,13 +838,31 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
           const uint8_t* sb = smem + st * SM::kStageBytes + SM::kABytes;
 #pragma unroll
           for (int j = 0; j < kCols; ++j) {
-            const int n = bt + j * 32 * kTcBiasWarps;
+            const int n = bias_col(j);
             if (n < BN) {
-              const int box = n >> 5, nn = n & 31, chunk = nn >> 3;
-              const float* base = reinterpret_cast<const float*>(sb + box * 4096) + (nn & 7);
+              if constexpr (H) {
+                // fp16 MN-major: 64-wide boxes of 64 K-rows, 16-byte chunk c of
+                // row k at c ^ (k & 7) (SWIZZLE_128B); this thread's column
+                // pair (n, n + 1) is one half2 per row
+                const int box = n >> 6, nn = n & 63, chunk = nn >> 3;
+                const uint8_t* base = sb + box * 8192 + (nn & 7) * 2;
+                float s0 = 0.f, s1 = 0.f;
 #pragma unroll 8
-              for (int k = 0; k < kTcBK; ++k)
-                sum[j] += base[(k * 128 + ((chunk ^ (k & 3)) << 5)) >> 2];
+                for (int k = 0; k < BK; ++k) {
+                  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(
+                      base + k * 128 + ((chunk ^ (k & 7)) << 4)));
+                  s0 += f.x;
+                  s1 += f.y;
+                }
+                sum[j] += s0;
+                sum2[j] += s1;
+              } else {
+                const int box = n >> 5, nn = n & 31, chunk = nn >> 3;
+                const float* base = reinterpret_cast<const float*>(sb + box * 4096) + (nn & 7);
+#pragma unroll 8
+                for (int k = 0; k < kTcBK; ++k)
+                  sum[j] += base[(k * 128 + ((chunk ^ (k & 3)) << 5)) >> 2];
+              }
             }
           }
         }
@@ -857,10 +879,11 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
       if (do_sum) {
 #pragma unroll
         for (int j = 0; j < kCols; ++j) {
-          const int n = bt + j * 32 * kTcBiasWarps;
-          if (n < BN && tn * BN + n < s.N)
-            s.bias_part[(int64_t)(s.g0 + zg) * s.bias_gstride + s.bias_off + zb * s.bias_zstride +
-                        tn * BN + n] = sum[j];
+          const int n = bias_col(j);
+          float* dst = s.bias_part + (int64_t)(s.g0 + zg) * s.bias_gstride + s.bias_off +
+                       zb * s.bias_zstride + tn * BN + n;
+          if (n < BN && tn * BN + n < s.N) dst[0] = sum[j];
+          if (H && n + 1 < BN && tn * BN + n + 1 < s.N) dst[1] = sum2[j];
         }
       }
     }
@@ -1131,7 +1154,7 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
   const int di = dev < 16 ? dev : 0;
   cudaError_t e = cudaSuccess;
   bool launched = false;
-  if constexpr (BMN && !H) {
+  if constexpr (BMN) {
     if (s.bias_part) {
       if (cl == 2) {
         static bool done[16] = {};

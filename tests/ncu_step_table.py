@@ -4,7 +4,7 @@
 sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,\
 lts__throughput.avg.pct_of_peak_sustained_elapsed --clock-control none \
         -k regex:'^(?!k_boot)' --csv --log-file X.csv python tests/prof_step.py 4096 1
-    python tests/ncu_step_table.py X.csv "title" > profiles/rNN_step_kernels.md
+    python tests/ncu_step_table.py X.csv "title" profiles/rNN_gemm_traffic.json > profiles/rNN_step_kernels.md
 
 Takes the LAST model step's launches (from the last k_embed_ln<1> on).
 """
@@ -52,6 +52,9 @@ def main(path, title):
         name = re.sub(r"^void ", "", name)
         t = e.get(M_T, 0) / 1e3
         rb, wb = e.get(M_R, 0) / 1e6, e.get(M_W, 0) / 1e6
+        if name.startswith("k_encode"):  # the coder's own stream, overlapped with the step
+            print(f"| {name} (encoder stream, not in the total) | {e['grid']} | {t:.1f} | | | | |")
+            continue
         tot += t
         if "k_tc_gemm" in name:
             gt += t
@@ -60,7 +63,13 @@ def main(path, title):
               f"{e.get(M_TC, 0):.1f} | {e.get(M_L2, 0):.1f} |")
     print(f"| **total** | | {tot:.1f} | | | | |")
     print(f"\ntcgen05 GEMMs: {gt:.1f} us of {tot:.1f} us; GEMM DRAM traffic {gb:.1f} MB per step.")
+    return dict(gemm_dram_bytes_per_step=gb * 1e6, gemm_us_per_step_serialized=gt,
+                step_us_serialized=tot, source=path)
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "one model step")
+    import json
+    r = main(sys.argv[1], sys.argv[2] if len(sys.argv) > 2 else "one model step")
+    if len(sys.argv) > 3:  # also write the per-step GEMM traffic (bench.py roofline.traffic)
+        with open(sys.argv[3], "w") as f:
+            json.dump(r, f)
