@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "../../include/edpc_b200.h"
 
@@ -70,5 +72,48 @@ __host__ __device__ __forceinline__ int group_begin(int g, int B) {
 }
 
 inline int cdiv(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+
+// ------------------------------------------------ programmatic dependent launch
+//
+// Every kernel of a model step is launched with programmatic stream
+// serialization (pdl_launch): the next kernel is launched as this one's CTAs
+// exit (implicit trigger), runs its prologue, and waits in pdl_entry() for
+// the full completion (and memory) of its predecessor -- the launch / ramp
+// bubbles between the ~45 kernels of a step overlap (C2: 7.35 -> 7.61 MB/s).
+// An explicit early trigger (griddepcontrol.launch_dependents at entry) was
+// measured slower (7.05): waiting CTAs then sat on SMs the side-stream
+// weight-gradient GEMMs could have used.  A kernel calls pdl_entry() before
+// touching anything its predecessor wrote (the tcgen05 GEMM after its TMEM
+// allocation).  Without the launch attribute it is a no-op.  EDPC_PDL=0
+// disables the attribute.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+inline bool pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EDPC_PDL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 }  // namespace edpc

@@ -38,6 +38,7 @@ constexpr int kSimtBM = 64, kSimtBN = 64, kSimtBK = 16;
 
 template <bool TA, bool TB, class Epi>
 __global__ void __launch_bounds__(256) k_gemm_simt(GemmShape g, Epi epi) {
+  pdl_entry();
   __shared__ float As[kSimtBK][kSimtBM + 4];
   __shared__ float Bs[kSimtBK][kSimtBN + 4];
   const int tid = threadIdx.x;
@@ -126,8 +127,7 @@ inline cudaError_t gemm_simt(const GemmShape& g, const Epi& epi, cudaStream_t st
   int nz = g.nzb * (g.ngroups > 0 ? g.ngroups : 1);
   dim3 grid((unsigned)cdiv(g.N, kSimtBN), (unsigned)cdiv(g.M, kSimtBM), (unsigned)nz);
   if (g.M <= 0 || g.N <= 0 || nz <= 0) return cudaSuccess;
-  k_gemm_simt<TA, TB, Epi><<<grid, 256, 0, st>>>(g, epi);
-  return cudaGetLastError();
+  return pdl_launch(k_gemm_simt<TA, TB, Epi>, grid, dim3(256), 0, st, g, epi);
 }
 
 // ------------------------------------------------------------- epilogues

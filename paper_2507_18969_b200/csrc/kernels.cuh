@@ -65,6 +65,7 @@ k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE,
            float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
            float* __restrict__ xhat, float* __restrict__ rstd, float* __restrict__ x0,
            __half* __restrict__ x0h) {
+  pdl_entry();
   const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= Bl) return;
@@ -109,6 +110,7 @@ constexpr int kMaxBranches = 8;
 // overwritten with D_z = GeLU'(prod) * prod_{j != z} H_j, everything the
 // backward product rule needs (model.py:107-119): g_H_z = g_ff * D_z.
 __global__ void k_mbrb_act(float* __restrict__ H, int K, int64_t plane, float* __restrict__ ff) {
+  pdl_entry();
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= plane) return;
   float h[kMaxBranches];
@@ -417,6 +419,7 @@ __global__ void __launch_bounds__(256)
 k_ln_bwd(const float* __restrict__ gx0, const float* __restrict__ xhat,
          const float* __restrict__ rstd, const float* __restrict__ gain,
          const float* __restrict__ up, float* __restrict__ out, int F, int Bl) {
+  pdl_entry();
   const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= Bl) return;
@@ -451,6 +454,7 @@ k_ln_bwd_fused(const float* __restrict__ gx0, const float* __restrict__ xhat,
                const float* __restrict__ up, float* __restrict__ out, int F, int B_global,
                int lane0, int g0, float* __restrict__ partials, int64_t n_shared, int64_t off_g,
                int64_t off_b, float* __restrict__ scratch, unsigned* __restrict__ tickets) {
+  pdl_entry();
   __shared__ float red[8][2 * kLnMaxF];
   __shared__ unsigned ticket;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -548,6 +552,7 @@ k_colsum_groups(const float* __restrict__ src, int64_t ld, int64_t sz,
                 const float* __restrict__ mul, int N, float* __restrict__ partials,
                 int64_t n_shared, int64_t off, int64_t sOff, int g0, int B_global, int lane0,
                 int vec) {
+  pdl_entry();
   __shared__ float4 red[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n = blockIdx.x * 128 + lane * 4;
@@ -608,6 +613,7 @@ k_colsum_groups(const float* __restrict__ src, int64_t ld, int64_t sz,
 __global__ void __launch_bounds__(256)
 k_fdm_fwd(const float* __restrict__ down, const float* __restrict__ U, float* __restrict__ mixed,
           int FP, int Bl) {
+  pdl_entry();
   const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= Bl) return;
@@ -658,6 +664,7 @@ k_fdm_bwd_adam(const float* __restrict__ down, const float* __restrict__ gmix,
                float* __restrict__ U, float* __restrict__ Um, float* __restrict__ Uv,
                float* __restrict__ gdown, int FP, int Bl, StepIdx si, AdamConsts c, double b1d,
                double b2d, float ginv) {
+  pdl_entry();
   const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= Bl) return;
@@ -701,6 +708,7 @@ template <int FP>
 __global__ void __launch_bounds__(256)
 k_fdm_fwd_v(const float* __restrict__ down, const float* __restrict__ U, float* __restrict__ mixed,
             int Bl) {
+  pdl_entry();
   using G = FdmGeo<FP>;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -739,6 +747,7 @@ k_fdm_bwd_adam_v(const float* __restrict__ down, const float* __restrict__ gmix,
                  float* __restrict__ U, float* __restrict__ Um, float* __restrict__ Uv,
                  float* __restrict__ gdown, int Bl, StepIdx si, AdamConsts c, double b1d,
                  double b2d, float ginv) {
+  pdl_entry();
   using G = FdmGeo<FP>;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -831,6 +840,7 @@ __global__ void __launch_bounds__(256)
 k_embed_grad_chunks(ByteCols src, StepIdx si, int T, int DE, int F,
                     const float* __restrict__ gx, const int* __restrict__ chunk_tab,
                     float* __restrict__ sub) {
+  pdl_entry();
   __shared__ uint8_t cbytes[4096];
   __shared__ float grows[kEmbSmemFloats];
   __shared__ int hist[256], off[256], run[256];
@@ -935,6 +945,7 @@ k_embed_grad_chunks(ByteCols src, StepIdx si, int T, int DE, int F,
 __global__ void k_embed_grad_reduce(const float* __restrict__ sub, const int* __restrict__ grp_chunks,
                                     int DE, float* __restrict__ partials, int64_t n_shared,
                                     int64_t off) {
+  pdl_entry();
   const int gl = blockIdx.y;  // local group slot
   const int gg = grp_chunks[3 * gl], k0 = grp_chunks[3 * gl + 1], k1 = grp_chunks[3 * gl + 2];
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -948,6 +959,7 @@ __global__ void k_embed_grad_reduce(const float* __restrict__ sub, const int* __
 // ------------------------------------------------------- fp16 helpers
 
 __global__ void k_to_half(const float* __restrict__ src, __half* __restrict__ dst, int64_t n) {
+  pdl_entry();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x)
     dst[e] = __float2half_rn(src[e]);
@@ -960,6 +972,7 @@ __global__ void k_to_half(const float* __restrict__ src, __half* __restrict__ ds
 __global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, float* __restrict__ V,
                               const float* __restrict__ P, int64_t n, StepIdx si, AdamConsts c,
                               double b1d, double b2d, float ginv, __half* __restrict__ Wh) {
+  pdl_entry();
   float bc1, bc2;
   adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
@@ -990,6 +1003,7 @@ __global__ void __launch_bounds__(256)
 k_softmax_quant(const float* __restrict__ logits, float* __restrict__ probs, int Bl,
                 ByteCols src, StepIdx si, uint32_t* __restrict__ intervals,
                 uint16_t* __restrict__ cdf16) {
+  pdl_entry();
   const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (b >= Bl) return;
@@ -1055,6 +1069,7 @@ k_softmax_quant(const float* __restrict__ logits, float* __restrict__ probs, int
 // multiply by 1/gscale, so the fp32 trajectory is bit-identical to unscaled.
 __global__ void k_dlogits(const float* __restrict__ probs, ByteCols src, StepIdx si, int Bl,
                           float Bf, float gscale, float* __restrict__ g, float* __restrict__ nll) {
+  pdl_entry();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)Bl * 256) return;
   const int b = (int)(e >> 8), v = (int)(e & 255);
@@ -1073,6 +1088,7 @@ __global__ void k_dlogits(const float* __restrict__ probs, ByteCols src, StepIdx
 // (pipeline.py:84-90, coder.py:118-123)
 __global__ void k_boot_intervals(const uint8_t* __restrict__ mat, int64_t L, int Bl, int64_t ncols,
                                  uint32_t* __restrict__ intervals) {
+  pdl_entry();
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= ncols * Bl) return;
   const int64_t i = e / Bl;
@@ -1086,6 +1102,7 @@ __global__ void k_boot_intervals(const uint8_t* __restrict__ mat, int64_t L, int
 __global__ void k_encode_columns(const uint32_t* __restrict__ intervals, int Bl, int spl, int Sl,
                                  int64_t i0, int64_t i1, int64_t* __restrict__ enc_state,
                                  uint32_t* __restrict__ words, int64_t cap_words) {
+  pdl_entry();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= Sl) return;
   int64_t* stp = enc_state + 4 * s;
@@ -1110,6 +1127,7 @@ __global__ void k_encode_columns(const uint32_t* __restrict__ intervals, int Bl,
 
 __global__ void k_encode_finish_all(int64_t* __restrict__ enc_state, uint32_t* __restrict__ words,
                                     int64_t cap_words, int Sl) {
+  pdl_entry();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= Sl) return;
   int64_t* stp = enc_state + 4 * s;
@@ -1125,6 +1143,7 @@ __global__ void k_encode_finish_all(int64_t* __restrict__ enc_state, uint32_t* _
 __global__ void k_decoder_init_all(int64_t* __restrict__ dec_state, const uint8_t* __restrict__ pay,
                                    const int64_t* __restrict__ pay_off,
                                    const int64_t* __restrict__ bits, int Sl) {
+  pdl_entry();
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= Sl) return;
   const uint8_t* d = pay + pay_off[s];
@@ -1145,6 +1164,7 @@ __global__ void k_decode_column(uint8_t* __restrict__ mat, int64_t L, StepIdx si
                                 int64_t* __restrict__ dec_state, const uint8_t* __restrict__ pay,
                                 const int64_t* __restrict__ pay_off,
                                 const int64_t* __restrict__ bits, int* __restrict__ err) {
+  pdl_entry();
   const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (s >= Sl) return;
@@ -1219,6 +1239,7 @@ struct EpiSplit {
 __global__ void k_splitk_reduce(const float* __restrict__ ws, int nsplit, int64_t plane, int N,
                                 const float* __restrict__ bias, const float* __restrict__ resid,
                                 float* __restrict__ out) {
+  pdl_entry();
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (e >= plane) return;
   float4 a = *reinterpret_cast<const float4*>(ws + e);
@@ -1239,6 +1260,7 @@ __global__ void k_splitk_reduce(const float* __restrict__ ws, int nsplit, int64_
 }
 
 __global__ void k_step_advance(int64_t* i, int64_t* t) {
+  pdl_entry();
   *i += 1;
   *t += 1;
 }

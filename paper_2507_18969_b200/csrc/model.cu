@@ -305,6 +305,8 @@ namespace edpc {
 
 constexpr int kTf32MinLanes = 1024;
 
+constexpr int kFdmWarps = 2;  // warps per block of the per-lane FDM kernels
+
 static bool sync_debug() {
   static int v = -1;
   if (v < 0) {
@@ -404,7 +406,7 @@ static cudaError_t splitk_reduce(edpc_ctx* c, int N, const float* bias, const fl
                                  float* out) {
   const int64_t plane = (int64_t)c->Bl * N;
   Scope sc(c, kRegElem, c->st);
-  k_splitk_reduce<<<(unsigned)cdiv(plane / 4, 256), 256, 0, c->st>>>(c->ws, kSplitK, plane, N, bias,
+  pdl_launch(k_splitk_reduce, (unsigned)cdiv(plane / 4, 256), 256, 0, c->st, c->ws, kSplitK, plane, N, bias,
                                                                     resid, out);
   return cudaGetLastError();
 }
@@ -530,7 +532,7 @@ static cudaError_t colsum(edpc_ctx* c, const float* src, int N, int nz, int64_t 
   const int vec = (N % 4 == 0 && sz % 4 == 0 && al16(src) && (!mul || al16(mul))) ? 1 : 0;
   dim3 grid((unsigned)cdiv(N, 128), (unsigned)nz, (unsigned)c->g_count);
   Scope sc(c, kRegColsum, st);
-  k_colsum_groups<<<grid, 256, 0, st>>>(src, N, sz, mul, N, c->Gp, c->lay.n_shared, off, sOff,
+  pdl_launch(k_colsum_groups, grid, 256, 0, st, src, N, sz, mul, N, c->Gp, c->lay.n_shared, off, sOff,
                                            c->g_first, c->lay.B, c->lane0, vec);
   return cudaGetLastError();
 }
@@ -669,11 +671,11 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
     Scope sc_ln(c, kRegElem, c->st);
     __half* x0h = c->h16 ? reinterpret_cast<__half*>(b.x0) : nullptr;
     if (gather)
-      k_embed_ln<true><<<g8, 256, 0, c->st>>>(src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
+      pdl_launch(k_embed_ln<true>, g8, 256, 0, c->st, src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
                                               c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0,
                                               x0h);
     else
-      k_embed_ln<false><<<g8, 256, 0, c->st>>>(src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
+      pdl_launch(k_embed_ln<false>, g8, 256, 0, c->st, src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
                                                c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0,
                                                x0h);
     CK(cudaGetLastError());
@@ -711,7 +713,7 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
     CK(fwd_linear(c, b.x0, F, F, c->W + o.w0, H, L.K, o.wstride, b.H, plane, c->W + o.b0, nullptr,
                   Bl));
     Scope sc_(c, kRegElem, c->st);
-    k_mbrb_act<<<(unsigned)cdiv(plane, 256), 256, 0, c->st>>>(b.H, L.K, plane, b.ff);
+    pdl_launch(k_mbrb_act, (unsigned)cdiv(plane, 256), 256, 0, c->st, b.H, L.K, plane, b.ff);
     CK(cudaGetLastError());
   }
   CK(fwd_linear(c, b.ff, H, H, c->W + o.out_w, F, 1, 0, b.out, 0, c->W + o.out_b, b.x, Bl));
@@ -728,16 +730,18 @@ static int forward(edpc_ctx* c, ByteCols src) {
   {
     Scope sc_(c, kRegFdmFwd, c->st);
     if (L.FP == 64 || L.FP == 128 || L.FP == 256) {
+    // 2-warp blocks: 256-thread blocks left 108 SMs with two blocks and 40
+    // with one (all resident at once), 86% balance; 64-thread blocks ~99%
     const int lpw = 32 / std::min(32, L.FP / 4);
-    const unsigned blocks = (unsigned)cdiv(cdiv(Bl, lpw), 8);
+    const unsigned blocks = (unsigned)cdiv(cdiv(Bl, lpw), kFdmWarps);
     if (L.FP == 64)
-      k_fdm_fwd_v<64><<<blocks, 256, 0, c->st>>>(c->down, c->U, c->mixed, Bl);
+      pdl_launch(k_fdm_fwd_v<64>, blocks, 32 * kFdmWarps, 0, c->st, c->down, c->U, c->mixed, Bl);
     else if (L.FP == 128)
-      k_fdm_fwd_v<128><<<blocks, 256, 0, c->st>>>(c->down, c->U, c->mixed, Bl);
+      pdl_launch(k_fdm_fwd_v<128>, blocks, 32 * kFdmWarps, 0, c->st, c->down, c->U, c->mixed, Bl);
     else
-      k_fdm_fwd_v<256><<<blocks, 256, 0, c->st>>>(c->down, c->U, c->mixed, Bl);
+      pdl_launch(k_fdm_fwd_v<256>, blocks, 32 * kFdmWarps, 0, c->st, c->down, c->U, c->mixed, Bl);
   } else {
-    k_fdm_fwd<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(c->down, c->U, c->mixed, L.FP, Bl);
+    pdl_launch(k_fdm_fwd, (unsigned)cdiv(Bl, 8), 256, 0, c->st, c->down, c->U, c->mixed, L.FP, Bl);
   }
   }
   CK(cudaGetLastError());
@@ -754,13 +758,13 @@ static int softmax_quant(edpc_ctx* c, int mode, ByteCols src) {
   dim3 g8((unsigned)cdiv(c->Bl, 8));
   Scope sc(c, kRegSoftmax, c->st);
   if (mode == kProbsOnly)
-    k_softmax_quant<kProbsOnly><<<g8, 256, 0, c->st>>>(c->logits, c->probs, c->Bl, src, c->si(),
+    pdl_launch(k_softmax_quant<kProbsOnly>, g8, 256, 0, c->st, c->logits, c->probs, c->Bl, src, c->si(),
                                                        c->intervals, c->cdf16);
   else if (mode == kEncode)
-    k_softmax_quant<kEncode><<<g8, 256, 0, c->st>>>(c->logits, c->probs, c->Bl, src, c->si(),
+    pdl_launch(k_softmax_quant<kEncode>, g8, 256, 0, c->st, c->logits, c->probs, c->Bl, src, c->si(),
                                                     c->intervals, c->cdf16);
   else
-    k_softmax_quant<kDecode><<<g8, 256, 0, c->st>>>(c->logits, c->probs, c->Bl, src, c->si(),
+    pdl_launch(k_softmax_quant<kDecode>, g8, 256, 0, c->st, c->logits, c->probs, c->Bl, src, c->si(),
                                                     c->intervals, c->cdf16);
   CK(cudaGetLastError());
   return EDPC_OK;
@@ -812,7 +816,7 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
       maxg = std::max(maxg, group_begin(g + 1, L.B) - group_begin(g, L.B));
     dim3 grid((unsigned)std::max(1, cdiv(maxg, kLnChunk)), (unsigned)c->g_count);
     Scope sc(c, kRegElem, c->st);
-    k_ln_bwd_fused<<<grid, 256, 0, c->st>>>(c->gx0, b.xhat, b.rstd, c->W + o.ln_g, g_up, g_in, F,
+    pdl_launch(k_ln_bwd_fused, grid, 256, 0, c->st, c->gx0, b.xhat, b.rstd, c->W + o.ln_g, g_up, g_in, F,
                                             L.B, c->lane0, c->g_first, c->Gp, L.n_shared, o.ln_g,
                                             o.ln_b, c->ln_scratch, c->ln_tickets);
     CK(cudaGetLastError());
@@ -820,7 +824,7 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
     CK(colsum(c, c->gx0, F, 1, 0, b.xhat, o.ln_g, 0));
     CK(colsum(c, c->gx0, F, 1, 0, nullptr, o.ln_b, 0));
     Scope sc(c, kRegElem, c->st);
-    k_ln_bwd<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(c->gx0, b.xhat, b.rstd, c->W + o.ln_g, g_up,
+    pdl_launch(k_ln_bwd, (unsigned)cdiv(Bl, 8), 256, 0, c->st, c->gx0, b.xhat, b.rstd, c->W + o.ln_g, g_up,
                                                        g_in, F, Bl);
     CK(cudaGetLastError());
   }
@@ -832,7 +836,7 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   const int Bl = c->Bl, F = L.F, FP = L.FP;
   {
     Scope sc_(c, kRegElem, c->st);
-    k_dlogits<<<(unsigned)cdiv((int64_t)Bl * 256, 256), 256, 0, c->st>>>(
+    pdl_launch(k_dlogits, (unsigned)cdiv((int64_t)Bl * 256, 256), 256, 0, c->st, 
         c->probs, src, c->si(), Bl, (float)L.B, ldexpf(1.0f, c->gs_log2), c->gl, nll);
   }
   CK(cudaGetLastError());
@@ -854,12 +858,12 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   {
     if (FP == 64 || FP == 128 || FP == 256) {
       const int lpw = 32 / std::min(32, FP / 4);
-      const unsigned blocks = (unsigned)cdiv(cdiv(Bl, lpw), 8);
+      const unsigned blocks = (unsigned)cdiv(cdiv(Bl, lpw), kFdmWarps);
       auto run = [&](auto kern, cudaStream_t st) {
         Scope sc_(c, kRegFdmBwd, st);
-        kern<<<blocks, 256, 0, st>>>(c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, Bl, c->si(),
-                                     c->adam, c->cfg.beta1, c->cfg.beta2,
-                                     ldexpf(1.0f, -c->gs_log2));
+        pdl_launch(kern, blocks, 32 * kFdmWarps, 0, st, c->down, c->gmix, c->U, c->Um, c->Uv,
+                   c->gdown, Bl, c->si(), c->adam, c->cfg.beta1, c->cfg.beta2,
+                   ldexpf(1.0f, -c->gs_log2));
       };
       // split measured 1% slower at C2: the persistent GEMMs own whole SMs,
       // so the side-stream Adam pass barely overlaps and U is read twice
@@ -891,7 +895,7 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
       }
     } else {
       Scope sc_(c, kRegFdmBwd, c->st);
-      k_fdm_bwd_adam<<<(unsigned)cdiv(Bl, 8), 256, 0, c->st>>>(
+      pdl_launch(k_fdm_bwd_adam, (unsigned)cdiv(Bl, 8), 256, 0, c->st, 
           c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, FP, Bl, c->si(), c->adam,
           c->cfg.beta1, c->cfg.beta2, ldexpf(1.0f, -c->gs_log2));
     }
@@ -911,14 +915,14 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll) {
   if (c->n_chunks > 0) {
     {
       Scope sc_(c, kRegEmbed, c->st);
-      k_embed_grad_chunks<<<(unsigned)c->n_chunks, 256, 0, c->st>>>(src, c->si(), L.T, L.DE, F,
+      pdl_launch(k_embed_grad_chunks, (unsigned)c->n_chunks, 256, 0, c->st, src, c->si(), L.T, L.DE, F,
                                                                     c->g_emb, c->chunk_tab, c->emb_sub);
     }
     CK(cudaGetLastError());
     dim3 gr((unsigned)cdiv(256 * L.DE, 256), (unsigned)c->g_count);
     {
       Scope sc_(c, kRegEmbed, c->st);
-      k_embed_grad_reduce<<<gr, 256, 0, c->st>>>(c->emb_sub, c->grp_chunks, L.DE, c->Gp,
+      pdl_launch(k_embed_grad_reduce, gr, 256, 0, c->st, c->emb_sub, c->grp_chunks, L.DE, c->Gp,
                                                  L.n_shared, L.emb);
     }
     CK(cudaGetLastError());
@@ -931,7 +935,7 @@ static int adam_shared(edpc_ctx* c) {
   int blocks = (int)std::min<int64_t>(cdiv(c->lay.n_shared, 256), 148 * 8);
   {
     Scope sc_(c, kRegAdam, c->st);
-    k_adam_shared<<<blocks, 256, 0, c->st>>>(c->W, c->M, c->V, c->Gp, c->lay.n_shared, c->si(),
+    pdl_launch(k_adam_shared, blocks, 256, 0, c->st, c->W, c->M, c->V, c->Gp, c->lay.n_shared, c->si(),
                                              c->adam, c->cfg.beta1, c->cfg.beta2,
                                              ldexpf(1.0f, -c->gs_log2), c->h16 ? c->Wh : nullptr);
   }
@@ -960,7 +964,7 @@ static int model_step(edpc_ctx* c, int mode) {
   EDPC_TRY(softmax_quant(c, mode, src));
   if (mode == kDecode) {
     Scope sc(c, kRegDecode, c->st);
-    k_decode_column<<<(unsigned)cdiv(c->Sl, 4), 128, 0, c->st>>>(
+    pdl_launch(k_decode_column, (unsigned)cdiv(c->Sl, 4), 128, 0, c->st, 
         c->mat, c->L, c->si(), c->spl, c->Sl, c->cdf16, false, c->dec_state, c->payload,
         c->pay_off, c->bit_len, c->dec_err);
     CK(cudaGetLastError());
@@ -970,7 +974,7 @@ static int model_step(edpc_ctx* c, int mode) {
   EDPC_TRY(adam_shared(c));
   {
     Scope sc_(c, kRegElem, c->st);
-    k_step_advance<<<1, 1, 0, c->st>>>(c->d_i, c->d_t);
+    pdl_launch(k_step_advance, 1, 1, 0, c->st, c->d_i, c->d_t);
   }
   CK(cudaGetLastError());
   return EDPC_OK;
@@ -1030,7 +1034,7 @@ static int launch_encoder(edpc_ctx* c, int64_t upto) {
   CK(cudaEventRecord(c->ev, c->st));
   CK(cudaStreamWaitEvent(c->st_enc, c->ev, 0));
   Scope sc(c, kRegEncode, c->st_enc);
-  k_encode_columns<<<(unsigned)cdiv(c->Sl, 64), 64, 0, c->st_enc>>>(
+  pdl_launch(k_encode_columns, (unsigned)cdiv(c->Sl, 64), 64, 0, c->st_enc, 
       c->intervals, c->Bl, c->spl, c->Sl, c->enc_upto, upto, c->enc_state, c->enc_words,
       c->enc_cap_words);
   CK(cudaGetLastError());
@@ -1304,7 +1308,7 @@ int edpc_load_params(edpc_ctx* c, const float* params, int64_t count) {
   EDPC_CUDA_TRY(cudaMemcpy(c->U, params + L.ref_lane_mats + (int64_t)c->lane0 * L.fdm,
                            (int64_t)c->Bl * L.fdm * 4, cudaMemcpyHostToDevice));
   if (c->h16) {  // the fp16 weight shadow starts from the loaded weights
-    k_to_half<<<(unsigned)std::min<int64_t>(cdiv(L.n_shared, 256), 148 * 8), 256, 0, c->st>>>(
+    pdl_launch(k_to_half, (unsigned)std::min<int64_t>(cdiv(L.n_shared, 256), 148 * 8), 256, 0, c->st, 
         c->W, c->Wh, L.n_shared);
     EDPC_CUDA_TRY(cudaGetLastError());
     EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
@@ -1419,7 +1423,7 @@ int edpc_compress_steps(edpc_ctx* c, int64_t i0, int64_t i1) {
   const int64_t boot = std::min<int64_t>(T, c->L);
   if (i0 < boot) {
     const int64_t a = i0, e = std::min(i1, boot);
-    k_boot_intervals<<<(unsigned)cdiv((e) * (int64_t)c->Bl, 256), 256, 0, c->st>>>(
+    pdl_launch(k_boot_intervals, (unsigned)cdiv((e) * (int64_t)c->Bl, 256), 256, 0, c->st, 
         c->mat, c->L, c->Bl, e, c->intervals);
     EDPC_CUDA_TRY(cudaGetLastError());
     (void)a;
@@ -1445,7 +1449,7 @@ int edpc_compress_finish(edpc_ctx* c, int64_t* bit_lengths, int64_t* total_bytes
   // a stream is finished after the columns actually produced (normally all L)
   EDPC_TRY(launch_encoder(c, c->cols_done));
   Scope sc(c, kRegEncode, c->st_enc, "encode_finish");
-  k_encode_finish_all<<<(unsigned)cdiv(c->Sl, 64), 64, 0, c->st_enc>>>(
+  pdl_launch(k_encode_finish_all, (unsigned)cdiv(c->Sl, 64), 64, 0, c->st_enc, 
       c->enc_state, c->enc_words, c->enc_cap_words, c->Sl);
   EDPC_CUDA_TRY(cudaGetLastError());
   EDPC_CUDA_TRY(cudaStreamSynchronize(c->st_enc));
@@ -1501,7 +1505,7 @@ int edpc_set_payloads(edpc_ctx* c, const uint8_t* data, const int64_t* bit_lengt
   }
   EDPC_CUDA_TRY(cudaMemcpy(c->pay_off, off.data(), (c->Sl + 1) * 8, cudaMemcpyHostToDevice));
   EDPC_CUDA_TRY(cudaMemcpy(c->bit_len, bit_lengths, c->Sl * 8, cudaMemcpyHostToDevice));
-  k_decoder_init_all<<<(unsigned)cdiv(c->Sl, 64), 64, 0, c->st>>>(c->dec_state, c->payload,
+  pdl_launch(k_decoder_init_all, (unsigned)cdiv(c->Sl, 64), 64, 0, c->st, c->dec_state, c->payload,
                                                                  c->pay_off, c->bit_len, c->Sl);
   EDPC_CUDA_TRY(cudaGetLastError());
   EDPC_CUDA_TRY(cudaMemsetAsync(c->mat, 0, (int64_t)c->Bl * std::max<int64_t>(c->L, 1), c->st));
@@ -1518,7 +1522,7 @@ int edpc_decompress_steps(edpc_ctx* c, int64_t i0, int64_t i1) {
   const int64_t boot = std::min<int64_t>(T, c->L);
   for (int64_t i = i0; i < std::min(i1, boot); ++i) {
     EDPC_TRY(set_step(c, i, 0));
-    k_decode_column<<<(unsigned)cdiv(c->Sl, 4), 128, 0, c->st>>>(
+    pdl_launch(k_decode_column, (unsigned)cdiv(c->Sl, 4), 128, 0, c->st, 
         c->mat, c->L, c->si(), c->spl, c->Sl, c->cdf16, true, c->dec_state, c->payload,
         c->pay_off, c->bit_len, c->dec_err);
     EDPC_CUDA_TRY(cudaGetLastError());
@@ -1606,7 +1610,7 @@ int edpc_step_phase(edpc_ctx* c, int64_t i, int32_t phase, int32_t decompress) {
     EDPC_TRY(forward(c, src));
     EDPC_TRY(softmax_quant(c, decompress ? kDecode : kEncode, src));
     if (decompress) {
-      k_decode_column<<<(unsigned)cdiv(c->Sl, 4), 128, 0, c->st>>>(
+      pdl_launch(k_decode_column, (unsigned)cdiv(c->Sl, 4), 128, 0, c->st, 
           c->mat, c->L, c->si(), c->spl, c->Sl, c->cdf16, false, c->dec_state, c->payload,
           c->pay_off, c->bit_len, c->dec_err);
       EDPC_CUDA_TRY(cudaGetLastError());
