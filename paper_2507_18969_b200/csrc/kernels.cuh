@@ -1002,7 +1002,7 @@ template <int kMode>
 __global__ void __launch_bounds__(256)
 k_softmax_quant(const float* __restrict__ logits, float* __restrict__ probs, int Bl,
                 ByteCols src, StepIdx si, uint32_t* __restrict__ intervals,
-                uint16_t* __restrict__ cdf16) {
+                uint16_t* __restrict__ cdf16, float Bf, float gscale, float* __restrict__ g) {
   pdl_entry();
   const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -1041,6 +1041,14 @@ k_softmax_quant(const float* __restrict__ logits, float* __restrict__ probs, int
   const int64_t i = *si.i;
   if (kMode == kEncode) {
     const int tgt = src.base[(int64_t)b * src.ld + i];
+    if (g) {  // the loss gradient, fused (k_dlogits' exact arithmetic; the target is known)
+      float gv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) gv[j] = ((lane * 8 + j == tgt ? x[j] - 1.0f : x[j]) / Bf) * gscale;
+      float* gr = g + (int64_t)b * 256 + lane * 8;
+      *reinterpret_cast<float4*>(gr) = make_float4(gv[0], gv[1], gv[2], gv[3]);
+      *reinterpret_cast<float4*>(gr + 4) = make_float4(gv[4], gv[5], gv[6], gv[7]);
+    }
     if ((tgt >> 3) == lane) {
       uint32_t lo = 0, fr = 0;
 #pragma unroll

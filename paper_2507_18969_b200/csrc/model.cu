@@ -757,15 +757,16 @@ static int forward(edpc_ctx* c, ByteCols src) {
 static int softmax_quant(edpc_ctx* c, int mode, ByteCols src) {
   dim3 g8((unsigned)cdiv(c->Bl, 8));
   Scope sc(c, kRegSoftmax, c->st);
+  const float Bf = (float)c->lay.B, gs = ldexpf(1.0f, c->gs_log2);
   if (mode == kProbsOnly)
-    pdl_launch(k_softmax_quant<kProbsOnly>, g8, 256, 0, c->st, c->logits, c->probs, c->Bl, src, c->si(),
-                                                       c->intervals, c->cdf16);
-  else if (mode == kEncode)
-    pdl_launch(k_softmax_quant<kEncode>, g8, 256, 0, c->st, c->logits, c->probs, c->Bl, src, c->si(),
-                                                    c->intervals, c->cdf16);
+    pdl_launch(k_softmax_quant<kProbsOnly>, g8, 256, 0, c->st, c->logits, c->probs, c->Bl, src,
+               c->si(), c->intervals, c->cdf16, Bf, gs, nullptr);
+  else if (mode == kEncode)  // also the loss gradient (backward skips k_dlogits)
+    pdl_launch(k_softmax_quant<kEncode>, g8, 256, 0, c->st, c->logits, c->probs, c->Bl, src,
+               c->si(), c->intervals, c->cdf16, Bf, gs, c->gl);
   else
-    pdl_launch(k_softmax_quant<kDecode>, g8, 256, 0, c->st, c->logits, c->probs, c->Bl, src, c->si(),
-                                                    c->intervals, c->cdf16);
+    pdl_launch(k_softmax_quant<kDecode>, g8, 256, 0, c->st, c->logits, c->probs, c->Bl, src,
+               c->si(), c->intervals, c->cdf16, Bf, gs, nullptr);
   CK(cudaGetLastError());
   return EDPC_OK;
 }
@@ -831,10 +832,10 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
   return EDPC_OK;
 }
 
-static int backward(edpc_ctx* c, ByteCols src, float* nll) {
+static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = false) {
   const Layout& L = c->lay;
   const int Bl = c->Bl, F = L.F, FP = L.FP;
-  {
+  if (!have_dlogits) {
     Scope sc_(c, kRegElem, c->st);
     pdl_launch(k_dlogits, (unsigned)cdiv((int64_t)Bl * 256, 256), 256, 0, c->st, 
         c->probs, src, c->si(), Bl, (float)L.B, ldexpf(1.0f, c->gs_log2), c->gl, nll);
@@ -969,7 +970,7 @@ static int model_step(edpc_ctx* c, int mode) {
         c->pay_off, c->bit_len, c->dec_err);
     CK(cudaGetLastError());
   }
-  EDPC_TRY(backward(c, src, nullptr));
+  EDPC_TRY(backward(c, src, nullptr, mode == kEncode));
   EDPC_TRY(exchange_partials(c));
   EDPC_TRY(adam_shared(c));
   {
@@ -1615,7 +1616,7 @@ int edpc_step_phase(edpc_ctx* c, int64_t i, int32_t phase, int32_t decompress) {
           c->pay_off, c->bit_len, c->dec_err);
       EDPC_CUDA_TRY(cudaGetLastError());
     }
-    EDPC_TRY(backward(c, src, nullptr));
+    EDPC_TRY(backward(c, src, nullptr, !decompress));
     if (!decompress) c->cols_done = std::max(c->cols_done, i + 1);
     return EDPC_OK;
   }
