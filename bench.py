@@ -206,9 +206,11 @@ def run_ours(args, wl):
     from paper_2507_18969_b200.model import DeviceContext
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    if world > 1 or args.gpus > 1:
+    # EDPC_BENCH_MULTI=1: the torchrun/NCCL path even at one rank (smoke test)
+    if world > 1 or args.gpus > 1 or os.environ.get("EDPC_BENCH_MULTI") == "1":
         from paper_2507_18969_b200.dist import bench_multi
-        return bench_multi(args, wl)
+        return bench_multi(args, wl, clocks_cls=Clocks, peaks=peaks()[0],
+                           flops_per_lane=gemm_flops_per_lane)
     lib = _lib.load()
     _lib.require_device(0)
     cfg = ModelConfig(**wl["model"], lanes=wl["lanes"])

@@ -1250,18 +1250,29 @@ __global__ void k_splitk_reduce(const float* __restrict__ ws, int nsplit, int64_
   pdl_entry();
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (e >= plane) return;
-  float4 a = *reinterpret_cast<const float4*>(ws + e);
-  for (int s = 1; s < nsplit; ++s) {
-    const float4 b = *reinterpret_cast<const float4*>(ws + s * plane + e);
-    a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
-  }
+  // every load issued before the first add (a dependent loop kept one in flight)
+  constexpr int kMax = 4;
+  float4 w[kMax];
+#pragma unroll
+  for (int s = 0; s < kMax; ++s)
+    if (s < nsplit) w[s] = *reinterpret_cast<const float4*>(ws + s * plane + e);
   const int n = (int)(e % N);
+  const float4 b = bias ? *reinterpret_cast<const float4*>(bias + n) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const float4 r = resid ? *reinterpret_cast<const float4*>(resid + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 a = w[0];
+#pragma unroll
+  for (int s = 1; s < kMax; ++s)
+    if (s < nsplit) {
+      a.x += w[s].x; a.y += w[s].y; a.z += w[s].z; a.w += w[s].w;
+    }
+  for (int s = kMax; s < nsplit; ++s) {
+    const float4 q = *reinterpret_cast<const float4*>(ws + s * plane + e);
+    a.x += q.x; a.y += q.y; a.z += q.z; a.w += q.w;
+  }
   if (bias) {
-    const float4 b = *reinterpret_cast<const float4*>(bias + n);
     a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
   }
   if (resid) {
-    const float4 r = *reinterpret_cast<const float4*>(resid + e);
     a.x += r.x; a.y += r.y; a.z += r.z; a.w += r.w;
   }
   *reinterpret_cast<float4*>(out + e) = a;

@@ -204,7 +204,7 @@ def torch_broadcast_id(uid):
     return obj[0]
 
 
-def bench_multi(args, wl) -> None:
+def bench_multi(args, wl, clocks_cls=None, peaks=None, flops_per_lane=None) -> None:
     """bench.py at N GPUs under torchrun: weak scaling (B/N lanes per GPU is
     fixed by the workload's per-GPU share), one NCCL all-gather of the
     gradient partials per model step inside the captured step graph; the
@@ -237,6 +237,7 @@ def bench_multi(args, wl) -> None:
     mine = np.frombuffer(synth.generate(wl["kind"], lc * L, wl["seed"] + rank), dtype=np.uint8)
     ctx = DeviceContext(cfg, S, n, local, lb, lc)
     ctx.load_flat(init_params_f32(cfg))
+    numerics = ctx.numerics()
     _lib.check(lib.edpc_set_input_local(ctx.h, mine.ctypes.data, mine.size))
     nccl_join(ctx, rank, world, torch_broadcast_id)
     _lib.check(lib.edpc_compress_steps(ctx.h, 0, T))
@@ -247,13 +248,17 @@ def bench_multi(args, wl) -> None:
     _lib.check(lib.edpc_sync(ctx.h))
     dist.barrier()
     torch.cuda.synchronize()
-    _lib.check(lib.edpc_timer(ctx.h, 0, None))
-    for k in range(K):
-        _lib.check(lib.edpc_compress_steps(ctx.h, col, col + chunk))
-        col += chunk
-    _lib.check(lib.edpc_timer(ctx.h, 1, None))
-    ms = ctypes.c_double()
-    _lib.check(lib.edpc_timer(ctx.h, 2, ctypes.byref(ms)))
+    import contextlib
+    sampler = clocks_cls(local) if (clocks_cls and rank == 0) else contextlib.nullcontext()
+    with sampler as clk:
+        _lib.check(lib.edpc_timer(ctx.h, 0, None))
+        for k in range(K):
+            _lib.check(lib.edpc_compress_steps(ctx.h, col, col + chunk))
+            col += chunk
+        _lib.check(lib.edpc_timer(ctx.h, 1, None))
+        ms = ctypes.c_double()
+        _lib.check(lib.edpc_timer(ctx.h, 2, ctypes.byref(ms)))
+    clocks = getattr(clk, "result", None) if clk is not None else None
     torch.cuda.synchronize()
     dist.barrier()
     t = torch.tensor([ms.value], device="cuda")
@@ -261,11 +266,22 @@ def bench_multi(args, wl) -> None:
     ms_max = float(t.item())
     total_bytes = cfg.lanes * chunk * K  # all ranks' lanes
     if rank == 0:
+        dtype = ("fp16+tf32" if numerics["fp16_mbrb"] else "tf32") if numerics["tcgen05"] else "fp32"
+        roof = None
+        if peaks and flops_per_lane:
+            # whole-step rate per GPU (this path has no per-kernel breakdown)
+            fl = flops_per_lane(wl["model"]) * lc * chunk * K
+            ach = fl / (ms_max / 1e3) / 1e12
+            pk = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops"))
+            roof = dict(bound="tensor", kernel="whole model step per GPU (all kernels)",
+                        achieved=ach, peak=pk, unit="TFLOP/s", frac=ach / pk, traffic=None)
         line = dict(metric="compress/decompress MB/s at 1/2/4/8 B200 + bits/byte vs CPU ref",
                     value=total_bytes / (ms_max / 1e3) / 1e6, unit="MB/s", n_gpus=world,
                     steps=K, warmup=W, ms_per_step=ms_max / K, higher_is_better=True,
-                    scaling="weak", vs_baseline=None,
-                    dtype="tf32", data=f"synthetic {wl['kind']}-like (PCG64 seed {wl['seed']} + rank)",
+                    scaling="weak", vs_baseline=None, numerics=numerics, clocks=clocks,
+                    roofline=roof, cpu_baseline=None,
+                    e2e=None, e2e_note="multi-GPU lines time the device-resident loop only",
+                    dtype=dtype, data=f"synthetic {wl['kind']}-like (PCG64 seed {wl['seed']} + rank)",
                     config=dict(workload=f"{wl['desc']} per GPU; {world} GPUs: B={cfg.lanes}, "
                                          f"S={S}, {n >> 20} MiB (C3-style weak scaling)",
                                 lanes=cfg.lanes, segments=S,
