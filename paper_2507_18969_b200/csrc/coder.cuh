@@ -237,6 +237,8 @@ __device__ __forceinline__ void enc_finish(EncState& st, BitWriter& w) {
 struct DecState {
   uint64_t low, high, code;
   int64_t bitpos;
+  int64_t cidx = -1;   // payload byte cached in cbyte (one load per 8 bits, not per bit)
+  uint32_t cbyte = 0;
 };
 
 __device__ __forceinline__ uint32_t read_bit(const uint8_t* data, int64_t bit_length,
@@ -271,7 +273,12 @@ __device__ __forceinline__ bool dec_advance(DecState& st, const uint8_t* data,
     high = (high << 1) | 1;
     uint32_t bit = 0;
     if (bp < bit_length) {
-      bit = (uint32_t)((data[bp >> 3] >> (7 - (bp & 7))) & 1);
+      const int64_t bi = bp >> 3;
+      if (bi != st.cidx) {
+        st.cidx = bi;
+        st.cbyte = data[bi];
+      }
+      bit = (st.cbyte >> (7 - (bp & 7))) & 1u;
     } else if (bp > limit) {
       st.bitpos = bp;
       return false;
@@ -286,9 +293,16 @@ __device__ __forceinline__ bool dec_advance(DecState& st, const uint8_t* data,
   return true;
 }
 
-// coder.py:186: value = ((code - low + 1) * TOTAL - 1) // span
+// coder.py:186: value = ((code - low + 1) * TOTAL - 1) // span.  num < 2^49
+// and span <= 2^32 are exact doubles; the correctly rounded quotient floors
+// to the true quotient or one above it (rounding up across an integer), so
+// one correction makes it exact -- instead of a 64-bit integer division on
+// the decoder's serial critical path.
 __device__ __forceinline__ uint64_t dec_value(const DecState& st, uint64_t span) {
-  return (((st.code - st.low + 1) << 16) - 1) / span;
+  const uint64_t num = ((st.code - st.low + 1) << 16) - 1;
+  uint64_t q = (uint64_t)((double)num / (double)span);
+  if (q * span > num) --q;
+  return q;
 }
 
 // Warp-cooperative symbol search: lane l holds cum[8l..8l+7] (cum[0] = 0).

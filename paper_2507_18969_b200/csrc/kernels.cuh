@@ -1183,29 +1183,48 @@ __global__ void k_decode_column(uint8_t* __restrict__ mat, int64_t L, StepIdx si
   const uint8_t* data = pay + pay_off[s];
   const int64_t nbits = bits[s];
   bool ok = !dead;
-  for (int bl = 0; bl < spl; ++bl) {
-    const int b = s * spl + bl;
-    int sym = 0;
-    if (ok) {
-      uint32_t cum[8];
-      if (uniform) {
+  // the segment's CDF rows are independent of the coder state: loaded kPf
+  // rows ahead (double-buffered) so the serial symbol chain never waits on them
+  constexpr int kPf = 8;
+  uint4 cur[kPf], nxt[kPf];
+  auto load_rows = [&](uint4 (&q)[kPf], int bl0) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) cum[j] = (uint32_t)(lane * 8 + j) * 256u;
-      } else {
-        uint4 pk = *reinterpret_cast<const uint4*>(cdf16 + (int64_t)b * 256 + lane * 8);
-        cum[0] = pk.x & 0xffffu; cum[1] = pk.x >> 16;
-        cum[2] = pk.y & 0xffffu; cum[3] = pk.y >> 16;
-        cum[4] = pk.z & 0xffffu; cum[5] = pk.z >> 16;
-        cum[6] = pk.w & 0xffffu; cum[7] = pk.w >> 16;
+    for (int j = 0; j < kPf; ++j)
+      if (!uniform && bl0 + j < spl)
+        q[j] = *reinterpret_cast<const uint4*>(cdf16 + (int64_t)(s * spl + bl0 + j) * 256 + lane * 8);
+  };
+  load_rows(cur, 0);
+  for (int g0 = 0; g0 < spl; g0 += kPf) {
+    if (g0 + kPf < spl) load_rows(nxt, g0 + kPf);
+#pragma unroll
+    for (int j = 0; j < kPf; ++j) {
+      const int bl = g0 + j;
+      if (bl >= spl) break;
+      const int b = s * spl + bl;
+      int sym = 0;
+      if (ok) {
+        uint32_t cum[8];
+        if (uniform) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) cum[u] = (uint32_t)(lane * 8 + u) * 256u;
+        } else {
+          const uint4 pk = cur[j];
+          cum[0] = pk.x & 0xffffu; cum[1] = pk.x >> 16;
+          cum[2] = pk.y & 0xffffu; cum[3] = pk.y >> 16;
+          cum[4] = pk.z & 0xffffu; cum[5] = pk.z >> 16;
+          cum[6] = pk.w & 0xffffu; cum[7] = pk.w >> 16;
+        }
+        const uint64_t span = st.high - st.low + 1;
+        const uint64_t value = dec_value(st, span);
+        uint32_t c_lo, c_hi;
+        sym = warp_find_symbol(cum, value, c_lo, c_hi);
+        ok = dec_advance(st, data, nbits, span, c_lo, c_hi);
+        if (!ok) sym = 0;
       }
-      const uint64_t span = st.high - st.low + 1;
-      const uint64_t value = dec_value(st, span);
-      uint32_t c_lo, c_hi;
-      sym = warp_find_symbol(cum, value, c_lo, c_hi);
-      ok = dec_advance(st, data, nbits, span, c_lo, c_hi);
-      if (!ok) sym = 0;
+      if (lane == 0) mat[(int64_t)b * L + i] = (uint8_t)sym;
     }
-    if (lane == 0) mat[(int64_t)b * L + i] = (uint8_t)sym;
+#pragma unroll
+    for (int j = 0; j < kPf; ++j) cur[j] = nxt[j];
   }
   if (lane == 0) {
     if (!ok && !dead) err[s] = 1;
