@@ -969,9 +969,12 @@ __global__ void k_to_half(const float* __restrict__ src, __half* __restrict__ ds
 
 // grad = ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)) -- the canonical G-invariant
 // tree over the 8 lane groups -- then fused Adam (_kernels.py:18-32).
+// Over params [0, n) of the given (offset) pointers; partial g of param e at
+// P[g * pstride + e].
 __global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, float* __restrict__ V,
-                              const float* __restrict__ P, int64_t n, StepIdx si, AdamConsts c,
-                              double b1d, double b2d, float ginv, __half* __restrict__ Wh) {
+                              const float* __restrict__ P, int64_t n, int64_t pstride, StepIdx si,
+                              AdamConsts c, double b1d, double b2d, float ginv,
+                              __half* __restrict__ Wh) {
   pdl_entry();
   float bc1, bc2;
   adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
@@ -979,7 +982,7 @@ __global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, floa
        e += (int64_t)gridDim.x * blockDim.x) {
     float q[8];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) q[g] = P[g * n + e];
+    for (int g = 0; g < 8; ++g) q[g] = P[g * pstride + e];
     const float grad = (((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]))) * ginv;
     float w = W[e], m = M[e], v = V[e];
     adam_elem(w, m, v, grad, c, bc1, bc2);

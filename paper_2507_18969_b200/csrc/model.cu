@@ -832,6 +832,9 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
   return EDPC_OK;
 }
 
+static int adam_range(edpc_ctx* c, int64_t off, int64_t len, cudaStream_t st);
+static bool early_adam(const edpc_ctx* c);
+
 static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = false) {
   const Layout& L = c->lay;
   const int Bl = c->Bl, F = L.F, FP = L.FP;
@@ -851,6 +854,10 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
   // global MBRB: d(x_global) -> d(x_lte)
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
   EDPC_TRY(mbrb_backward(c, L.glo, gb, c->g_head, c->g_lte, c->GH_g, c->guph_g));
+  if (early_adam(c)) {  // global MBRB weights + head: wgrads done on aux, dgrads issued on main
+    CK(fork_aux(c));
+    EDPC_TRY(adam_range(c, L.glo.w0, L.n_shared - L.glo.w0, c->st_aux));
+  }
   // LTE up
   CK(fork_aux(c));
   CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
@@ -909,6 +916,10 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
     CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore2{c->g_loc, c->guph_l, F}));
   else
     CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore{c->g_loc, F}));
+  if (early_adam(c)) {  // LTE down + up
+    CK(fork_aux(c));
+    EDPC_TRY(adam_range(c, L.down_w, L.glo.ln_g - L.down_w, c->st_aux));
+  }
   // local MBRB: d(x_local) -> d(x_emb) (gradient w.r.t. the embedded context)
   MbrbBufs lb{c->x_emb, c->l_xhat, c->l_rstd, c->l_x0, c->l_H, c->l_ff, c->x_local};
   EDPC_TRY(mbrb_backward(c, L.loc, lb, c->g_loc, c->g_emb, c->GH_l, c->guph_l));
@@ -932,16 +943,36 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
   return EDPC_OK;
 }
 
-static int adam_shared(edpc_ctx* c) {
-  int blocks = (int)std::min<int64_t>(cdiv(c->lay.n_shared, 256), 148 * 8);
+// Adam over shared params [off, off + len) on stream st
+static int adam_range(edpc_ctx* c, int64_t off, int64_t len, cudaStream_t st) {
+  if (len <= 0) return EDPC_OK;
+  const int blocks = (int)std::min<int64_t>(cdiv(len, 256), 148 * 8);
   {
-    Scope sc_(c, kRegAdam, c->st);
-    pdl_launch(k_adam_shared, blocks, 256, 0, c->st, c->W, c->M, c->V, c->Gp, c->lay.n_shared, c->si(),
-                                             c->adam, c->cfg.beta1, c->cfg.beta2,
-                                             ldexpf(1.0f, -c->gs_log2), c->h16 ? c->Wh : nullptr);
+    Scope sc_(c, kRegAdam, st);
+    pdl_launch(k_adam_shared, blocks, 256, 0, st, c->W + off, c->M + off, c->V + off, c->Gp + off,
+               len, c->lay.n_shared, c->si(), c->adam, c->cfg.beta1, c->cfg.beta2,
+               ldexpf(1.0f, -c->gs_log2), c->h16 ? c->Wh + off : nullptr);
   }
   CK(cudaGetLastError());
   return EDPC_OK;
+}
+
+// Early Adam: with all 8 lane groups in this context (no exchange before the
+// optimizer), the global-MBRB weights + head and the LTE projections are
+// updated on the side stream as soon as their gradients are complete and the
+// main stream has finished reading them; only the embedding, the local MBRB
+// and the global LN parameters are left for the end of the step.
+static bool early_adam(const edpc_ctx* c) {
+  return c->g_count == kNumGroups && !c->comm && aux_enabled();
+}
+
+static int adam_shared(edpc_ctx* c) {
+  const Layout& L = c->lay;
+  if (early_adam(c)) {
+    EDPC_TRY(adam_range(c, 0, L.down_w, c->st));                 // embedding + local MBRB
+    return adam_range(c, L.glo.ln_g, L.glo.w0 - L.glo.ln_g, c->st);  // global LN
+  }
+  return adam_range(c, 0, L.n_shared, c->st);
 }
 
 // Multi-GPU: every rank holds 8/G consecutive lane groups, so the partial
