@@ -43,6 +43,47 @@ __device__ __forceinline__ K warp_kth_largest(const K (&key)[8], int k, int top_
   return thr;
 }
 
+// The same selection for the 49-bit keys of fp32-representable rows, in two
+// 32-bit levels: the k-th largest of the high 32 bits (key >> 17) first, then
+// -- only if several keys tie at that threshold and not all of them are
+// selected -- the remaining low 17 bits among the tied keys.  Returns the
+// same key as warp_kth_largest<uint64_t, 49> (keys are distinct) in 32 cheap
+// iterations instead of 49 64-bit ones (the quantizer was issue-bound).
+__device__ __forceinline__ uint64_t warp_kth_largest_49(const uint64_t (&key)[8], int k) {
+  uint32_t hi[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) hi[j] = (uint32_t)(key[j] >> 17);
+  uint32_t thr = 0;
+  for (int bit = 31; bit >= 0; --bit) {
+    const uint32_t cand = thr | (1u << bit);
+    int c = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) c += hi[j] >= cand ? 1 : 0;
+    if (__reduce_add_sync(0xffffffffu, c) >= k) thr = cand;
+  }
+  int gt = 0, eq = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    gt += hi[j] > thr ? 1 : 0;
+    eq += hi[j] == thr ? 1 : 0;
+  }
+  gt = __reduce_add_sync(0xffffffffu, gt);
+  eq = __reduce_add_sync(0xffffffffu, eq);
+  const int k2 = k - gt;  // 1 <= k2 <= eq
+  uint32_t lo_thr = 0;
+  if (k2 < eq) {
+    for (int bit = 16; bit >= 0; --bit) {
+      const uint32_t cand = lo_thr | (1u << bit);
+      int c = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        c += (hi[j] == thr && (uint32_t)(key[j] & 0x1FFFFu) >= cand) ? 1 : 0;
+      if (__reduce_add_sync(0xffffffffu, c) >= k2) lo_thr = cand;
+    }
+  }
+  return ((uint64_t)thr << 17) | lo_thr;
+}
+
 // Remainder key.  For fp32-representable probabilities p*65280 has at most
 // 32 significant bits, so the float64 remainder's low 21 fraction bits are
 // zero: (bits >> 21) keeps the full order in 41 bits and leaves room for the
@@ -95,7 +136,11 @@ __device__ __forceinline__ void warp_quantize(const double (&p)[8], int (&freq)[
   if (deficit > 0) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) key[j] = Q::make(rem[j], lane * 8 + j);
-    K thr = warp_kth_largest<K, Q::kBits>(key, deficit, Q::kBits - 1);
+    K thr;
+    if constexpr (kF64)
+      thr = warp_kth_largest<K, Q::kBits>(key, deficit, Q::kBits - 1);
+    else
+      thr = warp_kth_largest_49(key, deficit);
 #pragma unroll
     for (int j = 0; j < 8; ++j) freq[j] += key[j] >= thr ? 1 : 0;
   } else if (deficit < 0) {

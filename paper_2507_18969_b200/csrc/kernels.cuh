@@ -720,7 +720,7 @@ k_fdm_fwd_v(const float* __restrict__ down, const float* __restrict__ U, float* 
   float4 acc[G::kNV];
 #pragma unroll
   for (int v = 0; v < G::kNV; ++v) acc[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 8
+#pragma unroll 16  // 16 rows of U in flight per thread
   for (int i = 0; i < FP; ++i) {
     const float di = d[i];
 #pragma unroll
