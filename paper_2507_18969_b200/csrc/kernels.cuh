@@ -57,6 +57,8 @@ __device__ __forceinline__ void gelu_pair(float x, float& f, float& dg) {
 
 // ------------------------------------------------------ gather + layer norm
 
+constexpr int kLnRowMax = 512;  // rows up to this many features stay in registers
+
 // x = E[ctx] (model.py:255), then LN (nn.py:103-113, population variance,
 // eps 1e-5 under the sqrt).  One warp per lane.  gather=false: x is input.
 template <bool kGather>
@@ -70,35 +72,87 @@ k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE,
   const int lane = threadIdx.x & 31;
   if (b >= Bl) return;
   float* xr = x + (int64_t)b * F;
-  float s = 0.f;
+  if (F > kLnRowMax) {  // generic path (rows longer than the register tile)
+    float s = 0.f;
+    if (kGather) {
+      const int64_t col0 = *si.i - T;
+      const uint8_t* row = src.base + (int64_t)b * src.ld + col0;
+      for (int f = lane; f < F; f += 32) {
+        int p = f / DE, d = f - p * DE;
+        float v = E[(int)row[p] * DE + d];
+        xr[f] = v;
+        s += v;
+      }
+    } else {
+      for (int f = lane; f < F; f += 32) s += xr[f];
+    }
+    const float mean = warp_sum(s) / (float)F;
+    float q = 0.f;
+    for (int f = lane; f < F; f += 32) {
+      float d = xr[f] - mean;
+      q += d * d;
+    }
+    const float var = warp_sum(q) / (float)F;
+    const float r = 1.0f / sqrtf(var + 1e-5f);
+    for (int f = lane; f < F; f += 32) {
+      float h = (xr[f] - mean) * r;
+      xhat[(int64_t)b * F + f] = h;
+      const float v = h * gain[f] + bias[f];
+      if (x0h)
+        x0h[(int64_t)b * F + f] = __float2half_rn(v);
+      else
+        x0[(int64_t)b * F + f] = v;
+    }
+    if (lane == 0) rstd[b] = r;
+    return;
+  }
+  // the row in registers, every gather / load in flight before the sums
+  // (re-reading x from global memory made this latency bound)
+  constexpr int kJ = kLnRowMax / 32;
+  float v[kJ];
   if (kGather) {
     const int64_t col0 = *si.i - T;
     const uint8_t* row = src.base + (int64_t)b * src.ld + col0;
-    for (int f = lane; f < F; f += 32) {
-      int p = f / DE, d = f - p * DE;
-      float v = E[(int)row[p] * DE + d];
-      xr[f] = v;
-      s += v;
+#pragma unroll
+    for (int j = 0; j < kJ; ++j) {
+      const int f = lane + 32 * j;
+      if (f < F) {
+        const int p = f / DE, d = f - p * DE;
+        v[j] = E[(int)row[p] * DE + d];
+      }
     }
   } else {
-    for (int f = lane; f < F; f += 32) s += xr[f];
+#pragma unroll
+    for (int j = 0; j < kJ; ++j)
+      if (lane + 32 * j < F) v[j] = xr[lane + 32 * j];
   }
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < kJ; ++j)
+    if (lane + 32 * j < F) s += v[j];
   const float mean = warp_sum(s) / (float)F;
   float q = 0.f;
-  for (int f = lane; f < F; f += 32) {
-    float d = xr[f] - mean;
-    q += d * d;
-  }
+#pragma unroll
+  for (int j = 0; j < kJ; ++j)
+    if (lane + 32 * j < F) {
+      const float d = v[j] - mean;
+      q += d * d;
+    }
   const float var = warp_sum(q) / (float)F;
   const float r = 1.0f / sqrtf(var + 1e-5f);
-  for (int f = lane; f < F; f += 32) {
-    float h = (xr[f] - mean) * r;
-    xhat[(int64_t)b * F + f] = h;
-    const float v = h * gain[f] + bias[f];
-    if (x0h)  // fp16 GEMM path: x0 only feeds the branch GEMM and its weight gradient
-      x0h[(int64_t)b * F + f] = __float2half_rn(v);
-    else
-      x0[(int64_t)b * F + f] = v;
+#pragma unroll
+  for (int j = 0; j < kJ; ++j) {
+    const int f = lane + 32 * j;
+    if (f < F) {
+      if (kGather) xr[f] = v[j];
+      const float h = (v[j] - mean) * r;
+      xhat[(int64_t)b * F + f] = h;
+      const float o = h * gain[f] + bias[f];
+      if (x0h)  // fp16 GEMM path: x0 only feeds the branch GEMM and its weight gradient
+        x0h[(int64_t)b * F + f] = __float2half_rn(o);
+      else
+        x0[(int64_t)b * F + f] = o;
+    }
   }
   if (lane == 0) rstd[b] = r;
 }
