@@ -873,9 +873,10 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
                    c->gdown, Bl, c->si(), c->adam, c->cfg.beta1, c->cfg.beta2,
                    ldexpf(1.0f, -c->gs_log2));
       };
-      // split measured 1% slower at C2: the persistent GEMMs own whole SMs,
-      // so the side-stream Adam pass barely overlaps and U is read twice
-      const bool split = false;
+      // split (EDPC_FDM_SPLIT=1, experiment) measured 3% slower at C2: the
+      // side-stream Adam pass competes with the main stream for HBM and U is
+      // read twice
+      const bool split = getenv("EDPC_FDM_SPLIT") && getenv("EDPC_FDM_SPLIT")[0] == '1';
       if (FP == 64) {
         if (split) {
           run(k_fdm_bwd_adam_v<64, true, false>, c->st);
