@@ -854,9 +854,9 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
   // global MBRB: d(x_global) -> d(x_lte)
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
   EDPC_TRY(mbrb_backward(c, L.glo, gb, c->g_head, c->g_lte, c->GH_g, c->guph_g));
-  if (early_adam(c)) {  // global MBRB weights + head: wgrads done on aux, dgrads issued on main
+  if (early_adam(c)) {  // global MBRB (its LN backward included) + head: gradients complete
     CK(fork_aux(c));
-    EDPC_TRY(adam_range(c, L.glo.w0, L.n_shared - L.glo.w0, c->st_aux));
+    EDPC_TRY(adam_range(c, L.glo.ln_g, L.n_shared - L.glo.ln_g, c->st_aux));
   }
   // LTE up
   CK(fork_aux(c));
@@ -961,18 +961,15 @@ static int adam_range(edpc_ctx* c, int64_t off, int64_t len, cudaStream_t st) {
 // Early Adam: with all 8 lane groups in this context (no exchange before the
 // optimizer), the global-MBRB weights + head and the LTE projections are
 // updated on the side stream as soon as their gradients are complete and the
-// main stream has finished reading them; only the embedding, the local MBRB
-// and the global LN parameters are left for the end of the step.
+// main stream has finished reading them; only the embedding and the local
+// MBRB are left for the end of the step.
 static bool early_adam(const edpc_ctx* c) {
   return c->g_count == kNumGroups && !c->comm && aux_enabled();
 }
 
 static int adam_shared(edpc_ctx* c) {
   const Layout& L = c->lay;
-  if (early_adam(c)) {
-    EDPC_TRY(adam_range(c, 0, L.down_w, c->st));                 // embedding + local MBRB
-    return adam_range(c, L.glo.ln_g, L.glo.w0 - L.glo.ln_g, c->st);  // global LN
-  }
+  if (early_adam(c)) return adam_range(c, 0, L.down_w, c->st);  // embedding + local MBRB
   return adam_range(c, 0, L.n_shared, c->st);
 }
 
