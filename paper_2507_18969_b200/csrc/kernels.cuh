@@ -694,20 +694,27 @@ __device__ __forceinline__ double ipow(double a, int64_t e) {
   return r;
 }
 
+// Per-launch Adam constants from the bias corrections bc1 = 1 - b1^t,
+// bc2 = 1 - b2^t (t shared by all parameters, numba's exponentiation by
+// squaring): step = lr / bc1 and rs2 = 1 / sqrt(bc2).
 __device__ __forceinline__ void adam_bc(const AdamConsts& c, double b1d, double b2d, int64_t t,
-                                        float& bc1, float& bc2) {
-  bc1 = (float)(1.0 - ipow(b1d, t));
-  bc2 = (float)(1.0 - ipow(b2d, t));
+                                        float& step, float& rs2) {
+  const double bc1 = 1.0 - ipow(b1d, t), bc2 = 1.0 - ipow(b2d, t);
+  step = (float)((double)c.lr / bc1);
+  rs2 = (float)(1.0 / sqrt(bc2));
 }
 
-// _kernels.py:26-31 in fp32
+// _kernels.py:26-31 in fp32: w -= lr * (m/bc1) / (sqrt(v/bc2) + eps), with the
+// bias corrections folded into the per-launch constants and one fast division
+// (~2 ulp; it scales the update, not w) instead of two IEEE divisions and a
+// sqrt of a quotient -- the per-lane FDM Adam was issue-bound on them.
 __device__ __forceinline__ void adam_elem(float& w, float& m, float& v, float g,
-                                          const AdamConsts& c, float bc1, float bc2) {
-  float mi = c.b1 * m + c.k1 * g;
-  float vi = c.b2 * v + c.k2 * (g * g);
+                                          const AdamConsts& c, float step, float rs2) {
+  const float mi = c.b1 * m + c.k1 * g;
+  const float vi = c.b2 * v + c.k2 * (g * g);
   m = mi;
   v = vi;
-  w -= (c.lr * (mi / bc1)) / (sqrtf(vi / bc2) + c.eps);
+  w -= __fdividef(step * mi, fmaf(sqrtf(vi), rs2, c.eps));
 }
 
 // Fused FDM backward + per-lane Adam (nn.py:177-179 then _kernels.py:18-32 on
