@@ -532,6 +532,13 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   };
 
   if (warp == 0 && lane == 0) {
+    // descriptors fetched while the predecessor drains (before pdl_entry)
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+    if (s.ts) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_c) : "memory");
+      if (kTsIn > 0) asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_d) : "memory");
+    }
     for (int st = 0; st < kStages; ++st) {
       mbar_init(&full[st], 1);
       mbar_init(&empty[st], CL * (BIAS ? 2 : 1));
