@@ -145,23 +145,35 @@ int edpc_train_step(edpc_ctx* ctx, const uint8_t* targets, float* loss);
 int edpc_last_probs(edpc_ctx* ctx, float* probs);
 
 /* --------------------------------------------------- multi-GPU step phases
- * For G > 1 the host drives each model step as: phase 0 (forward, coder,
- * backward, per-lane FDM update; shared-parameter gradients left as 8 fixed
- * lane-group partials) -> exchange of the partials -> phase 1 (canonical
- * tree reduction + Adam).  edpc_grad_partials exposes the device buffer. */
+ * Replaces the reference's single shared-model update (model.py:265-281,
+ * _adam_all model.py:223-235) when the lanes of one container are sharded
+ * over G contexts (G divides 8, rank r owns lane groups
+ * [r*8/G, (r+1)*8/G)).  Sharded optimizer, per model step:
+ *   phase 0: forward, coder, backward, per-lane FDM update; the rank's
+ *            shared-parameter gradient partials reduced to its subtree sum;
+ *   exchange 1: rank j's subtree sum of rank r's owned parameter slice ->
+ *            rank r (edpc_partials_pull, or NCCL send/recv inside phase 1);
+ *   phase 1: G-leaf canonical tree + Adam on the owned slice only;
+ *   exchange 2: the owned slices of the updated weights to every rank
+ *            (edpc_weights_pull, or NCCL all-gather inside phase 1).
+ * The trajectory is bit-identical to one context holding all 8 groups. */
 int edpc_step_phase(edpc_ctx* ctx, int64_t i, int32_t phase, int32_t decompress);
 int edpc_grad_partials(edpc_ctx* ctx, float** dev_ptr, int64_t* n_shared);
 /* this context's lane groups [g_first, g_first + g_count) */
 int edpc_ctx_groups(edpc_ctx* ctx, int32_t* g_first, int32_t* g_count);
+/* this context's owned shared-parameter slice [off, off + len) */
+int edpc_shard_range(edpc_ctx* ctx, int64_t* off, int64_t* len);
 /* host copy of lane-group partials [g0, g0+ng) x n_shared (to_device 0: read) */
 int edpc_partials_copy(edpc_ctx* ctx, int32_t g0, int32_t ng, float* host, int32_t to_device);
-/* single-process multi-context exchange: dst <- src's own groups (peer copy) */
+/* single-process multi-context exchanges (peer copies, stream-ordered):
+ * dst <- src's subtree sum of dst's owned slice; dst <- src's owned weights */
 int edpc_partials_pull(edpc_ctx* dst, edpc_ctx* src);
+int edpc_weights_pull(edpc_ctx* dst, edpc_ctx* src);
 /* hand produced columns [.., upto) to the encoder stream (phase-driven compress) */
 int edpc_encode_pending(edpc_ctx* ctx, int64_t upto);
 /* NCCL: rank 0 makes an id (128 bytes), every rank joins concurrently; after
- * that each model step all-gathers the partials in place over NVLink inside
- * the step (and inside its CUDA graph) -- multi-process, one GPU per rank. */
+ * that each model step runs both exchanges over NVLink inside the step (and
+ * inside its CUDA graph) -- multi-process, one GPU per rank. */
 int edpc_nccl_unique_id(uint8_t* out, int32_t cap);
 int edpc_ctx_set_comm(edpc_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t rank);
 

@@ -83,6 +83,8 @@ _SIGS = {
     "edpc_partials_copy": ([_P, _I32, _I32, _P, _I32], ctypes.c_int),
     "edpc_encode_pending": ([_P, _I64], ctypes.c_int),
     "edpc_partials_pull": ([_P, _P], ctypes.c_int),
+    "edpc_weights_pull": ([_P, _P], ctypes.c_int),
+    "edpc_shard_range": ([_P, _P, _P], ctypes.c_int),
     "edpc_nccl_unique_id": ([_P, _I32], ctypes.c_int),
     "edpc_ctx_set_comm": ([_P, _P, _I32, _I32], ctypes.c_int),
     "edpc_sync": ([_P], ctypes.c_int),

@@ -46,6 +46,9 @@ struct Status {
 constexpr int kVocab = 256;
 constexpr int kTotal = 1 << 16;
 constexpr int kNumGroups = 8;  // fixed lane groups of the G-invariant reduction
+// padding of the weight buffers so G <= 8 slices of 64-aligned equal length
+// cover them (in-place all-gather of the sharded optimizer's output)
+constexpr int64_t kShardPad = kNumGroups * 64;
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll

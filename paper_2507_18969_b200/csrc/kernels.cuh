@@ -1028,10 +1028,25 @@ __global__ void k_to_half(const float* __restrict__ src, __half* __restrict__ ds
 
 // ------------------------------------------------------- Adam (shared)
 
-// grad = ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7)) -- the canonical G-invariant
-// tree over the 8 lane groups -- then fused Adam (_kernels.py:18-32).
-// Over params [0, n) of the given (offset) pointers; partial g of param e at
-// P[g * pstride + e].
+// Pairwise tree over NL in {1,2,4,8} leaves q[0..NL): for NL = 8 this is
+// ((q0+q1)+(q2+q3))+((q4+q5)+(q6+q7)) -- the canonical G-invariant order over
+// the 8 lane groups.  A subtree of 8/G consecutive groups is
+// itself a tree of this shape, so "subtree sums on each of G ranks, then the
+// NL = G tree over the subtree sums" is bit-identical to the NL = 8 tree.
+template <int NL>
+__device__ __forceinline__ float tree_sum(const float* q) {
+  if constexpr (NL == 1) {
+    return q[0];
+  } else {
+    return tree_sum<NL / 2>(q) + tree_sum<NL / 2>(q + NL / 2);
+  }
+}
+
+// grad = tree over NL leaves (leaf g of param e at P[g * pstride + e]) then
+// fused Adam (_kernels.py:18-32).  NL = 8: the 8 lane-group partials of one
+// context; NL = G: the G ranks' subtree sums of this rank's owned slice
+// (multi-GPU, after the slice exchange).
+template <int NL>
 __global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, float* __restrict__ V,
                               const float* __restrict__ P, int64_t n, int64_t pstride, StepIdx si,
                               AdamConsts c, double b1d, double b2d, float ginv,
@@ -1041,16 +1056,30 @@ __global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, floa
   adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
-    float q[8];
+    float q[NL];
 #pragma unroll
-    for (int g = 0; g < 8; ++g) q[g] = P[g * pstride + e];
-    const float grad = (((q[0] + q[1]) + (q[2] + q[3])) + ((q[4] + q[5]) + (q[6] + q[7]))) * ginv;
+    for (int g = 0; g < NL; ++g) q[g] = P[g * pstride + e];
+    const float grad = tree_sum<NL>(q) * ginv;
     float w = W[e], m = M[e], v = V[e];
     adam_elem(w, m, v, grad, c, bc1, bc2);
     W[e] = w;
     if (Wh) Wh[e] = __float2half_rn(w);  // fp16 shadow for the fp16 GEMMs
     M[e] = m;
     V[e] = v;
+  }
+}
+
+// Multi-GPU: P[0][e] = tree over this rank's NL lane-group partials
+// P[g * pstride + e] (in place into leaf 0; elementwise, so no hazard).
+template <int NL>
+__global__ void k_group_tree(float* __restrict__ P, int64_t n, int64_t pstride) {
+  pdl_entry();
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float q[NL];
+#pragma unroll
+    for (int g = 0; g < NL; ++g) q[g] = P[g * pstride + e];
+    P[e] = tree_sum<NL>(q);
   }
 }
 

@@ -36,6 +36,11 @@ struct NcclApi {
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
   ncclResult_t (*allGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*groupStart)() = nullptr;
+  ncclResult_t (*groupEnd)() = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
   const char* (*getErrorString)(ncclResult_t) = nullptr;
   bool ok = false;
@@ -52,10 +57,14 @@ static NcclApi& nccl() {
       api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
       api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
       api.allGather = (decltype(api.allGather))dlsym(h, "ncclAllGather");
+      api.send = (decltype(api.send))dlsym(h, "ncclSend");
+      api.recv = (decltype(api.recv))dlsym(h, "ncclRecv");
+      api.groupStart = (decltype(api.groupStart))dlsym(h, "ncclGroupStart");
+      api.groupEnd = (decltype(api.groupEnd))dlsym(h, "ncclGroupEnd");
       api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
       api.getErrorString = (decltype(api.getErrorString))dlsym(h, "ncclGetErrorString");
-      api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.commDestroy &&
-               api.getErrorString;
+      api.ok = api.getUniqueId && api.commInitRank && api.allGather && api.send && api.recv &&
+               api.groupStart && api.groupEnd && api.commDestroy && api.getErrorString;
     }
   }
   return api;
@@ -220,7 +229,7 @@ struct edpc_ctx {
   cudaEvent_t ev = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr, tj = nullptr;
   cudaGraphExec_t graph[2] = {nullptr, nullptr};
-  ncclComm_t comm = nullptr;  // multi-GPU: all-gather of the lane-group gradient partials
+  ncclComm_t comm = nullptr;  // multi-GPU: slice exchange of subtree sums + weight all-gather
   int nranks = 1, rank = 0;
   AdamConsts adam{};
 
@@ -832,7 +841,8 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
   return EDPC_OK;
 }
 
-static int adam_range(edpc_ctx* c, int64_t off, int64_t len, cudaStream_t st);
+static int adam_range(edpc_ctx* c, int64_t off, int64_t len, cudaStream_t st, int nl = kNumGroups,
+                      int64_t pstride = -1);
 static bool early_adam(const edpc_ctx* c);
 
 static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = false) {
@@ -944,15 +954,68 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
   return EDPC_OK;
 }
 
-// Adam over shared params [off, off + len) on stream st
-static int adam_range(edpc_ctx* c, int64_t off, int64_t len, cudaStream_t st) {
+// ------------------------------------------------ shared-parameter Adam
+//
+// One context holding all 8 lane groups: grad = the 8-leaf canonical tree
+// over its partials, Adam over every shared parameter.
+//
+// G > 1 contexts (one per GPU, or several on one GPU through dist.ShardSet),
+// rank r owning the 8/G groups [r*8/G, (r+1)*8/G) -- the sharded optimizer of
+// SURVEY.md §8e:
+//   1. k_group_tree: the rank's subtree sum of its groups, into its first
+//      group's partial slot (skipped when 8/G == 1);
+//   2. slice exchange: the shared parameters are cut into G slices; rank j's
+//      subtree sum of slice r goes to rank r (NCCL send/recv, or peer copies
+//      via edpc_partials_pull), landing in slot j*8/G of r's partial buffer;
+//   3. k_adam_shared<G> on the owned slice: the G-leaf tree over the subtree
+//      sums (= the 8-leaf tree, bit for bit) then Adam; m, v are only ever
+//      touched on the owned slice;
+//   4. all-gather of the updated fp32 weights and their fp16 shadow (NCCL
+//      in place, or edpc_weights_pull).
+// Per step each GPU sends (G-1)/G of one partial and receives (G-1)/G of the
+// weights, instead of all-gathering 8/G full partials per rank.
+
+static int shard_count(const edpc_ctx* c) {
+  return c->g_count > 0 && c->g_count < kNumGroups ? kNumGroups / c->g_count : 1;
+}
+static int shard_rank(const edpc_ctx* c) {
+  return shard_count(c) > 1 ? c->g_first / c->g_count : 0;
+}
+static int64_t shard_slice(const edpc_ctx* c) {
+  const int G = shard_count(c);
+  return (cdiv(c->lay.n_shared, (int64_t)G) + 63) / 64 * 64;
+}
+// owned parameter range [*off, *off + *len) of shard r
+static void shard_range(const edpc_ctx* c, int r, int64_t* off, int64_t* len) {
+  const int64_t s = shard_slice(c), P = c->lay.n_shared;
+  *off = std::min<int64_t>(P, (int64_t)r * s);
+  *len = std::min<int64_t>(P, (int64_t)(r + 1) * s) - *off;
+}
+
+template <int NL>
+static void adam_launch(edpc_ctx* c, int blocks, cudaStream_t st, int64_t off, int64_t len,
+                        int64_t pstride) {
+  pdl_launch(k_adam_shared<NL>, blocks, 256, 0, st, c->W + off, c->M + off, c->V + off,
+             c->Gp + off, len, pstride, c->si(), c->adam, c->cfg.beta1, c->cfg.beta2,
+             ldexpf(1.0f, -c->gs_log2), c->h16 ? c->Wh + off : nullptr);
+}
+
+// Adam over shared params [off, off + len) on stream st; nl leaves at stride
+// pstride (8 lane groups, or G subtree sums)
+static int adam_range(edpc_ctx* c, int64_t off, int64_t len, cudaStream_t st, int nl,
+                      int64_t pstride) {
   if (len <= 0) return EDPC_OK;
+  if (pstride < 0) pstride = c->lay.n_shared;
   const int blocks = (int)std::min<int64_t>(cdiv(len, 256), 148 * 8);
   {
     Scope sc_(c, kRegAdam, st);
-    pdl_launch(k_adam_shared, blocks, 256, 0, st, c->W + off, c->M + off, c->V + off, c->Gp + off,
-               len, c->lay.n_shared, c->si(), c->adam, c->cfg.beta1, c->cfg.beta2,
-               ldexpf(1.0f, -c->gs_log2), c->h16 ? c->Wh + off : nullptr);
+    switch (nl) {
+      case 1: adam_launch<1>(c, blocks, st, off, len, pstride); break;
+      case 2: adam_launch<2>(c, blocks, st, off, len, pstride); break;
+      case 4: adam_launch<4>(c, blocks, st, off, len, pstride); break;
+      case 8: adam_launch<8>(c, blocks, st, off, len, pstride); break;
+      default: set_error("bad leaf count"); return EDPC_ERR_INVALID;
+    }
   }
   CK(cudaGetLastError());
   return EDPC_OK;
@@ -967,23 +1030,87 @@ static bool early_adam(const edpc_ctx* c) {
   return c->g_count == kNumGroups && !c->comm && aux_enabled();
 }
 
+// step 1 (sharded): subtree sum of the local groups into slot g_first
+static int group_tree(edpc_ctx* c) {
+  if (shard_count(c) < 2 || c->g_count < 2) return EDPC_OK;
+  const int64_t P = c->lay.n_shared;
+  const int blocks = (int)std::min<int64_t>(cdiv(P, 256), 148 * 8);
+  float* base = c->Gp + (size_t)c->g_first * P;
+  {
+    Scope sc_(c, kRegAdam, c->st);
+    if (c->g_count == 2)
+      pdl_launch(k_group_tree<2>, blocks, 256, 0, c->st, base, P, P);
+    else if (c->g_count == 4)
+      pdl_launch(k_group_tree<4>, blocks, 256, 0, c->st, base, P, P);
+    else {
+      set_error("bad lane-group share");
+      return EDPC_ERR_INVALID;
+    }
+  }
+  CK(cudaGetLastError());
+  return EDPC_OK;
+}
+
 static int adam_shared(edpc_ctx* c) {
   const Layout& L = c->lay;
+  const int G = shard_count(c);
+  if (G > 1) {  // step 3 (sharded): owned slice, G-leaf tree over subtree sums
+    int64_t off, len;
+    shard_range(c, shard_rank(c), &off, &len);
+    return adam_range(c, off, len, c->st, G, (int64_t)c->g_count * L.n_shared);
+  }
   if (early_adam(c)) return adam_range(c, 0, L.down_w, c->st);  // embedding + local MBRB
   return adam_range(c, 0, L.n_shared, c->st);
 }
 
-// Multi-GPU: every rank holds 8/G consecutive lane groups, so the partial
-// buffer [8][n_shared] is exactly an in-place all-gather of equal slices.
-static int exchange_partials(edpc_ctx* c) {
+static int nccl_fail(const char* what, ncclResult_t r) {
+  set_error(std::string(what) + ": " + nccl().getErrorString(r));
+  return EDPC_ERR_CUDA;
+}
+
+// step 2 over NCCL: rank j's subtree sum of slice r -> rank r, slot j*8/G
+static int exchange_slices(edpc_ctx* c) {
   if (!c->comm || c->nranks < 2) return EDPC_OK;
-  const size_t cnt = (size_t)c->g_count * c->lay.n_shared;
-  ncclResult_t r = nccl().allGather(c->Gp + (size_t)c->g_first * c->lay.n_shared, c->Gp, cnt,
-                                    ncclFloat, c->comm, c->st);
-  if (r != ncclSuccess) {
-    set_error(std::string("ncclAllGather: ") + nccl().getErrorString(r));
-    return EDPC_ERR_CUDA;
+  const int G = c->nranks, r = c->rank;
+  const size_t P = (size_t)c->lay.n_shared, gc = (size_t)c->g_count;
+  int64_t ro, rl;
+  shard_range(c, r, &ro, &rl);
+  ncclResult_t e = nccl().groupStart();
+  if (e != ncclSuccess) return nccl_fail("ncclGroupStart", e);
+  for (int j = 0; j < G && e == ncclSuccess; ++j) {
+    if (j == r) continue;
+    int64_t jo, jl;
+    shard_range(c, j, &jo, &jl);
+    if (jl > 0) e = nccl().send(c->Gp + r * gc * P + jo, (size_t)jl, ncclFloat, j, c->comm, c->st);
+    if (e == ncclSuccess && rl > 0)
+      e = nccl().recv(c->Gp + j * gc * P + ro, (size_t)rl, ncclFloat, j, c->comm, c->st);
   }
+  ncclResult_t e2 = nccl().groupEnd();
+  if (e != ncclSuccess) return nccl_fail("ncclSend/ncclRecv", e);
+  if (e2 != ncclSuccess) return nccl_fail("ncclGroupEnd", e2);
+  return EDPC_OK;
+}
+
+// step 4 over NCCL: in-place all-gather of the owned weight slices (fp32 and
+// the fp16 shadow); W / Wh are padded to G equal slices
+static int exchange_weights(edpc_ctx* c) {
+  if (!c->comm || c->nranks < 2) return EDPC_OK;
+  const size_t s = (size_t)shard_slice(c), r = (size_t)c->rank;
+  ncclResult_t e = nccl().allGather(c->W + r * s, c->W, s, ncclFloat, c->comm, c->st);
+  if (e != ncclSuccess) return nccl_fail("ncclAllGather(W)", e);
+  if (c->h16) {
+    e = nccl().allGather(c->Wh + r * s, c->Wh, s, ncclHalf, c->comm, c->st);
+    if (e != ncclSuccess) return nccl_fail("ncclAllGather(Wh)", e);
+  }
+  return EDPC_OK;
+}
+
+// steps 1-4 after backward()
+static int optimizer_step(edpc_ctx* c) {
+  EDPC_TRY(group_tree(c));
+  EDPC_TRY(exchange_slices(c));
+  EDPC_TRY(adam_shared(c));
+  EDPC_TRY(exchange_weights(c));
   return EDPC_OK;
 }
 
@@ -1000,8 +1127,7 @@ static int model_step(edpc_ctx* c, int mode) {
     CK(cudaGetLastError());
   }
   EDPC_TRY(backward(c, src, nullptr, mode == kEncode));
-  EDPC_TRY(exchange_partials(c));
-  EDPC_TRY(adam_shared(c));
+  EDPC_TRY(optimizer_step(c));
   {
     Scope sc_(c, kRegElem, c->st);
     pdl_launch(k_step_advance, 1, 1, 0, c->st, c->d_i, c->d_t);
@@ -1187,7 +1313,7 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
     int _r = c->alloc(&(p), (n));       \
     if (_r != EDPC_OK) return fail(_r); \
   } while (0)
-  A_(c->W, L.n_shared);
+  A_(c->W, L.n_shared + kShardPad);  // padded: in-place all-gather of equal slices
   A_(c->M, L.n_shared);
   A_(c->V, L.n_shared);
   A_(c->Gp, (int64_t)kNumGroups * L.n_shared);
@@ -1225,7 +1351,7 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
   A_(c->GH_g, (int64_t)L.K * Bl * L.HG);
   A_(c->GH_l, (int64_t)L.K * Bl * L.HL);
   if (c->h16) {
-    A_(c->Wh, L.n_shared);
+    A_(c->Wh, L.n_shared + kShardPad);
     A_(c->guph_l, Bl * F);
     A_(c->guph_g, Bl * F);
   }
@@ -1646,12 +1772,14 @@ int edpc_step_phase(edpc_ctx* c, int64_t i, int32_t phase, int32_t decompress) {
       EDPC_CUDA_TRY(cudaGetLastError());
     }
     EDPC_TRY(backward(c, src, nullptr, !decompress));
+    EDPC_TRY(group_tree(c));
     if (!decompress) c->cols_done = std::max(c->cols_done, i + 1);
     return EDPC_OK;
   }
   EDPC_CHECK_ARG(phase == 1, "phase must be 0 or 1");
-  EDPC_TRY(exchange_partials(c));
+  EDPC_TRY(exchange_slices(c));
   EDPC_TRY(adam_shared(c));
+  EDPC_TRY(exchange_weights(c));
   return EDPC_OK;
 }
 
@@ -1675,23 +1803,53 @@ int edpc_partials_copy(edpc_ctx* c, int32_t g0, int32_t ng, float* host, int32_t
   return EDPC_OK;
 }
 
-// dst <- src's own lane-group partials, device to device (peer copy over
-// NVLink when the contexts sit on different GPUs).  Ordered after src's
-// queued work; src's later work is ordered after the copy.
-int edpc_partials_pull(edpc_ctx* dst, edpc_ctx* src) {
-  EDPC_CHECK_ARG(dst && src && dst->lay.n_shared == src->lay.n_shared, "bad contexts");
-  if (src->g_count == 0) return EDPC_OK;
+// Peer copy src -> dst of `bytes` on dst's stream, ordered after src's queued
+// work; src's later work is ordered after the copy.
+static int pull_ordered(edpc_ctx* dst, edpc_ctx* src, void* to, const void* from, size_t bytes) {
   EDPC_CUDA_TRY(cudaSetDevice(src->device));
   EDPC_CUDA_TRY(cudaEventRecord(src->ev, src->st));
   EDPC_CUDA_TRY(cudaSetDevice(dst->device));
   EDPC_CUDA_TRY(cudaStreamWaitEvent(dst->st, src->ev, 0));
-  const size_t off = (size_t)src->g_first * src->lay.n_shared;
-  const size_t bytes = (size_t)src->g_count * src->lay.n_shared * 4;
-  EDPC_CUDA_TRY(cudaMemcpyPeerAsync(dst->Gp + off, dst->device, src->Gp + off, src->device, bytes,
-                                    dst->st));
+  EDPC_CUDA_TRY(cudaMemcpyPeerAsync(to, dst->device, from, src->device, bytes, dst->st));
   EDPC_CUDA_TRY(cudaEventRecord(dst->ev, dst->st));
   EDPC_CUDA_TRY(cudaSetDevice(src->device));
   EDPC_CUDA_TRY(cudaStreamWaitEvent(src->st, dst->ev, 0));
+  return EDPC_OK;
+}
+
+static bool same_shard_set(const edpc_ctx* a, const edpc_ctx* b) {
+  return a->lay.n_shared == b->lay.n_shared && a->g_count == b->g_count && a->h16 == b->h16;
+}
+
+// Sharded-optimizer step 2 without NCCL (dist.ShardSet): dst <- src's subtree
+// sum of dst's owned parameter slice, into slot src->g_first (device to
+// device; a peer copy over NVLink when the contexts sit on different GPUs).
+int edpc_partials_pull(edpc_ctx* dst, edpc_ctx* src) {
+  EDPC_CHECK_ARG(dst && src && same_shard_set(dst, src), "bad contexts");
+  if (src == dst || shard_count(dst) < 2) return EDPC_OK;
+  int64_t off, len;
+  shard_range(dst, shard_rank(dst), &off, &len);
+  if (len <= 0) return EDPC_OK;
+  const size_t at = (size_t)src->g_first * src->lay.n_shared + (size_t)off;
+  return pull_ordered(dst, src, dst->Gp + at, src->Gp + at, (size_t)len * 4);
+}
+
+// Sharded-optimizer step 4 without NCCL: dst <- src's owned slice of the
+// updated weights (fp32 and the fp16 shadow).
+int edpc_weights_pull(edpc_ctx* dst, edpc_ctx* src) {
+  EDPC_CHECK_ARG(dst && src && same_shard_set(dst, src), "bad contexts");
+  if (src == dst || shard_count(src) < 2) return EDPC_OK;
+  int64_t off, len;
+  shard_range(src, shard_rank(src), &off, &len);
+  if (len <= 0) return EDPC_OK;
+  EDPC_TRY(pull_ordered(dst, src, dst->W + off, src->W + off, (size_t)len * 4));
+  if (src->h16) EDPC_TRY(pull_ordered(dst, src, dst->Wh + off, src->Wh + off, (size_t)len * 2));
+  return EDPC_OK;
+}
+
+int edpc_shard_range(edpc_ctx* c, int64_t* off, int64_t* len) {
+  EDPC_CHECK_ARG(c && off && len, "null argument");
+  shard_range(c, shard_rank(c), off, len);
   return EDPC_OK;
 }
 

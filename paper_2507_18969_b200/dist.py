@@ -8,11 +8,15 @@ segments are contiguous lane ranges with their own coders (`pipeline.py:66-68`).
 Partition: G ranks (G | 8, B % 8 == 0); rank r owns lanes [r*B/G, (r+1)*B/G)
 = the 8/G consecutive lane groups of the canonical gradient reduction and the
 segments inside them, their per-lane FDM state, coders and lane-matrix slice.
-Per model step each rank computes its groups' gradient partials; the
-partials are exchanged (NCCL all-gather inside the library for one process per
-GPU; device-to-device peer copies for several contexts in one process); then
-every rank runs the same canonical tree + Adam on identical inputs, so the
-trajectory -- and the container bytes -- are those of a single GPU.
+Sharded optimizer, per model step: each rank reduces its
+groups' gradient partials to one subtree sum; the shared parameters are cut
+into G slices (``shard_ranges``) and rank j's subtree sum of slice r goes to
+rank r; rank r runs the top of the canonical tree over the G subtree sums and
+Adam on its slice only; the updated weight slices are all-gathered.  (NCCL
+send/recv + all-gather inside the library for one process per GPU;
+stream-ordered peer copies for several contexts in one process.)  The tree is
+the single-GPU one, so the trajectory -- and the container bytes -- do not
+depend on G.
 """
 
 from __future__ import annotations
@@ -32,6 +36,27 @@ from .lanes import lane_len_for, validate_geometry
 from .model import DeviceContext
 
 NUM_GROUPS = 8
+
+
+def shard_ranges(n_shared: int, world: int) -> list[tuple[int, int]]:
+    """[(offset, length)] of each rank's owned shared-parameter slice; mirrors
+    ``shard_range`` in csrc/model.cu (64-aligned equal slices, last shorter)."""
+    s = -(-n_shared // world)
+    s = -(-s // 64) * 64
+    out = []
+    for r in range(world):
+        o = min(n_shared, r * s)
+        out.append((o, min(n_shared, (r + 1) * s) - o))
+    return out
+
+
+def tree_sum(parts):
+    """Pairwise tree over 1/2/4/8 leaves, the order of ``tree_sum`` in
+    csrc/kernels.cuh: 8 leaves -> ((p0+p1)+(p2+p3))+((p4+p5)+(p6+p7))."""
+    if len(parts) == 1:
+        return parts[0]
+    h = len(parts) // 2
+    return tree_sum(parts[:h]) + tree_sum(parts[h:])
 
 
 def lane_plan(cfg: ModelConfig, segments: int, world: int) -> list[tuple[int, int]]:
@@ -100,6 +125,10 @@ class ShardSet:
                     _lib.check(lib.edpc_partials_pull(dst.h, src.h))
         for c in self.ctxs:
             _lib.check(lib.edpc_step_phase(c.h, i, 1, int(decompress)))
+        for dst in self.ctxs:
+            for src in self.ctxs:
+                if src is not dst:
+                    _lib.check(lib.edpc_weights_pull(dst.h, src.h))
 
 
 def compress_multi(data: bytes, cfg: ModelConfig, segments: int, devices: list[int], *,
@@ -205,10 +234,10 @@ def torch_broadcast_id(uid):
 
 
 def bench_multi(args, wl, clocks_cls=None, peaks=None, flops_per_lane=None) -> None:
-    """bench.py at N GPUs under torchrun: weak scaling (B/N lanes per GPU is
-    fixed by the workload's per-GPU share), one NCCL all-gather of the
-    gradient partials per model step inside the captured step graph; the
-    step time is the max over ranks of CUDA-event time."""
+    """bench.py at N GPUs under torchrun: weak scaling (the single-GPU
+    workload's lanes per GPU), the sharded optimizer's two NCCL exchanges per
+    model step inside the captured step graph; the step time is the max over
+    ranks of CUDA-event time."""
     import json
 
     import torch
@@ -286,8 +315,11 @@ def bench_multi(args, wl, clocks_cls=None, peaks=None, flops_per_lane=None) -> N
                                          f"S={S}, {n >> 20} MiB (C3-style weak scaling)",
                                 lanes=cfg.lanes, segments=S,
                                 lanes_per_gpu=lc, columns_per_step=chunk,
-                                exchange="NCCL all-gather of 8 lane-group gradient partials "
-                                         "per model step (inside the step graph)"))
+                                exchange="sharded optimizer per model step, inside the step "
+                                         "graph: NCCL send/recv of subtree-sum slices "
+                                         "((G-1)/G x 19.3 MB out per GPU), G-leaf tree + Adam on "
+                                         "the owned slice, NCCL all-gather of the updated fp32 "
+                                         "weights + fp16 shadow"))
         print(json.dumps(line), flush=True)
     ctx.close()
     dist.barrier()
