@@ -23,6 +23,7 @@
 #include "common.cuh"
 #include "gemm_simt.cuh"
 #include "kernels.cuh"
+#include "lte.cuh"
 #include "tc_gemm.cuh"
 
 namespace edpc {
@@ -729,11 +730,47 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
   return EDPC_OK;
 }
 
+// Fused LTE kernels (lte.cuh): paper dims on the tcgen05 path (the SIMT
+// path keeps the reference-shaped GEMM -> FDM -> GEMM sequence).
+// Forward: on by default (ncu: 24.8 us vs 39.7 us for the three launches);
+// EDPC_LTE_FUSED=0 switches it off.  Backward: off by default -- k_lte_bwd
+// measured 96.9 us vs 91.7 us for up-dgrad + FDM-bwd/Adam + down-dgrad (its
+// CTAs run the projection phases in lockstep, leaving HBM idle meanwhile);
+// EDPC_LTE_FUSED_BWD=1 switches it on (experiments only).
+static bool lte_fused(const edpc_ctx* c, bool bwd = false) {
+  static int v = -1, vb = -1;
+  if (v < 0) {
+    const char* e = getenv("EDPC_LTE_FUSED");
+    v = (e && e[0] == '0') ? 0 : 1;
+    e = getenv("EDPC_LTE_FUSED_BWD");
+    vb = (e && e[0] == '1') ? 1 : 0;
+  }
+  if (!((bwd ? vb : v) == 1 && c->use_tc && c->lay.F == lte::kF && c->lay.FP == lte::kFP)) return false;
+  static signed char attr[64] = {};  // per device: 0 unset, 1 ok, -1 failed
+  signed char& a = attr[c->device & 63];
+  if (a == 0) {
+    a = cudaFuncSetAttribute(k_lte_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)lte::kSmemBytes) == cudaSuccess &&
+                cudaFuncSetAttribute(k_lte_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)lte::kSmemBytes) == cudaSuccess
+            ? 1
+            : -1;
+  }
+  return a == 1;
+}
+
 static int forward(edpc_ctx* c, ByteCols src) {
   const Layout& L = c->lay;
   const int Bl = c->Bl;
   MbrbBufs lb{c->x_emb, c->l_xhat, c->l_rstd, c->l_x0, c->l_H, c->l_ff, c->x_local};
   EDPC_TRY(mbrb_forward(c, L.loc, lb, true, src));
+  if (lte_fused(c)) {
+    Scope sc_(c, kRegFdmFwd, c->st);
+    pdl_launch(k_lte_fwd, (unsigned)cdiv(Bl, lte::kRows), lte::kThreads, lte::kSmemBytes, c->st,
+               c->x_local, c->W + L.down_w, c->W + L.down_b, c->U, c->W + L.up_w, c->W + L.up_b,
+               c->down, c->mixed, c->x_lte, Bl);
+    CK(cudaGetLastError());
+  } else {
   CK(fwd_linear(c, c->x_local, L.F, L.F, c->W + L.down_w, L.FP, 1, 0, c->down, 0,
                 c->W + L.down_b, nullptr, Bl));
   {
@@ -756,6 +793,7 @@ static int forward(edpc_ctx* c, ByteCols src) {
   CK(cudaGetLastError());
   CK(fwd_linear(c, c->mixed, L.FP, L.FP, c->W + L.up_w, L.F, 1, 0, c->x_lte, 0, c->W + L.up_b,
                 nullptr, Bl));
+  }
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
   EDPC_TRY(mbrb_forward(c, L.glo, gb, false, src));
   CK(fwd_linear(c, c->x_global, L.F, L.F, c->W + L.head_w, 256, 1, 0, c->logits, 0,
@@ -871,62 +909,75 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
   // LTE up
   CK(fork_aux(c));
   CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
-  CK(dgrad(c, c->g_lte, F, 1, 0, c->W + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
-  // per-lane FDM: g_down with the old U, then U's Adam step (fused: U read once)
-  {
-    if (FP == 64 || FP == 128 || FP == 256) {
-      const int lpw = 32 / std::min(32, FP / 4);
-      const unsigned blocks = (unsigned)cdiv(cdiv(Bl, lpw), kFdmWarps);
-      auto run = [&](auto kern, cudaStream_t st) {
-        Scope sc_(c, kRegFdmBwd, st);
-        pdl_launch(kern, blocks, 32 * kFdmWarps, 0, st, c->down, c->gmix, c->U, c->Um, c->Uv,
-                   c->gdown, Bl, c->si(), c->adam, c->cfg.beta1, c->cfg.beta2,
-                   ldexpf(1.0f, -c->gs_log2));
-      };
-      // split (EDPC_FDM_SPLIT=1, experiment) measured 3% slower at C2: the
-      // side-stream Adam pass competes with the main stream for HBM and U is
-      // read twice
-      const bool split = getenv("EDPC_FDM_SPLIT") && getenv("EDPC_FDM_SPLIT")[0] == '1';
-      if (FP == 64) {
-        if (split) {
-          run(k_fdm_bwd_adam_v<64, true, false>, c->st);
-          CK(fork_aux(c));
-          run(k_fdm_bwd_adam_v<64, false, true>, c->st_aux);
+  if (lte_fused(c, true)) {  // up dgrad + FDM backward/Adam + down dgrad, one kernel
+    {
+      Scope sc_(c, kRegFdmBwd, c->st);
+      pdl_launch(k_lte_bwd, (unsigned)cdiv(Bl, lte::kRows), lte::kThreads, lte::kSmemBytes, c->st,
+                 c->g_lte, c->W + L.up_w, c->down, c->U, c->Um, c->Uv, c->W + L.down_w, c->gdown,
+                 c->g_loc, c->h16 ? c->guph_l : nullptr, Bl, c->si(), c->adam, c->cfg.beta1,
+                 c->cfg.beta2, ldexpf(1.0f, -c->gs_log2));
+    }
+    CK(cudaGetLastError());
+    CK(fork_aux(c));
+    CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
+  } else {
+    CK(dgrad(c, c->g_lte, F, 1, 0, c->W + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
+    // per-lane FDM: g_down with the old U, then U's Adam step (fused: U read once)
+    {
+      if (FP == 64 || FP == 128 || FP == 256) {
+        const int lpw = 32 / std::min(32, FP / 4);
+        const unsigned blocks = (unsigned)cdiv(cdiv(Bl, lpw), kFdmWarps);
+        auto run = [&](auto kern, cudaStream_t st) {
+          Scope sc_(c, kRegFdmBwd, st);
+          pdl_launch(kern, blocks, 32 * kFdmWarps, 0, st, c->down, c->gmix, c->U, c->Um, c->Uv,
+                     c->gdown, Bl, c->si(), c->adam, c->cfg.beta1, c->cfg.beta2,
+                     ldexpf(1.0f, -c->gs_log2));
+        };
+        // split (EDPC_FDM_SPLIT=1, experiment) measured 3% slower at C2: the
+        // side-stream Adam pass competes with the main stream for HBM and U is
+        // read twice
+        const bool split = getenv("EDPC_FDM_SPLIT") && getenv("EDPC_FDM_SPLIT")[0] == '1';
+        if (FP == 64) {
+          if (split) {
+            run(k_fdm_bwd_adam_v<64, true, false>, c->st);
+            CK(fork_aux(c));
+            run(k_fdm_bwd_adam_v<64, false, true>, c->st_aux);
+          } else {
+            run(k_fdm_bwd_adam_v<64>, c->st);
+          }
+        } else if (FP == 128) {
+          if (split) {
+            run(k_fdm_bwd_adam_v<128, true, false>, c->st);
+            CK(fork_aux(c));
+            run(k_fdm_bwd_adam_v<128, false, true>, c->st_aux);
+          } else {
+            run(k_fdm_bwd_adam_v<128>, c->st);
+          }
         } else {
-          run(k_fdm_bwd_adam_v<64>, c->st);
-        }
-      } else if (FP == 128) {
-        if (split) {
-          run(k_fdm_bwd_adam_v<128, true, false>, c->st);
-          CK(fork_aux(c));
-          run(k_fdm_bwd_adam_v<128, false, true>, c->st_aux);
-        } else {
-          run(k_fdm_bwd_adam_v<128>, c->st);
+          if (split) {
+            run(k_fdm_bwd_adam_v<256, true, false>, c->st);
+            CK(fork_aux(c));
+            run(k_fdm_bwd_adam_v<256, false, true>, c->st_aux);
+          } else {
+            run(k_fdm_bwd_adam_v<256>, c->st);
+          }
         }
       } else {
-        if (split) {
-          run(k_fdm_bwd_adam_v<256, true, false>, c->st);
-          CK(fork_aux(c));
-          run(k_fdm_bwd_adam_v<256, false, true>, c->st_aux);
-        } else {
-          run(k_fdm_bwd_adam_v<256>, c->st);
-        }
+        Scope sc_(c, kRegFdmBwd, c->st);
+        pdl_launch(k_fdm_bwd_adam, (unsigned)cdiv(Bl, 8), 256, 0, c->st, 
+            c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, FP, Bl, c->si(), c->adam,
+            c->cfg.beta1, c->cfg.beta2, ldexpf(1.0f, -c->gs_log2));
       }
-    } else {
-      Scope sc_(c, kRegFdmBwd, c->st);
-      pdl_launch(k_fdm_bwd_adam, (unsigned)cdiv(Bl, 8), 256, 0, c->st, 
-          c->down, c->gmix, c->U, c->Um, c->Uv, c->gdown, FP, Bl, c->si(), c->adam,
-          c->cfg.beta1, c->cfg.beta2, ldexpf(1.0f, -c->gs_log2));
     }
+    CK(cudaGetLastError());
+    // LTE down
+    CK(fork_aux(c));
+    CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
+    if (c->h16)
+      CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore2{c->g_loc, c->guph_l, F}));
+    else
+      CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore{c->g_loc, F}));
   }
-  CK(cudaGetLastError());
-  // LTE down
-  CK(fork_aux(c));
-  CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
-  if (c->h16)
-    CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore2{c->g_loc, c->guph_l, F}));
-  else
-    CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore{c->g_loc, F}));
   if (early_adam(c)) {  // LTE down + up
     CK(fork_aux(c));
     EDPC_TRY(adam_range(c, L.down_w, L.glo.ln_g - L.down_w, c->st_aux));
@@ -934,6 +985,10 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
   // local MBRB: d(x_local) -> d(x_emb) (gradient w.r.t. the embedded context)
   MbrbBufs lb{c->x_emb, c->l_xhat, c->l_rstd, c->l_x0, c->l_H, c->l_ff, c->x_local};
   EDPC_TRY(mbrb_backward(c, L.loc, lb, c->g_loc, c->g_emb, c->GH_l, c->guph_l));
+  if (early_adam(c)) {  // local MBRB: gradients complete; overlaps the embedding scatter-add
+    CK(fork_aux(c));
+    EDPC_TRY(adam_range(c, L.loc.ln_g, L.down_w - L.loc.ln_g, c->st_aux));
+  }
   // embedding scatter-add as per-group partials
   if (c->n_chunks > 0) {
     {
@@ -1022,10 +1077,10 @@ static int adam_range(edpc_ctx* c, int64_t off, int64_t len, cudaStream_t st, in
 }
 
 // Early Adam: with all 8 lane groups in this context (no exchange before the
-// optimizer), the global-MBRB weights + head and the LTE projections are
-// updated on the side stream as soon as their gradients are complete and the
-// main stream has finished reading them; only the embedding and the local
-// MBRB are left for the end of the step.
+// optimizer), the global-MBRB weights + head, the LTE projections and the
+// local MBRB are updated on the side stream as soon as their gradients are
+// complete and the main stream has finished reading them; only the embedding
+// (256 x d_e parameters) is left for the end of the step.
 static bool early_adam(const edpc_ctx* c) {
   return c->g_count == kNumGroups && !c->comm && aux_enabled();
 }
@@ -1059,7 +1114,7 @@ static int adam_shared(edpc_ctx* c) {
     shard_range(c, shard_rank(c), &off, &len);
     return adam_range(c, off, len, c->st, G, (int64_t)c->g_count * L.n_shared);
   }
-  if (early_adam(c)) return adam_range(c, 0, L.down_w, c->st);  // embedding + local MBRB
+  if (early_adam(c)) return adam_range(c, 0, L.loc.ln_g, c->st);  // the embedding
   return adam_range(c, 0, L.n_shared, c->st);
 }
 
