@@ -221,7 +221,7 @@ k_lte_bwd(const float* __restrict__ g_lte, const float* __restrict__ Wu,
   const int b0 = blockIdx.x * kRows;
   pdl_entry();
   float bc1, bc2;
-  adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
+  adam_bc(c, b1d, b2d, si.T(), bc1, bc2);
   stage(Ws, kLdWuB, Wu, kFP, kF);
   stage_rows(Gs, kLdX, g_lte, kF, b0, Bl);
   stage_rows(DNs, kLdS, down, kFP, b0, Bl);

@@ -306,7 +306,8 @@ struct edpc_ctx {
     return EDPC_OK;
   }
 
-  StepIdx si() const { return StepIdx{d_i, d_t}; }
+  int step_off = 0;  // model steps since d_i / d_t were last advanced (inside a graph capture)
+  StepIdx si() const { return StepIdx{d_i, d_t, step_off}; }
   ByteCols lanes_src() const { return ByteCols{mat, L}; }
   ByteCols seam_src() const { return ByteCols{scratch, (int64_t)lay.T + 1}; }
 };
@@ -421,6 +422,23 @@ static cudaError_t splitk_reduce(edpc_ctx* c, int N, const float* bias, const fl
   return cudaGetLastError();
 }
 
+// one split-K GEMM into out (+ bias) (+ resid): EpiSplit partials + k_splitk_reduce.
+// (Reducing inside the GEMM -- the last CTA of a tile, or all of a tile's CTAs
+// after a wait -- measured slower at C2: 7.35 / 7.74 vs 8.14 MB/s; CTAs that
+// stay resident to reduce hold SMs the side-stream weight-gradient GEMMs need.)
+template <bool AMN, bool BMN, bool H = false>
+static cudaError_t split_gemm(edpc_ctx* c, const TcShape& s, const TcOperand& a, const TcOperand& b,
+                              const float* bias, const float* resid, float* out) {
+  const int N = s.N;
+  const int64_t plane = (int64_t)c->Bl * N;
+  {
+    Scope sc(c, kRegGemm, c->st);
+    int st = tc_gemm<AMN, BMN, H>(s, a, b, EpiSplit{c->ws, N, plane}, c->st);
+    if (st != EDPC_OK) return cudaErrorUnknown;
+  }
+  return splitk_reduce(c, N, bias, resid, out);
+}
+
 // out[Bl][N] = A[Bl][Kd] . W[Kd][N] (+ bias) over nzb batches (weights at
 // w + z*sW, bias at bias + z*sW, out at out + z*sOut)
 static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, const float* w,
@@ -430,12 +448,7 @@ static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, cons
     TcOperand a{A, lda, 0, 1}, b{w, N, sW, nzb};
     if (nzb == 1 && M == c->Bl && use_split(N, Kd, Kd)) {
       TcShape s{M, N, Kd, 1, 1, kBatchNone, kBatchNone, 2, kSplitK, 0, 0, 0};
-      {
-        Scope sc(c, kRegGemm, c->st);
-        int st = tc_gemm<false, true>(s, a, b, EpiSplit{c->ws, N, (int64_t)M * N}, c->st);
-        if (st != EDPC_OK) return cudaErrorUnknown;
-      }
-      return splitk_reduce(c, N, bias, resid, out);
+      return split_gemm<false, true>(c, s, a, b, bias, resid, out);
     }
     Scope sc(c, kRegGemm, c->st);
     TcShape s{M, N, Kd, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 0, 1, 0, 0, 0};
@@ -557,12 +570,7 @@ static cudaError_t dgrad(edpc_ctx* c, const float* G, int Kd, int nsum, int64_t 
       if (epi.ldc == N && use_split(N, (int64_t)Kd * nsum, Kd)) {
         TcShape s{c->Bl, N, Kd, 1, nsum, nsum > 1 ? kBatchSum : kBatchNone,
                   nsum > 1 ? kBatchSum : kBatchNone, 2, kSplitK, 0, 0, 0};
-        {
-          Scope sc(c, kRegGemm, c->st);
-          int st = tc_gemm<false, false>(s, a, b, EpiSplit{c->ws, N, (int64_t)c->Bl * N}, c->st);
-          if (st != EDPC_OK) return cudaErrorUnknown;
-        }
-        return splitk_reduce(c, N, nullptr, nullptr, epi.C);
+        return split_gemm<false, false>(c, s, a, b, nullptr, nullptr, epi.C);
       }
     }
     Scope sc(c, kRegGemm, c->st);
@@ -601,12 +609,7 @@ static cudaError_t fwd_linear_h(edpc_ctx* c, const __half* A, int Kd, const __ha
   TcOperand a{A, Kd, 0, 1}, b{w, N, 0, 1};
   if (N <= 256 && N % 4 == 0 && Kd >= 1024 && Kd % (kSplitK * tc_bk<true>()) == 0) {
     TcShape s{M, N, Kd, 1, 1, kBatchNone, kBatchNone, 2, kSplitK, 0, 0, 0};
-    {
-      Scope sc(c, kRegGemm, c->st);
-      int st = tc_gemm<false, true, true>(s, a, b, EpiSplit{c->ws, N, (int64_t)M * N}, c->st);
-      if (st != EDPC_OK) return cudaErrorUnknown;
-    }
-    return splitk_reduce(c, N, bias, resid, out);
+    return split_gemm<false, true, true>(c, s, a, b, bias, resid, out);
   }
   Scope sc(c, kRegGemm, c->st);
   TcShape s{M, N, Kd, 1, 1, kBatchNone, kBatchNone, 0, 1, 0, 0, 0};
@@ -623,12 +626,7 @@ static cudaError_t dgrad_h(edpc_ctx* c, const __half* G, int Kd, int nsum, int64
   if (N <= 256 && N % 4 == 0 && (int64_t)Kd * nsum >= 1024 &&
       Kd % (kSplitK * tc_bk<true>()) == 0) {
     TcShape s{c->Bl, N, Kd, 1, nsum, bt, bt, 2, kSplitK, 0, 0, 0};
-    {
-      Scope sc(c, kRegGemm, c->st);
-      int st = tc_gemm<false, false, true>(s, a, b, EpiSplit{c->ws, N, (int64_t)c->Bl * N}, c->st);
-      if (st != EDPC_OK) return cudaErrorUnknown;
-    }
-    return splitk_reduce(c, N, nullptr, nullptr, out);
+    return split_gemm<false, false, true>(c, s, a, b, nullptr, nullptr, out);
   }
   Scope sc(c, kRegGemm, c->st);
   TcShape s{c->Bl, N, Kd, 1, nsum, bt, bt, 0, 1, 0, 0, 0};
@@ -1169,8 +1167,10 @@ static int optimizer_step(edpc_ctx* c) {
   return EDPC_OK;
 }
 
-// One model step at lane column i (already in d_i / d_t).
-static int model_step(edpc_ctx* c, int mode) {
+// One model step at lane column d_i + step_off (Adam count d_t + step_off);
+// advance > 0: the step ends by moving d_i / d_t on by `advance` (a captured
+// graph of kGraphSteps steps advances once, by kGraphSteps, at its end).
+static int model_step(edpc_ctx* c, int mode, int advance = 1) {
   ByteCols src = c->lanes_src();
   EDPC_TRY(forward(c, src));
   EDPC_TRY(softmax_quant(c, mode, src));
@@ -1183,9 +1183,9 @@ static int model_step(edpc_ctx* c, int mode) {
   }
   EDPC_TRY(backward(c, src, nullptr, mode == kEncode));
   EDPC_TRY(optimizer_step(c));
-  {
+  if (advance > 0) {
     Scope sc_(c, kRegElem, c->st);
-    pdl_launch(k_step_advance, 1, 1, 0, c->st, c->d_i, c->d_t);
+    pdl_launch(k_step_advance, 1, 1, 0, c->st, c->d_i, c->d_t, advance);
   }
   CK(cudaGetLastError());
   return EDPC_OK;
@@ -1213,7 +1213,11 @@ static int run_model_steps(edpc_ctx* c, int64_t n, int mode) {
       cudaGraph_t g = nullptr;
       CK(cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal));
       int st = EDPC_OK;
-      for (int k = 0; k < kGraphSteps && st == EDPC_OK; ++k) st = model_step(c, mode);
+      for (int k = 0; k < kGraphSteps && st == EDPC_OK; ++k) {
+        c->step_off = k;
+        st = model_step(c, mode, k == kGraphSteps - 1 ? kGraphSteps : 0);
+      }
+      c->step_off = 0;
       cudaError_t e = cudaStreamEndCapture(c->st, &g);
       if (st != EDPC_OK) {
         if (g) cudaGraphDestroy(g);

@@ -173,3 +173,34 @@ def test_ratio_within_half_percent_of_reference_run(name):
     blob = write_container(compress(data, cfg, ref["segments"]))
     assert abs((len(data) / len(blob)) / ref["ratio"] - 1) <= RATIO_TOL
     assert decompress(read_container(blob)) == data
+
+
+def test_cli_round_trip_and_metrics(tmp_path):
+    """compress -> verify -> decompress through the CLI (reference cli.py
+    flow), a corrupted payload bit -> verify mismatch (exit 1) or a coder
+    error, and `bench` over a two-file corpus."""
+    import json as _json
+
+    from paper_2507_18969_b200 import cli
+    from paper_2507_18969_b200 import synth as _synth
+
+    data = _synth.generate("text", 50_000, 4)
+    src, enc, out, mfile = (tmp_path / n for n in ("in.bin", "in.edpc", "out.bin", "m.jsonl"))
+    src.write_bytes(data)
+    flags = ["--profile", "desk", "--lanes", "32", "--segments", "8"]
+    assert cli.main(["compress", "-i", str(src), "-o", str(enc), "--metrics-out", str(mfile),
+                     *flags]) == cli.EXIT_OK
+    m = _json.loads(mfile.read_text().splitlines()[-1])
+    assert m["original_bytes"] == len(data) and m["compressed_bytes"] == enc.stat().st_size
+    assert m["ratio"] > 1.0 and m["mb_per_s"] > 0
+    assert cli.main(["verify", "-i", str(src), "-c", str(enc)]) == cli.EXIT_OK
+    assert cli.main(["decompress", "-i", str(enc), "-o", str(out), "--devices", "0"]) == cli.EXIT_OK
+    assert out.read_bytes() == data
+    other = tmp_path / "other.bin"
+    other.write_bytes(data[:-1] + bytes([data[-1] ^ 1]))
+    assert cli.main(["verify", "-i", str(other), "-c", str(enc)]) == cli.EXIT_MISMATCH
+    corpus = tmp_path / "corpus"
+    corpus.mkdir()
+    (corpus / "a.txt").write_bytes(data[:20_000])
+    (corpus / "b.bin").write_bytes(_synth.generate("image", 20_000, 1))
+    assert cli.main(["bench", "-i", str(corpus), *flags]) == cli.EXIT_OK
