@@ -23,6 +23,9 @@ struct ByteCols {
 struct StepIdx {
   const int64_t* i;  // current lane column (device)
   const int64_t* t;  // Adam step count (device), model.py:230
+  int off;           // steps past (*i, *t): position inside a captured multi-step graph
+  __device__ __forceinline__ int64_t I() const { return *i + off; }
+  __device__ __forceinline__ int64_t T() const { return *t + off; }
 };
 
 // GeLU and its derivative together (_kernels.py:35-51, exact-erf GeLU):
@@ -75,7 +78,7 @@ k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE,
   if (F > kLnRowMax) {  // generic path (rows longer than the register tile)
     float s = 0.f;
     if (kGather) {
-      const int64_t col0 = *si.i - T;
+      const int64_t col0 = si.I() - T;
       const uint8_t* row = src.base + (int64_t)b * src.ld + col0;
       for (int f = lane; f < F; f += 32) {
         int p = f / DE, d = f - p * DE;
@@ -111,7 +114,7 @@ k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE,
   constexpr int kJ = kLnRowMax / 32;
   float v[kJ];
   if (kGather) {
-    const int64_t col0 = *si.i - T;
+    const int64_t col0 = si.I() - T;
     const uint8_t* row = src.base + (int64_t)b * src.ld + col0;
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
@@ -730,7 +733,7 @@ k_fdm_bwd_adam(const float* __restrict__ down, const float* __restrict__ gmix,
   const int lane = threadIdx.x & 31;
   if (b >= Bl) return;
   float bc1, bc2;
-  adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
+  adam_bc(c, b1d, b2d, si.T(), bc1, bc2);
   const float* d = down + (int64_t)b * FP;
   const float* gm = gmix + (int64_t)b * FP;
   const int64_t base = (int64_t)b * FP * FP;
@@ -817,7 +820,7 @@ k_fdm_bwd_adam_v(const float* __restrict__ down, const float* __restrict__ gmix,
   const bool live = b < Bl;
   const int bb = live ? b : 0;
   float bc1 = 0.f, bc2 = 0.f;
-  if (ADAM) adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
+  if (ADAM) adam_bc(c, b1d, b2d, si.T(), bc1, bc2);
   const float* d = down + (int64_t)bb * FP;
   const float4* gm4 = reinterpret_cast<const float4*>(gmix + (int64_t)bb * FP);
   float4 g[G::kNV];
@@ -912,7 +915,7 @@ k_embed_grad_chunks(ByteCols src, StepIdx si, int T, int DE, int F,
   const int lb = chunk_tab[3 * k + 1], le = chunk_tab[3 * k + 2];
   const int nl = le - lb;
   const int n = nl * T;
-  const int64_t col0 = *si.i - T;
+  const int64_t col0 = si.I() - T;
   for (int e = tid; e < n; e += blockDim.x) {
     int bl = e / T, p = e - bl * T;
     cbytes[e] = src.base[(int64_t)(lb + bl) * src.ld + col0 + p];
@@ -1053,7 +1056,7 @@ __global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, floa
                               __half* __restrict__ Wh) {
   pdl_entry();
   float bc1, bc2;
-  adam_bc(c, b1d, b2d, *si.t, bc1, bc2);
+  adam_bc(c, b1d, b2d, si.T(), bc1, bc2);
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     float q[NL];
@@ -1131,7 +1134,7 @@ k_softmax_quant(const float* __restrict__ logits, float* __restrict__ probs, int
   warp_quantize<false>(p, freq);
   uint32_t cum[8];
   warp_cdf(freq, cum);
-  const int64_t i = *si.i;
+  const int64_t i = si.I();
   if (kMode == kEncode) {
     const int tgt = src.base[(int64_t)b * src.ld + i];
     if (g) {  // the loss gradient, fused (k_dlogits' exact arithmetic; the target is known)
@@ -1174,7 +1177,7 @@ __global__ void k_dlogits(const float* __restrict__ probs, ByteCols src, StepIdx
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= (int64_t)Bl * 256) return;
   const int b = (int)(e >> 8), v = (int)(e & 255);
-  const int tgt = src.base[(int64_t)b * src.ld + *si.i];
+  const int tgt = src.base[(int64_t)b * src.ld + si.I()];
   float p = probs[e];
   if (v == tgt) {
     if (nll) nll[b] = -logf(p);
@@ -1269,7 +1272,7 @@ __global__ void k_decode_column(uint8_t* __restrict__ mat, int64_t L, StepIdx si
   const int s = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (s >= Sl) return;
-  const int64_t i = *si.i;
+  const int64_t i = si.I();
   int64_t* stp = dec_state + 4 * s;
   const bool dead = err[s] != 0;
   DecState st{(uint64_t)stp[0], (uint64_t)stp[1], (uint64_t)stp[2], stp[3]};
@@ -1390,10 +1393,10 @@ __global__ void k_splitk_reduce(const float* __restrict__ ws, int nsplit, int64_
   *reinterpret_cast<float4*>(out + e) = a;
 }
 
-__global__ void k_step_advance(int64_t* i, int64_t* t) {
+__global__ void k_step_advance(int64_t* i, int64_t* t, int n) {
   pdl_entry();
-  *i += 1;
-  *t += 1;
+  *i += n;
+  *t += n;
 }
 
 }  // namespace edpc
