@@ -525,18 +525,33 @@ k_ln_bwd_fused(const float* __restrict__ gx0, const float* __restrict__ xhat,
   float gn[kJ];
 #pragma unroll
   for (int j = 0; j < kJ; ++j) gn[j] = lane + 32 * j < F ? gain[lane + 32 * j] : 0.f;
-  for (int b = lb + warp; b < le; b += 8) {
+  // rows b = lb + warp, +8, ... (kLnChunk / 8 = 2 per warp): both rows' loads
+  // in flight before the first is used (one DRAM round trip, not two)
+  static_assert(kLnChunk == 16, "two rows per warp");
+  float gxv2[2][kJ], xhv2[2][kJ], upv2[2][kJ], r2[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int b = lb + warp + 8 * q;
     const int64_t o = (int64_t)b * F;
-    // the row's loads all in flight first, kept in registers for both passes
-    float gxv[kJ], xhv[kJ], upv[kJ];
+    r2[q] = b < le ? rstd[b] : 0.f;
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
       const int f = lane + 32 * j;
-      gxv[j] = f < F ? gx0[o + f] : 0.f;
-      xhv[j] = f < F ? xhat[o + f] : 0.f;
-      upv[j] = f < F ? up[o + f] : 0.f;
+      const bool ok = b < le && f < F;
+      gxv2[q][j] = ok ? gx0[o + f] : 0.f;
+      xhv2[q][j] = ok ? xhat[o + f] : 0.f;
+      upv2[q][j] = ok ? up[o + f] : 0.f;
     }
-    const float r = rstd[b];
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int b = lb + warp + 8 * q;
+    if (b >= le) break;
+    const int64_t o = (int64_t)b * F;
+    const float* gxv = gxv2[q];
+    const float* xhv = xhv2[q];
+    const float* upv = upv2[q];
+    const float r = r2[q];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int j = 0; j < kJ; ++j) {
@@ -584,11 +599,25 @@ k_ln_bwd_fused(const float* __restrict__ gx0, const float* __restrict__ xhat,
   __threadfence();
   const float* all = scratch + (int64_t)blockIdx.y * nchunk * 2 * F;
   for (int f = threadIdx.x; f < F; f += blockDim.x) {
-    float a = all[f], c = all[F + f];
-#pragma unroll 8  // the loads are independent: keep 8 in flight (this tail is L2-latency bound)
-    for (int k = 1; k < nchunk; ++k) {
-      a += all[(int64_t)k * 2 * F + f];
-      c += all[(int64_t)k * 2 * F + F + f];
+    // this tail is L2-latency bound: up to 32 chunks' loads issued at once
+    // (one round trip), then summed in chunk order
+    constexpr int kMaxCh = 32;
+    float va[kMaxCh], vc[kMaxCh];
+#pragma unroll
+    for (int k = 0; k < kMaxCh; ++k) {
+      va[k] = k < nchunk ? __ldcg(all + (int64_t)k * 2 * F + f) : 0.f;
+      vc[k] = k < nchunk ? __ldcg(all + (int64_t)k * 2 * F + F + f) : 0.f;
+    }
+    float a = va[0], c = vc[0];
+#pragma unroll
+    for (int k = 1; k < kMaxCh; ++k)
+      if (k < nchunk) {
+        a += va[k];
+        c += vc[k];
+      }
+    for (int k = kMaxCh; k < nchunk; ++k) {
+      a += __ldcg(all + (int64_t)k * 2 * F + f);
+      c += __ldcg(all + (int64_t)k * 2 * F + F + f);
     }
     partials[(int64_t)gg * n_shared + off_g + f] = a;
     partials[(int64_t)gg * n_shared + off_b + f] = c;
