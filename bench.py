@@ -2,7 +2,7 @@
 """EDPC hot-path benchmark on B200 (contract: one JSON line from rank 0).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload c2|c4a|c4b|c3] [--chunk COLS]
+                    [--workload c2|c4a|c4b|c3|c5] [--chunk COLS]
 
 Workload (default ``c2``, BASELINE.json configs[1]): 64 MiB synthetic
 text-like stream (PCG64 seed 0), the reference default model (t16 d_e16
@@ -66,6 +66,10 @@ WORKLOADS = {
                 model=dict(PAPER, lte_ratio=1), desc="C4b: as C2 with full-width LTE (F'=F)"),
     "c3": dict(kind="mixed", nbytes=1 << 30, seed=0, lanes=32768, segments=1024, model=PAPER,
                desc="C3: 1 GiB mixed text/image stream, B=32768, S=1024 (lanes sharded over GPUs)"),
+    "c5": dict(kind="mixed", nbytes=1 << 30, seed=0, lanes=32768, segments=1024,
+               model=dict(PAPER, context_len=32, hidden_local=4096, hidden_global=8192),
+               desc="C5: scaled EDPC (t=32, F=512, F'=128, h 4096/8192), 1 GiB mixed stream, "
+                    "B=32768, S=1024, online adaptation (lanes sharded over GPUs)"),
 }
 METRIC = "compress/decompress MB/s at 1/2/4/8 B200 + bits/byte vs CPU ref"
 

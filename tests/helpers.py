@@ -14,6 +14,9 @@ DESK = dict(context_len=16, embed_dim=8, hidden_local=256, hidden_global=512, lt
             branches=2)
 PAPER = dict(context_len=16, embed_dim=16, hidden_local=2048, hidden_global=4096, lte_ratio=4,
              branches=2)
+# BASELINE.json config 5 (scaled EDPC)
+SCALED = dict(context_len=32, embed_dim=16, hidden_local=4096, hidden_global=8192, lte_ratio=4,
+              branches=2)
 
 
 def tiny_cfg(**kw):

@@ -11,7 +11,7 @@ import pytest
 from oracle.model import OracleModel
 from paper_2507_18969_b200 import EdpcModel, ModelConfig
 from paper_2507_18969_b200.init import init_params_f32
-from helpers import PAPER, TINY, TOY, DESK, tiny_cfg
+from helpers import PAPER, SCALED, TINY, TOY, DESK, tiny_cfg
 
 pytestmark = pytest.mark.gpu
 PROB_TOL = 1e-3
@@ -58,6 +58,25 @@ def test_paper_dims_predict_matches_oracle_at_init():
     g.train_step(cg, tg)
     o.train_step(co, tg)
     ctx2 = rng.integers(0, 256, size=(64, 16))
+    assert np.abs(g.predict(ctx2)[0] - o.predict(ctx2)[0]).max() <= PROB_TOL
+
+
+@pytest.mark.parametrize("lanes", [64, 1024])
+def test_scaled_dims_predict_matches_oracle(lanes):
+    """BASELINE config 5's scaled model (t = 32, F = 512, F' = 128, h 4096 /
+    8192): fp32 SIMT path (64 lanes) and tcgen05 + fp16-MBRB path (1024
+    lanes) against the fp64 oracle at init and after one online update."""
+    cfg = ModelConfig(**SCALED, lanes=lanes)
+    g, o = _pair(cfg)
+    rng = np.random.default_rng(5)
+    ctx = rng.integers(0, 256, size=(lanes, cfg.context_len))
+    pg, cg = g.predict(ctx)
+    po, co = o.predict(ctx)
+    assert np.abs(pg - po).max() <= PROB_TOL
+    tg = rng.integers(0, 256, size=lanes)
+    g.train_step(cg, tg)
+    o.train_step(co, tg)
+    ctx2 = rng.integers(0, 256, size=(lanes, cfg.context_len))
     assert np.abs(g.predict(ctx2)[0] - o.predict(ctx2)[0]).max() <= PROB_TOL
 
 
