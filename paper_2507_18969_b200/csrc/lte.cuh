@@ -42,6 +42,15 @@ constexpr int kWFloats = kF * kLdWdF;  // the largest of the four
 static_assert(kWFloats >= kFP * kLdWuF && kWFloats >= kFP * kLdWuB && kWFloats >= kF * kLdWdB);
 constexpr int kSmemFloats = kRows * kLdX + kWFloats + 3 * kRows * kLdS;
 constexpr size_t kSmemBytes = (size_t)kSmemFloats * 4;
+// forward: the weights pass through shared memory in halves (W_down by K rows,
+// W_up by N columns) -- 62 KB per CTA, 3 CTAs / SM instead of 2 (ncu: the
+// FDM phase was latency-bound at 25% occupancy, r01_ncu_lte_fwd.md).  The
+// MMA sequence per output tile is unchanged, so results are bit-identical.
+constexpr int kLdWuF2 = kF / 2 + 8;  // W_up column half [64][128]
+constexpr int kWFloatsF = (kF / 2) * kLdWdF;
+static_assert(kWFloatsF >= kFP * kLdWuF2);
+constexpr int kSmemFloatsF = kRows * kLdX + kWFloatsF + 2 * kRows * kLdS;
+constexpr size_t kSmemBytesF = (size_t)kSmemFloatsF * 4;
 
 __device__ __forceinline__ void cp_async16(float* smem, const float* gmem) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -73,6 +82,16 @@ __device__ __forceinline__ void stage(float* dst, int ld, const float* src, int 
   for (int e = threadIdx.x; e < rows * c4; e += kThreads) {
     const int r = e / c4, q = e - r * c4;
     cp_async16(dst + r * ld + q * 4, src + (int64_t)r * cols + q * 4);
+  }
+}
+
+// rows x cols block of a row-major source with row stride src_ld -> shared
+__device__ __forceinline__ void stage_ld(float* dst, int ld, const float* src, int src_ld, int rows,
+                                        int cols) {
+  const int c4 = cols / 4;
+  for (int e = threadIdx.x; e < rows * c4; e += kThreads) {
+    const int r = e / c4, q = e - r * c4;
+    cp_async16(dst + r * ld + q * 4, src + (int64_t)r * src_ld + q * 4);
   }
 }
 
@@ -128,7 +147,7 @@ struct Frag {
 // down = x_local W_d + b_d; mixed_b = down_b U_b; x_lte = mixed W_u + b_u.
 // Also stores down and mixed (operands of the FDM backward and of the
 // weight-gradient GEMMs).
-__global__ void __launch_bounds__(lte::kThreads, 2)
+__global__ void __launch_bounds__(lte::kThreads, 3)
 k_lte_fwd(const float* __restrict__ x_local, const float* __restrict__ Wd,
           const float* __restrict__ bd, const float* __restrict__ U, const float* __restrict__ Wu,
           const float* __restrict__ bu, float* __restrict__ down, float* __restrict__ mixed,
@@ -137,19 +156,25 @@ k_lte_fwd(const float* __restrict__ x_local, const float* __restrict__ Wd,
   extern __shared__ float4 lte_smem4[];
   float* Xs = reinterpret_cast<float*>(lte_smem4);
   float* Ws = Xs + kRows * kLdX;
-  float* Ds = Ws + kWFloats;
+  float* Ds = Ws + kWFloatsF;
   float* Ms = Ds + kRows * kLdS;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int b0 = blockIdx.x * kRows;
   pdl_entry();  // x_local and the weights come from the previous kernels
-  stage(Ws, kLdWdF, Wd, kF, kFP);
+  stage(Ws, kLdWdF, Wd, kF / 2, kFP);  // W_down rows [0, 128)
   stage_rows(Xs, kLdX, x_local, kF, b0, Bl);
   cp_async_commit();
   cp_async_wait_all();
   __syncthreads();
-  {  // down projection: warp w -> columns [8w, 8w + 8)
+  {  // down projection: warp w -> columns [8w, 8w + 8), K in two halves
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    warp_tile<kF, true>(acc, Xs, kLdX, Ws, kLdWdF, warp * 8);
+    warp_tile<kF / 2, true>(acc, Xs, kLdX, Ws, kLdWdF, warp * 8);
+    __syncthreads();
+    stage(Ws, kLdWdF, Wd + (kF / 2) * kFP, kF / 2, kFP);  // W_down rows [128, 256)
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    warp_tile<kF / 2, true>(acc, Xs + kF / 2, kLdX, Ws, kLdWdF, warp * 8);
     const Frag f(warp * 8);
     const float q0 = bd[f.c0], q1 = bd[f.c0 + 1];
     const float2 lo = make_float2(acc[0] + q0, acc[1] + q1), hi = make_float2(acc[2] + q0, acc[3] + q1);
@@ -160,7 +185,7 @@ k_lte_fwd(const float* __restrict__ x_local, const float* __restrict__ Wd,
       *reinterpret_cast<float2*>(down + (int64_t)(b0 + f.r0 + 8) * kFP + f.c0) = hi;
   }
   __syncthreads();  // W_d no longer read; down complete
-  stage(Ws, kLdWuF, Wu, kFP, kF);  // lands while the FDM step streams U
+  stage_ld(Ws, kLdWuF2, Wu, kF, kFP, kF / 2);  // W_up columns [0, 128), lands while the FDM step streams U
   cp_async_commit();
   {  // per-lane FDM: 16 threads per lane, float4 columns, 16 rows of U in flight
     const int r = tid >> 4, t = tid & 15, b = b0 + r;
@@ -185,9 +210,16 @@ k_lte_fwd(const float* __restrict__ x_local, const float* __restrict__ Wd,
   __syncthreads();
 #pragma unroll 1
   for (int j = 0; j < kF / 64; ++j) {  // up projection: warp w -> column tiles w, w+8, ...
+    if (j == 2) {  // second column half of W_up
+      __syncthreads();
+      stage_ld(Ws, kLdWuF2, Wu + kF / 2, kF, kFP, kF / 2);
+      cp_async_commit();
+      cp_async_wait_all();
+      __syncthreads();
+    }
     const int n0 = (warp + 8 * j) * 8;
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    warp_tile<kFP, true>(acc, Ms, kLdS, Ws, kLdWuF, n0);
+    warp_tile<kFP, true>(acc, Ms, kLdS, Ws + (j >= 2 ? -(kF / 2) : 0), kLdWuF2, n0);
     const Frag f(n0);
     const float q0 = bu[f.c0], q1 = bu[f.c0 + 1];
     if (b0 + f.r0 < Bl)

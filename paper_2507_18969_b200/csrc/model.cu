@@ -748,7 +748,7 @@ static bool lte_fused(const edpc_ctx* c, bool bwd = false) {
   signed char& a = attr[c->device & 63];
   if (a == 0) {
     a = cudaFuncSetAttribute(k_lte_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)lte::kSmemBytes) == cudaSuccess &&
+                             (int)lte::kSmemBytesF) == cudaSuccess &&
                 cudaFuncSetAttribute(k_lte_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      (int)lte::kSmemBytes) == cudaSuccess
             ? 1
@@ -764,7 +764,7 @@ static int forward(edpc_ctx* c, ByteCols src) {
   EDPC_TRY(mbrb_forward(c, L.loc, lb, true, src));
   if (lte_fused(c)) {
     Scope sc_(c, kRegFdmFwd, c->st);
-    pdl_launch(k_lte_fwd, (unsigned)cdiv(Bl, lte::kRows), lte::kThreads, lte::kSmemBytes, c->st,
+    pdl_launch(k_lte_fwd, (unsigned)cdiv(Bl, lte::kRows), lte::kThreads, lte::kSmemBytesF, c->st,
                c->x_local, c->W + L.down_w, c->W + L.down_b, c->U, c->W + L.up_w, c->W + L.up_b,
                c->down, c->mixed, c->x_lte, Bl);
     CK(cudaGetLastError());
