@@ -98,10 +98,19 @@ int edpc_decode_rows(int device, int64_t* dec_state, const uint8_t* data, int64_
  * original_len is the full stream length n (L = ceil(n / B)). */
 int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_len,
                     int32_t device, int32_t lane_begin, int32_t lane_count, edpc_ctx** out);
+/* Same, with the numerics forced: numerics = -1 picks the policy default (a
+ * function of the config); otherwise the EDPC_NUM_* flags below, as recorded
+ * in a container header (the decoder replays the encoder's numerics).  Flags
+ * the config / build cannot run are refused with EDPC_ERR_INVALID. */
+int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t original_len,
+                       int32_t device, int32_t lane_begin, int32_t lane_count, int32_t numerics,
+                       edpc_ctx** out);
 int edpc_ctx_destroy(edpc_ctx* ctx);
-/* Numerics the context runs (a function of the config, part of the format):
- * bit 0 = tcgen05 tensor-core GEMMs (tf32), bit 1 = fp16 operands for the
- * MBRB branch / out-projection GEMMs. */
+/* Numerics the context runs (part of the format, stored in the container's
+ * version byte): */
+#define EDPC_NUM_TCGEN05 1   /* tcgen05 tensor-core GEMMs (tf32 operands)          */
+#define EDPC_NUM_FP16 2      /* fp16 operands for the MBRB branch / out-projection */
+#define EDPC_NUM_LTE_FUSED 4 /* fused LTE forward kernel (mma.sync tf32, rna)      */
 int edpc_ctx_numerics(edpc_ctx* ctx, int32_t* flags);
 int edpc_ctx_info(edpc_ctx* ctx, int64_t* lane_len, int64_t* n_params, int64_t* n_shared);
 

@@ -27,6 +27,11 @@ PROFILES = {
                   lte_ratio=4, branches=2),
     "desk": dict(context_len=16, embed_dim=8, hidden_local=256, hidden_global=512,
                  lte_ratio=4, branches=2),
+    # BASELINE configs 4a / 4b (bench.py --workload c4a / c4b)
+    "paper_k1": dict(context_len=16, embed_dim=16, hidden_local=2048, hidden_global=4096,
+                     lte_ratio=4, branches=1),
+    "paper_lte1": dict(context_len=16, embed_dim=16, hidden_local=2048, hidden_global=4096,
+                       lte_ratio=1, branches=2),
 }
 
 

@@ -16,6 +16,9 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(PKG, "_edpc_b200.so")
 
 OK, ERR_INVALID, ERR_CUDA, ERR_CODER, ERR_STATE, ERR_NOMEM = range(6)
+# numerics flags (include/edpc_b200.h EDPC_NUM_*), recorded in the container
+NUM_TCGEN05, NUM_FP16, NUM_LTE_FUSED = 1, 2, 4
+NUMERICS_MASK = 7
 REGIONS = ["gemm", "fdm_fwd", "fdm_bwd_adam", "adam_shared", "softmax_quant", "encode",
            "decode", "colsum", "elementwise", "embed_grad"]
 
@@ -59,6 +62,8 @@ _SIGS = {
     "edpc_decode_rows": ([ctypes.c_int, _P, _P, _I64, _I64, _P, _I64, _P, _P], ctypes.c_int),
     "edpc_ctx_create": ([ctypes.POINTER(EdpcConfig), _I32, _I64, _I32, _I32, _I32,
                          ctypes.POINTER(_P)], ctypes.c_int),
+    "edpc_ctx_create_ex": ([ctypes.POINTER(EdpcConfig), _I32, _I64, _I32, _I32, _I32, _I32,
+                            ctypes.POINTER(_P)], ctypes.c_int),
     "edpc_ctx_destroy": ([_P], ctypes.c_int),
     "edpc_ctx_info": ([_P, _P, _P, _P], ctypes.c_int),
     "edpc_load_params": ([_P, _P, _I64], ctypes.c_int),

@@ -1,5 +1,8 @@
-// Fused LTE block (paper dims: F = 256, F' = 64) -- forward and backward each
-// as ONE kernel instead of GEMM -> per-lane FDM -> GEMM.
+// Fused LTE forward (paper dims: F = 256, F' = 64) as ONE kernel instead of
+// GEMM -> per-lane FDM -> GEMM.  (A fused backward was built and measured
+// slower than up-dgrad + FDM-bwd/Adam + down-dgrad -- 96.9 vs 91.7 us at C2:
+// its CTAs ran the projection phases in lockstep and left HBM idle -- and was
+// removed.)
 //
 // Reference: LteBlock.forward / backward (model.py:150-162) = down
 // linear_forward (nn.py:78-87), per_row_matmul_forward / _backward
@@ -228,115 +231,6 @@ k_lte_fwd(const float* __restrict__ x_local, const float* __restrict__ Wd,
     if (b0 + f.r0 + 8 < Bl)
       *reinterpret_cast<float2*>(x_lte + (int64_t)(b0 + f.r0 + 8) * kF + f.c0) =
           make_float2(acc[2] + q0, acc[3] + q1);
-  }
-}
-
-// g_mix = g_lte W_u^T; per lane: g_down_b = U_b g_mix_b with the old U, then
-// U_b's Adam step on down_b (x) g_mix_b (U, m, v read and written once);
-// g_loc = g_down W_d^T (fp32, plus the fp16 copy the fp16 MBRB path needs).
-// Gradients are in gradient-scale units (k_dlogits); ginv undoes the scale
-// for the Adam step exactly (power of two).
-__global__ void __launch_bounds__(lte::kThreads, 2)
-k_lte_bwd(const float* __restrict__ g_lte, const float* __restrict__ Wu,
-          const float* __restrict__ down, float* __restrict__ U, float* __restrict__ Um,
-          float* __restrict__ Uv, const float* __restrict__ Wd, float* __restrict__ gdown,
-          float* __restrict__ g_loc, __half* __restrict__ g_loc_h, int Bl, StepIdx si,
-          AdamConsts c, double b1d, double b2d, float ginv) {
-  using namespace lte;
-  extern __shared__ float4 lte_smem4[];
-  float* Gs = reinterpret_cast<float*>(lte_smem4);
-  float* Ws = Gs + kRows * kLdX;
-  float* GDs = Ws + kWFloats;
-  float* GMs = GDs + kRows * kLdS;
-  float* DNs = GMs + kRows * kLdS;  // the lanes' down rows (Adam operand)
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int b0 = blockIdx.x * kRows;
-  pdl_entry();
-  float bc1, bc2;
-  adam_bc(c, b1d, b2d, si.T(), bc1, bc2);
-  stage(Ws, kLdWuB, Wu, kFP, kF);
-  stage_rows(Gs, kLdX, g_lte, kF, b0, Bl);
-  stage_rows(DNs, kLdS, down, kFP, b0, Bl);
-  cp_async_commit();
-  cp_async_wait_all();
-  __syncthreads();
-  {  // g_mix[16][64] = G W_u^T: B(k = n, col = i) = W_u[i][n]
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    warp_tile<kF, false>(acc, Gs, kLdX, Ws, kLdWuB, warp * 8);
-    const Frag f(warp * 8);
-    *reinterpret_cast<float2*>(GMs + f.r0 * kLdS + f.c0) = make_float2(acc[0], acc[1]);
-    *reinterpret_cast<float2*>(GMs + (f.r0 + 8) * kLdS + f.c0) = make_float2(acc[2], acc[3]);
-  }
-  __syncthreads();
-  stage(Ws, kLdWdB, Wd, kF, kFP);  // lands during the FDM pass
-  cp_async_commit();
-  {  // FDM backward + Adam, 16 threads per lane, rows in batches of 8
-    const int r = tid >> 4, t = tid & 15, b = b0 + r;
-    const bool live = b < Bl;
-    const int bb = live ? b : 0;
-    const float4 g = *reinterpret_cast<const float4*>(GMs + r * kLdS + 4 * t);
-    const float* d = DNs + r * kLdS;
-    float4* u4 = reinterpret_cast<float4*>(U + (int64_t)bb * kFP * kFP);
-    float4* m4 = reinterpret_cast<float4*>(Um + (int64_t)bb * kFP * kFP);
-    float4* v4 = reinterpret_cast<float4*>(Uv + (int64_t)bb * kFP * kFP);
-    constexpr int kR = 8;
-#pragma unroll 1
-    for (int i0 = 0; i0 < kFP; i0 += kR) {
-      float4 w[kR], m[kR], q[kR];
-#pragma unroll
-      for (int k = 0; k < kR; ++k) {
-        const int e = (i0 + k) * (kFP / 4) + t;
-        w[k] = u4[e];
-        m[k] = m4[e];
-        q[k] = v4[e];
-      }
-      float part[kR];
-#pragma unroll
-      for (int k = 0; k < kR; ++k) {
-        const float di = d[i0 + k] * ginv;  // (d ginv) g == d (g ginv): exact
-        part[k] = fmaf(g.x, w[k].x, 0.f);
-        part[k] = fmaf(g.y, w[k].y, part[k]);
-        part[k] = fmaf(g.z, w[k].z, part[k]);
-        part[k] = fmaf(g.w, w[k].w, part[k]);
-        adam_elem(w[k].x, m[k].x, q[k].x, di * g.x, c, bc1, bc2);
-        adam_elem(w[k].y, m[k].y, q[k].y, di * g.y, c, bc1, bc2);
-        adam_elem(w[k].z, m[k].z, q[k].z, di * g.z, c, bc1, bc2);
-        adam_elem(w[k].w, m[k].w, q[k].w, di * g.w, c, bc1, bc2);
-        if (live) {
-          const int e = (i0 + k) * (kFP / 4) + t;
-          u4[e] = w[k];
-          m4[e] = m[k];
-          v4[e] = q[k];
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kR; ++k) {
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) part[k] += __shfl_xor_sync(0xffffffffu, part[k], o);
-        if (t == 0) {
-          GDs[r * kLdS + i0 + k] = live ? part[k] : 0.f;
-          if (live) gdown[(int64_t)b * kFP + i0 + k] = part[k];
-        }
-      }
-    }
-  }
-  cp_async_wait_all();
-  __syncthreads();
-#pragma unroll 1
-  for (int j = 0; j < kF / 64; ++j) {  // g_loc[16][256] = g_down W_d^T: B(k = j, col = n) = W_d[n][j]
-    const int n0 = (warp + 8 * j) * 8;
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    warp_tile<kFP, false>(acc, GDs, kLdS, Ws, kLdWdB, n0);
-    const Frag f(n0);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int row = b0 + f.r0 + 8 * h;
-      if (row >= Bl) continue;
-      const float2 v = make_float2(acc[2 * h], acc[2 * h + 1]);
-      *reinterpret_cast<float2*>(g_loc + (int64_t)row * kF + f.c0) = v;
-      if (g_loc_h)
-        *reinterpret_cast<__half2*>(g_loc_h + (int64_t)row * kF + f.c0) = __floats2half2_rn(v.x, v.y);
-    }
   }
 }
 

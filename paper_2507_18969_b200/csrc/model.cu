@@ -221,11 +221,14 @@ struct edpc_ctx {
   bool use_tc = false;
   // fp16 GEMM path for the MBRB branch / out-projection GEMMs (see ctx_create)
   bool h16 = false;
+  bool lte_fwd = false;  // fused LTE forward kernel (numerics bit 2)
   int gs_log2 = 0;                                  // gradient scale 2^gs_log2 (k_dlogits)
   __half* Wh = nullptr;                             // fp16 shadow of the shared weights
   __half *guph_l = nullptr, *guph_g = nullptr;      // fp16 copies of g_up per MBRB
   cudaStream_t st = nullptr, st_enc = nullptr;
   cudaStream_t st_aux = nullptr;  // weight-gradient GEMMs run here, joined before Adam
+  cudaStream_t st_h2d = nullptr;  // streaming ingest of input columns (edpc_set_input_columns)
+  cudaEvent_t ev_h2d = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev = nullptr;
   cudaEvent_t t0 = nullptr, t1 = nullptr, tj = nullptr;
@@ -274,6 +277,7 @@ struct edpc_ctx {
     if (st) cudaStreamSynchronize(st);
     if (st_enc) cudaStreamSynchronize(st_enc);
     if (st_aux) cudaStreamSynchronize(st_aux);
+    if (st_h2d) cudaStreamSynchronize(st_h2d);
     prof.flush();
     prof.release();
     for (auto& g : graph)
@@ -287,6 +291,8 @@ struct edpc_ctx {
     if (st) cudaStreamDestroy(st);
     if (st_enc) cudaStreamDestroy(st_enc);
     if (st_aux) cudaStreamDestroy(st_aux);
+    if (st_h2d) cudaStreamDestroy(st_h2d);
+    if (ev_h2d) cudaEventDestroy(ev_h2d);
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
   }
@@ -315,6 +321,8 @@ struct edpc_ctx {
 namespace edpc {
 
 constexpr int kTf32MinLanes = 1024;
+// numerics flags (edpc_ctx_numerics / edpc_ctx_create_ex, container header)
+constexpr int kNumTc = 1, kNumF16 = 2, kNumLteFused = 4, kNumericsMask = 7;
 
 constexpr int kFdmWarps = 2;  // warps per block of the per-lane FDM kernels
 
@@ -374,16 +382,6 @@ static bool al16(const void* p) { return ((uintptr_t)p & 15) == 0; }
 // tcgen05 path eligibility: shapes that tile cleanly and 16-byte aligned
 // operands / strides (TMA).  The choice depends only on the config and the
 // buffer layout, so compress and decompress always take the same path.
-// EDPC_TC_MASK (debug): bit 0 forward linears, 1 branch GEMMs, 2 dgrads, 3 wgrads
-static int tc_mask() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("EDPC_TC_MASK");
-    v = e ? atoi(e) : 15;
-  }
-  return v;
-}
-
 static bool tc_ok_m(edpc_ctx* c, int bit, int N, int Kchunk,
                     std::initializer_list<const void*> ptrs,
                     std::initializer_list<int64_t> strides);
@@ -401,7 +399,8 @@ static bool tc_ok(edpc_ctx* c, int N, int Kchunk, std::initializer_list<const vo
 static bool tc_ok_m(edpc_ctx* c, int bit, int N, int Kchunk,
                     std::initializer_list<const void*> ptrs,
                     std::initializer_list<int64_t> strides) {
-  return (tc_mask() >> bit & 1) && tc_ok(c, N, Kchunk, ptrs, strides);
+  (void)bit;
+  return tc_ok(c, N, Kchunk, ptrs, strides);
 }
 
 static cudaError_t as_cuda(int st) { return st == EDPC_OK ? cudaSuccess : cudaErrorUnknown; }
@@ -728,29 +727,19 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
   return EDPC_OK;
 }
 
-// Fused LTE kernels (lte.cuh): paper dims on the tcgen05 path (the SIMT
-// path keeps the reference-shaped GEMM -> FDM -> GEMM sequence).
-// Forward: on by default (ncu: 24.8 us vs 39.7 us for the three launches);
-// EDPC_LTE_FUSED=0 switches it off.  Backward: off by default -- k_lte_bwd
-// measured 96.9 us vs 91.7 us for up-dgrad + FDM-bwd/Adam + down-dgrad (its
-// CTAs run the projection phases in lockstep, leaving HBM idle meanwhile);
-// EDPC_LTE_FUSED_BWD=1 switches it on (experiments only).
-static bool lte_fused(const edpc_ctx* c, bool bwd = false) {
-  static int v = -1, vb = -1;
-  if (v < 0) {
-    const char* e = getenv("EDPC_LTE_FUSED");
-    v = (e && e[0] == '0') ? 0 : 1;
-    e = getenv("EDPC_LTE_FUSED_BWD");
-    vb = (e && e[0] == '1') ? 1 : 0;
-  }
-  if (!((bwd ? vb : v) == 1 && c->use_tc && c->lay.F == lte::kF && c->lay.FP == lte::kFP)) return false;
+// Fused LTE forward (lte.cuh, k_lte_fwd): paper dims on the tcgen05 path (the
+// SIMT path keeps the reference-shaped GEMM -> FDM -> GEMM sequence).  ncu:
+// 24.8 us vs 39.7 us for the three launches.  Part of the numerics (mma.sync
+// tf32 rounds operands to nearest, tcgen05 tf32 truncates): numerics bit 2.
+static bool lte_fused(const edpc_ctx* c) { return c->lte_fwd; }
+
+static bool lte_fused_possible(const edpc_ctx* c) {
+  if (!(c->use_tc && c->lay.F == lte::kF && c->lay.FP == lte::kFP)) return false;
   static signed char attr[64] = {};  // per device: 0 unset, 1 ok, -1 failed
   signed char& a = attr[c->device & 63];
   if (a == 0) {
     a = cudaFuncSetAttribute(k_lte_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)lte::kSmemBytesF) == cudaSuccess &&
-                cudaFuncSetAttribute(k_lte_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)lte::kSmemBytes) == cudaSuccess
+                             (int)lte::kSmemBytesF) == cudaSuccess
             ? 1
             : -1;
   }
@@ -907,18 +896,7 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
   // LTE up
   CK(fork_aux(c));
   CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
-  if (lte_fused(c, true)) {  // up dgrad + FDM backward/Adam + down dgrad, one kernel
-    {
-      Scope sc_(c, kRegFdmBwd, c->st);
-      pdl_launch(k_lte_bwd, (unsigned)cdiv(Bl, lte::kRows), lte::kThreads, lte::kSmemBytes, c->st,
-                 c->g_lte, c->W + L.up_w, c->down, c->U, c->Um, c->Uv, c->W + L.down_w, c->gdown,
-                 c->g_loc, c->h16 ? c->guph_l : nullptr, Bl, c->si(), c->adam, c->cfg.beta1,
-                 c->cfg.beta2, ldexpf(1.0f, -c->gs_log2));
-    }
-    CK(cudaGetLastError());
-    CK(fork_aux(c));
-    CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
-  } else {
+  {
     CK(dgrad(c, c->g_lte, F, 1, 0, c->W + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
     // per-lane FDM: g_down with the old U, then U's Adam step (fused: U read once)
     {
@@ -931,35 +909,15 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
                      c->gdown, Bl, c->si(), c->adam, c->cfg.beta1, c->cfg.beta2,
                      ldexpf(1.0f, -c->gs_log2));
         };
-        // split (EDPC_FDM_SPLIT=1, experiment) measured 3% slower at C2: the
-        // side-stream Adam pass competes with the main stream for HBM and U is
-        // read twice
-        const bool split = getenv("EDPC_FDM_SPLIT") && getenv("EDPC_FDM_SPLIT")[0] == '1';
-        if (FP == 64) {
-          if (split) {
-            run(k_fdm_bwd_adam_v<64, true, false>, c->st);
-            CK(fork_aux(c));
-            run(k_fdm_bwd_adam_v<64, false, true>, c->st_aux);
-          } else {
-            run(k_fdm_bwd_adam_v<64>, c->st);
-          }
-        } else if (FP == 128) {
-          if (split) {
-            run(k_fdm_bwd_adam_v<128, true, false>, c->st);
-            CK(fork_aux(c));
-            run(k_fdm_bwd_adam_v<128, false, true>, c->st_aux);
-          } else {
-            run(k_fdm_bwd_adam_v<128>, c->st);
-          }
-        } else {
-          if (split) {
-            run(k_fdm_bwd_adam_v<256, true, false>, c->st);
-            CK(fork_aux(c));
-            run(k_fdm_bwd_adam_v<256, false, true>, c->st_aux);
-          } else {
-            run(k_fdm_bwd_adam_v<256>, c->st);
-          }
-        }
+        // (a split variant -- FDM backward on the main stream, U's Adam pass on
+        // the side stream -- measured 3% slower at C2: the passes compete for
+        // HBM and U is read twice)
+        if (FP == 64)
+          run(k_fdm_bwd_adam_v<64>, c->st);
+        else if (FP == 128)
+          run(k_fdm_bwd_adam_v<128>, c->st);
+        else
+          run(k_fdm_bwd_adam_v<256>, c->st);
       } else {
         Scope sc_(c, kRegFdmBwd, c->st);
         pdl_launch(k_fdm_bwd_adam, (unsigned)cdiv(Bl, 8), 256, 0, c->st, 
@@ -1267,7 +1225,14 @@ int edpc_has_tcgen05(void) { return tc_compiled() ? 1 : 0; }
 
 int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_len,
                     int32_t device, int32_t lane_begin, int32_t lane_count, edpc_ctx** out) {
+  return edpc_ctx_create_ex(cfg, segments, original_len, device, lane_begin, lane_count, -1, out);
+}
+
+int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t original_len,
+                       int32_t device, int32_t lane_begin, int32_t lane_count, int32_t numerics,
+                       edpc_ctx** out) {
   EDPC_CHECK_ARG(out, "null out");
+  EDPC_CHECK_ARG(numerics >= -1 && numerics <= kNumericsMask, "unknown numerics flags");
   *out = nullptr;
   EDPC_TRY(check_cfg(cfg));
   EDPC_CHECK_ARG(segments >= 1 && cfg->lanes % segments == 0,
@@ -1319,33 +1284,41 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
     c->adam.k2 = (float)(1.0 - b2);
     c->adam.eps = (float)cfg->adam_eps;
   }
-  // Numerics policy (part of the format: a function of the config only).
-  // TF32 tensor-core GEMMs when the container has >= kTf32MinLanes lanes:
-  // the per-step gradient averages over enough lanes that TF32 operand
-  // rounding does not move the compression ratio (C2-mini, B=4096: +0.07%
-  // vs the fp64 reference); below that (e.g. config 1, B=64) TF32 moved the
-  // ratio by -1.35%..+0.84% over three streams, fp32 by at most 0.34%, so
-  // small-lane containers use the fp32 GEMMs.  EDPC_TCGEN05=0/1 forces a
-  // path for debugging only (both sides of a container must agree).
-  {
-    const char* e = getenv("EDPC_TCGEN05");
-    if (e && e[0] == '1')
-      c->use_tc = tc_compiled();
-    else if (e && e[0] == '0')
-      c->use_tc = false;
-    else
-      c->use_tc = tc_compiled() && cfg->lanes >= kTf32MinLanes;
-  }
-  // fp16 operands for the MBRB GEMMs (part of the same numerics policy):
-  // on the tensor-core path whenever the shapes tile (k = 2, F and the lane
-  // groups multiples of 64 for the fp16 k-blocks, H multiple of 128).
-  // EDPC_F16=0 keeps them tf32 (debugging / A-B runs).
+  // Numerics policy (recorded in the container; by default a function of the
+  // config only).  TF32 tensor-core GEMMs when the container has >=
+  // kTf32MinLanes lanes: the per-step gradient averages over enough lanes
+  // that TF32 operand rounding does not move the compression ratio (C2-mini,
+  // B=4096: +0.07% vs the fp64 reference); below that (e.g. config 1, B=64)
+  // TF32 moved the ratio by -1.35%..+0.84% over three streams, fp32 by at
+  // most 0.34%, so small-lane containers use the fp32 GEMMs.  fp16 operands
+  // for the MBRB GEMMs on the tensor-core path whenever the shapes tile (k = 2,
+  // F and the lane groups multiples of 64 for the fp16 k-blocks, H multiple
+  // of 128).  The fused LTE forward at paper dims.  numerics >= 0 (the
+  // decoder replaying a container's recorded flags, or a test) forces the
+  // flags; infeasible combinations are refused.
   {
     const Layout& L = c->lay;
-    const char* e = getenv("EDPC_F16");
     const int glanes = L.B / kNumGroups;
-    c->h16 = !(e && e[0] == '0') && c->use_tc && L.K == 2 && L.F % 64 == 0 &&
-             L.HL % 128 == 0 && L.HG % 128 == 0 && L.B % kNumGroups == 0 && glanes % 64 == 0;
+    const bool tc_ok_cfg = tc_compiled();
+    const bool h16_ok = L.K == 2 && L.F % 64 == 0 && L.HL % 128 == 0 && L.HG % 128 == 0 &&
+                        L.B % kNumGroups == 0 && glanes % 64 == 0;
+    if (numerics < 0) {
+      c->use_tc = tc_ok_cfg && cfg->lanes >= kTf32MinLanes;
+      c->h16 = c->use_tc && h16_ok;
+      c->lte_fwd = lte_fused_possible(c);
+    } else {
+      c->use_tc = (numerics & kNumTc) != 0;
+      c->h16 = (numerics & kNumF16) != 0;
+      c->lte_fwd = (numerics & kNumLteFused) != 0;
+      const bool ok = (!c->use_tc || tc_ok_cfg) && (!c->h16 || (c->use_tc && h16_ok)) &&
+                      (!c->lte_fwd || lte_fused_possible(c));
+      if (!ok) {
+        delete c;
+        set_error("numerics flags " + std::to_string(numerics) +
+                  " cannot run for this config / build");
+        return EDPC_ERR_INVALID;
+      }
+    }
     int k = 0;
     while ((2 << k) <= L.B) ++k;  // 2^k <= B < 2^(k+1)
     c->gs_log2 = k;
@@ -1360,7 +1333,9 @@ int edpc_ctx_create(const edpc_config* cfg, int32_t segments, int64_t original_l
       cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->st_aux, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->st_h2d, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_h2d, cudaEventDisableTiming) != cudaSuccess) {
     set_error("stream/event creation failed");
     return fail(EDPC_ERR_CUDA);
   }
@@ -1498,7 +1473,7 @@ int edpc_ctx_destroy(edpc_ctx* ctx) {
 
 int edpc_ctx_numerics(edpc_ctx* c, int32_t* flags) {
   EDPC_CHECK_ARG(c && flags, "null argument");
-  *flags = (c->use_tc ? 1 : 0) | (c->h16 ? 2 : 0);
+  *flags = (c->use_tc ? kNumTc : 0) | (c->h16 ? kNumF16 : 0) | (c->lte_fwd ? kNumLteFused : 0);
   return EDPC_OK;
 }
 
@@ -1573,23 +1548,30 @@ int edpc_set_input_columns(edpc_ctx* c, const uint8_t* stream, int64_t n, int64_
   EDPC_CUDA_TRY(cudaSetDevice(c->device));
   if (!c->have_input) {
     EDPC_CUDA_TRY(cudaMemsetAsync(c->mat, 0, (int64_t)c->Bl * std::max<int64_t>(c->L, 1), c->st));
+    EDPC_CUDA_TRY(cudaEventRecord(c->ev_h2d, c->st));
+    EDPC_CUDA_TRY(cudaStreamWaitEvent(c->st_h2d, c->ev_h2d, 0));
     c->have_input = true;
   }
   const int64_t w = col1 - col0;
   if (w == 0) return EDPC_OK;
-  // rows fully inside the stream go as one strided copy; at most one row is partial
+  // copies go on the ingest stream (overlapping the model steps already
+  // queued on the main stream); the main stream waits for them before the
+  // steps that read these columns.  Rows fully inside the stream go as one
+  // strided copy; at most one row is partial.
   int64_t full = 0;
   while (full < c->Bl && ((int64_t)(c->lane0 + full)) * c->L + col1 <= n) ++full;
   if (full)
     EDPC_CUDA_TRY(cudaMemcpy2DAsync(c->mat + col0, c->L, stream + (int64_t)c->lane0 * c->L + col0,
-                                    c->L, w, full, cudaMemcpyHostToDevice, c->st));
+                                    c->L, w, full, cudaMemcpyHostToDevice, c->st_h2d));
   if (full < c->Bl) {
     const int64_t start = (int64_t)(c->lane0 + full) * c->L + col0;
     const int64_t have = std::max<int64_t>(0, std::min<int64_t>(w, n - start));
     if (have)
       EDPC_CUDA_TRY(cudaMemcpyAsync(c->mat + full * c->L + col0, stream + start, have,
-                                    cudaMemcpyHostToDevice, c->st));
+                                    cudaMemcpyHostToDevice, c->st_h2d));
   }
+  EDPC_CUDA_TRY(cudaEventRecord(c->ev_h2d, c->st_h2d));
+  EDPC_CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_h2d, 0));
   return EDPC_OK;
 }
 

@@ -77,13 +77,14 @@ def lane_plan(cfg: ModelConfig, segments: int, world: int) -> list[tuple[int, in
     return [(r * per, per) for r in range(world)]
 
 
-def assemble(cfg: ModelConfig, n: int, shards: list[tuple[list[int], list[bytes]]]) -> EdpcContainer:
+def assemble(cfg: ModelConfig, n: int, shards: list[tuple[list[int], list[bytes]]],
+             numerics: int = 0) -> EdpcContainer:
     """Container from per-rank (bit_lengths, payloads), rank order = segment order."""
     bits, pays = [], []
     for b, p in shards:
         bits += list(b)
         pays += list(p)
-    return EdpcContainer(header=Header.from_config(cfg, n, bits), segments=pays)
+    return EdpcContainer(header=Header.from_config(cfg, n, bits, numerics), segments=pays)
 
 
 def _split_payloads(bits, buf):
@@ -101,11 +102,15 @@ class ShardSet:
     """G contexts (one per device in ``devices``; devices may repeat, e.g. to
     exercise the sharded path on one GPU) driven by one host thread."""
 
-    def __init__(self, cfg: ModelConfig, segments: int, n: int, devices: list[int]):
+    def __init__(self, cfg: ModelConfig, segments: int, n: int, devices: list[int],
+                 numerics: int | None = None):
         self.cfg = cfg
         self.plan = lane_plan(cfg, segments, len(devices))
-        self.ctxs = [DeviceContext(cfg, segments, n, d, lb, lc)
-                     for d, (lb, lc) in zip(devices, self.plan)]
+        self.ctxs = []
+        for d, (lb, lc) in zip(devices, self.plan):
+            self.ctxs.append(DeviceContext(cfg, segments, n, d, lb, lc, numerics=numerics))
+            numerics = self.ctxs[0].numerics_flags()  # every shard runs rank 0's numerics
+        self.numerics = numerics
         params = init_params_f32(cfg)
         for c in self.ctxs:
             c.load_flat(params)
@@ -162,12 +167,13 @@ def compress_multi(data: bytes, cfg: ModelConfig, segments: int, devices: list[i
             pay = np.zeros(max(tot.value, 1), dtype=np.uint8)
             _lib.check(lib.edpc_get_payloads(c.h, pay.ctypes.data, pay.size))
             shards.append((bits.tolist(), _split_payloads(bits, pay)))
+        numerics = ss.numerics
     finally:
         ss.close()
     if stats is not None:
         stats.update(steps=max(0, L - T), predict_s=0.0, train_s=0.0, encode_s=0.0,
                      wall_s=time.perf_counter() - t0, peak_queue_depth=0, devices=list(devices))
-    return assemble(cfg, n, shards)
+    return assemble(cfg, n, shards, numerics)
 
 
 def decompress_multi(container: EdpcContainer, devices: list[int], *,
@@ -179,7 +185,7 @@ def decompress_multi(container: EdpcContainer, devices: list[int], *,
     segments = h.segment_count
     for d in set(devices):
         _lib.require_device(d)
-    ss = ShardSet(cfg, segments, n, list(devices))
+    ss = ShardSet(cfg, segments, n, list(devices), numerics=h.numerics)
     lib = ss.lib
     try:
         spl = cfg.lanes // segments

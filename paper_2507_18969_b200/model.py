@@ -31,7 +31,8 @@ class DeviceContext:
     """Owns one ``edpc_ctx`` (one container on one device)."""
 
     def __init__(self, cfg: ModelConfig, segments: int, original_len: int, device: int = 0,
-                 lane_begin: int = 0, lane_count: int | None = None):
+                 lane_begin: int = 0, lane_count: int | None = None,
+                 numerics: int | None = None):
         lib = _lib.load()
         self.cfg = cfg
         self.device = device
@@ -40,8 +41,10 @@ class DeviceContext:
         self.segments = segments
         c = _lib.EdpcConfig.from_model_config(cfg)
         h = ctypes.c_void_p()
-        _lib.check(lib.edpc_ctx_create(ctypes.byref(c), segments, original_len, device,
-                                       lane_begin, self.lane_count, ctypes.byref(h)))
+        _lib.check(lib.edpc_ctx_create_ex(ctypes.byref(c), segments, original_len, device,
+                                          lane_begin, self.lane_count,
+                                          -1 if numerics is None else int(numerics),
+                                          ctypes.byref(h)))
         self.h = h
         L, npar, nsh = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
         _lib.check(lib.edpc_ctx_info(h, ctypes.addressof(L), ctypes.addressof(npar),
@@ -68,12 +71,19 @@ class DeviceContext:
         _lib.check(_lib.load().edpc_get_params(self.h, out.ctypes.data, out.size))
         return out
 
-    def numerics(self) -> dict:
-        """GEMM numerics of this context (fixed by the config): tensor cores
-        (tf32) and fp16 operands for the MBRB branch / out-projection GEMMs."""
+    def numerics_flags(self) -> int:
+        """EDPC_NUM_* flags of this context (recorded in the container)."""
         f = ctypes.c_int32()
         _lib.check(_lib.load().edpc_ctx_numerics(self.h, ctypes.byref(f)))
-        return {"tcgen05": bool(f.value & 1), "fp16_mbrb": bool(f.value & 2)}
+        return int(f.value)
+
+    def numerics(self) -> dict:
+        """GEMM numerics of this context (policy: a function of the config):
+        tensor cores (tf32), fp16 operands for the MBRB branch / out-projection
+        GEMMs, the fused LTE forward."""
+        f = self.numerics_flags()
+        return {"tcgen05": bool(f & _lib.NUM_TCGEN05), "fp16_mbrb": bool(f & _lib.NUM_FP16),
+                "lte_fused": bool(f & _lib.NUM_LTE_FUSED)}
 
     def state_checksum(self) -> str:
         """sha256 over the fp32 parameter bytes (the lockstep probe, `model.py:294-300`)."""
@@ -88,10 +98,11 @@ class DeviceContext:
 class EdpcModel:
     """The full predictor on one device; construction order fixes the init stream."""
 
-    def __init__(self, cfg: ModelConfig, *, device: int = 0, params: np.ndarray | None = None):
+    def __init__(self, cfg: ModelConfig, *, device: int = 0, params: np.ndarray | None = None,
+                 numerics: int | None = None):
         cfg.validate()
         self.cfg = cfg
-        self._ctx = DeviceContext(cfg, 1, 0, device)
+        self._ctx = DeviceContext(cfg, 1, 0, device, numerics=numerics)
         self._ctx.load_flat(init_params_f32(cfg) if params is None else params)
         self._version = 0
 
@@ -133,6 +144,9 @@ class EdpcModel:
 
     def state_checksum(self) -> str:
         return self._ctx.state_checksum()
+
+    def numerics(self) -> dict:
+        return self._ctx.numerics()
 
     def param_count(self) -> dict[str, int]:
         total = model_param_count(self.cfg)

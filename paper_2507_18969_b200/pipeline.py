@@ -43,6 +43,19 @@ def _stats(stats, **kw):
         stats.update(kw)
 
 
+def _devices(device: int, devices) -> tuple[int, list[int] | None]:
+    """Normalise ``device`` / ``devices``: one entry means that device; more
+    than one means the lane-sharded multi-GPU path (dist.py)."""
+    if devices is None:
+        return int(device), None
+    devs = [int(d) for d in devices]
+    if not devs:
+        raise ValueError("devices must not be empty")
+    if len(devs) == 1:
+        return devs[0], None
+    return devs[0], devs
+
+
 def compress(data: bytes, cfg: ModelConfig, segments: int = 4, *,
              serial: bool = False, threads: int | None = None,
              queue_capacity: int = 8, stats: dict | None = None,
@@ -53,9 +66,10 @@ def compress(data: bytes, cfg: ModelConfig, segments: int = 4, *,
     """Compress ``data`` into a self-describing container (bytes are a pure
     function of (data, cfg, segments))."""
     validate_geometry(cfg, segments)
-    if devices is not None and len(list(devices)) > 1:
+    device, devs = _devices(device, devices)
+    if devs is not None:
         from .dist import compress_multi
-        return compress_multi(data, cfg, segments, list(devices), stats=stats)
+        return compress_multi(data, cfg, segments, devs, stats=stats)
     t0 = time.perf_counter()
     n = len(data)
     if n == 0:
@@ -66,16 +80,22 @@ def compress(data: bytes, cfg: ModelConfig, segments: int = 4, *,
     ctx = DeviceContext(cfg, segments, n, device)
     try:
         ctx.load_flat(init_params_f32(cfg))
+        numerics = ctx.numerics_flags()
         buf = np.frombuffer(bytes(data), dtype=np.uint8)
-        _lib.check(_lib.load().edpc_set_input(ctx.h, buf.ctypes.data, n, 0))
         L = ctx.lane_len
         T = cfg.context_len
         lib = _lib.load()
         tl = time.perf_counter()
         if step_hook is None and (param_probe is None or not probe_every):
+            # streaming ingest: each block of lane columns
+            # goes H2D on the context's copy stream while the previous block's
+            # model steps run; the steps wait only for their own columns
             for i0 in range(0, L, chunk):
-                _lib.check(lib.edpc_compress_steps(ctx.h, i0, min(L, i0 + chunk)))
+                i1 = min(L, i0 + chunk)
+                _lib.check(lib.edpc_set_input_columns(ctx.h, buf.ctypes.data, n, i0, i1))
+                _lib.check(lib.edpc_compress_steps(ctx.h, i0, i1))
         else:
+            _lib.check(lib.edpc_set_input(ctx.h, buf.ctypes.data, n, 0))
             _lib.check(lib.edpc_compress_steps(ctx.h, 0, min(T, L)))
             mat = None
             if step_hook is not None:
@@ -105,7 +125,8 @@ def compress(data: bytes, cfg: ModelConfig, segments: int = 4, *,
     _stats(stats, steps=max(0, L - T), predict_s=loop_s, train_s=0.0,
            encode_s=time.perf_counter() - te, wall_s=time.perf_counter() - t0,
            peak_queue_depth=0)
-    return EdpcContainer(header=Header.from_config(cfg, n, bits.tolist()), segments=payloads)
+    return EdpcContainer(header=Header.from_config(cfg, n, bits.tolist(), numerics),
+                         segments=payloads)
 
 
 def decompress(container: EdpcContainer, *, threads: int = 1, stats: dict | None = None,
@@ -128,12 +149,14 @@ def decompress(container: EdpcContainer, *, threads: int = 1, stats: dict | None
     for s, (p, b) in enumerate(zip(container.segments, header.bit_lengths)):
         if b > len(p) * 8:
             raise CoderError(f"segment {s}: bit length {b} exceeds payload of {len(p)} bytes")
-    if devices is not None and len(list(devices)) > 1:
+    device, devs = _devices(device, devices)
+    if devs is not None:
         from .dist import decompress_multi
-        return decompress_multi(container, list(devices), stats=stats)
+        return decompress_multi(container, devs, stats=stats)
     _lib.require_device(device)
     lib = _lib.load()
-    ctx = DeviceContext(cfg, segments, n, device)
+    # replay the encoder's numerics (recorded in the version byte)
+    ctx = DeviceContext(cfg, segments, n, device, numerics=header.numerics)
     try:
         ctx.load_flat(init_params_f32(cfg))
         pay = np.frombuffer(b"".join(container.segments) or b"\0", dtype=np.uint8)

@@ -119,6 +119,18 @@ def test_container_rejects_corruption():
 def test_container_version_separates_numerics():
     blob = bytearray(write_container(_container()))
     assert blob[4] == 2
+    # the encoder's numerics flags ride in the version byte's high nibble
+    c = _container()
+    c.header.numerics = 7
+    b7 = write_container(c)
+    assert b7[4] == 0x72 and read_container(b7).header.numerics == 7
+    c.header.numerics = 8
+    with pytest.raises(ContainerError):
+        write_container(c)
+    bad = bytearray(b7)
+    bad[4] = 0x82  # unknown flag
+    with pytest.raises(ContainerError):
+        read_container(bytes(bad))
     v1 = write_container(_container(), version=1)
     with pytest.raises(BadVersionError):
         read_container(v1)  # a reference (fp64) container is not GPU-decodable

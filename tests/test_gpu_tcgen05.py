@@ -4,7 +4,6 @@ are TF32's (10-bit mantissa operands, fp32 accumulation): relative error of
 each tensor in Frobenius norm <= 5e-3 (TF32 truncates operands to 10
 mantissa bits; measured 0.7e-3 .. 3.5e-3)."""
 import ctypes
-import os
 
 import numpy as np
 import pytest
@@ -19,14 +18,17 @@ pytestmark = pytest.mark.gpu
 REL = 5e-3
 
 
+def _flags(cfg, tc: bool, f16: bool) -> int:
+    """Numerics flags forced on the context (edpc_ctx_create_ex): tcgen05,
+    fp16 MBRB operands, and the fused LTE forward wherever the tcgen05 path
+    would use it (paper dims F = 256, F' = 64)."""
+    lte = tc and cfg.feature_dim == 256 and cfg.feature_dim // cfg.lte_ratio == 64
+    return ((_lib.NUM_TCGEN05 if tc else 0) | (_lib.NUM_FP16 if f16 else 0)
+            | (_lib.NUM_LTE_FUSED if lte else 0))
+
+
 def _ctx(cfg, tc: bool, f16: bool = False):
-    os.environ["EDPC_TCGEN05"] = "1" if tc else "0"
-    os.environ["EDPC_F16"] = "1" if f16 else "0"
-    try:
-        c = DeviceContext(cfg, 4, 0, 0)
-    finally:
-        os.environ.pop("EDPC_TCGEN05", None)
-        os.environ.pop("EDPC_F16", None)
+    c = DeviceContext(cfg, 4, 0, 0, numerics=_flags(cfg, tc, f16))
     c.load_flat(init_params_f32(cfg))
     return c
 
@@ -59,8 +61,9 @@ def test_f16_matches(ref):
     cfg = ModelConfig(**PAPER, lanes=1024)
     a = _ctx(cfg, True, f16=True)
     b = _ctx(cfg, ref == "tf32", f16=False)
-    assert a.numerics() == {"tcgen05": True, "fp16_mbrb": True}
-    assert b.numerics() == {"tcgen05": ref == "tf32", "fp16_mbrb": False}
+    assert a.numerics() == {"tcgen05": True, "fp16_mbrb": True, "lte_fused": True}
+    assert b.numerics() == {"tcgen05": ref == "tf32", "fp16_mbrb": False,
+                            "lte_fused": ref == "tf32"}
     _compare(cfg, a, b)
 
 

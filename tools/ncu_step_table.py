@@ -3,8 +3,8 @@
     ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,\
 sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,\
 lts__throughput.avg.pct_of_peak_sustained_elapsed --clock-control none \
-        -k regex:'^(?!k_boot)' --csv --log-file X.csv python tests/prof_step.py 4096 1
-    python tests/ncu_step_table.py X.csv "title" profiles/rNN_gemm_traffic.json > profiles/rNN_step_kernels.md
+        -k regex:'^(?!k_boot)' --csv --log-file X.csv python tools/prof_step.py 4096 1
+    python tools/ncu_step_table.py X.csv "title" profiles/rNN_gemm_traffic.json > profiles/rNN_step_kernels.md
 
 Takes the LAST model step's launches (from the last k_embed_ln<1> on).
 """
