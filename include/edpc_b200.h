@@ -191,8 +191,15 @@ int edpc_sync(edpc_ctx* ctx);
 /* test/debug read-back of internal fp32 buffers after a step:
  * 0 gradient partials [8][n_shared], 1 probs, 2 x_local, 3 x_lte, 4 x_global,
  * 5 local branch outputs [k][B][h_l], 6 global branch outputs, 7 d(embedded
- * context), 8 logits.  count must equal the buffer's element count. */
+ * context), 8 logits, 9 per-lane FDM Adam m [B][F'][F'], 10 shared Adam m,
+ * 11 shared Adam v, 12 per-lane FDM U.  count must equal the buffer's
+ * element count. */
 int edpc_debug_read(edpc_ctx* ctx, int32_t which, float* out, int64_t count);
+/* the shared-parameter Adam kernel on host arrays: `steps` updates of w0 by
+ * grads[t][n] (_kernels.py:18-32 adam_update; tests pin it to the reference) */
+int edpc_debug_adam(const float* w0, const float* grads, int64_t n, int32_t steps, double lr,
+                    double beta1, double beta2, double eps, float* w_out, float* m_out,
+                    float* v_out);
 /* bare tcgen05 GEMM microbenchmark on device operands (avg ms per launch) */
 int edpc_bench_gemm(int32_t M, int32_t N, int32_t K, int32_t a_mn, int32_t b_mn, int32_t nsplit,
                     int32_t iters, double* ms);

@@ -2164,6 +2164,10 @@ int edpc_debug_read(edpc_ctx* c, int32_t which, float* out, int64_t count) {
     case 6: src = c->g_H; n = (int64_t)L.K * Bl * L.HG; break;
     case 7: src = c->g_emb; n = Bl * L.F; break;
     case 8: src = c->logits; n = Bl * 256; break;
+    case 9: src = c->Um; n = Bl * L.fdm; break;   // per-lane FDM Adam m
+    case 10: src = c->M; n = L.n_shared; break;   // shared Adam m
+    case 11: src = c->V; n = L.n_shared; break;   // shared Adam v
+    case 12: src = c->U; n = Bl * L.fdm; break;   // per-lane FDM U
     default: EDPC_CHECK_ARG(false, "unknown debug buffer");
   }
   EDPC_CHECK_ARG(count == n, "debug buffer size mismatch (expected " + std::to_string(n) + ")");
@@ -2178,6 +2182,54 @@ int edpc_debug_read(edpc_ctx* c, int32_t which, float* out, int64_t count) {
     const float inv = ldexpf(1.0f, -c->gs_log2);
     for (int64_t e = 0; e < n; ++e) out[e] *= inv;
   }
+  return EDPC_OK;
+}
+
+// The shared-parameter Adam kernel (k_adam_shared, one leaf) on host arrays:
+// `steps` updates of w0 by grads[t][n], t = 1..steps (`_kernels.py:18-32`,
+// the reference's adam_update over a flat buffer).  Tests pin it against the
+// reference-generated trajectory (tests/golden/adam.npz).
+int edpc_debug_adam(const float* w0, const float* grads, int64_t n, int32_t steps, double lr,
+                    double beta1, double beta2, double eps, float* w_out, float* m_out,
+                    float* v_out) {
+  EDPC_CHECK_ARG(w0 && grads && w_out && m_out && v_out && n > 0 && steps >= 0, "bad arguments");
+  float *W, *M, *V, *P;
+  int64_t* d_t;
+  EDPC_CUDA_TRY(cudaMalloc(&W, n * 4));
+  EDPC_CUDA_TRY(cudaMalloc(&M, n * 4));
+  EDPC_CUDA_TRY(cudaMalloc(&V, n * 4));
+  EDPC_CUDA_TRY(cudaMalloc(&P, n * 4));
+  EDPC_CUDA_TRY(cudaMalloc(&d_t, 8));
+  EDPC_CUDA_TRY(cudaMemcpy(W, w0, n * 4, cudaMemcpyHostToDevice));
+  EDPC_CUDA_TRY(cudaMemset(M, 0, n * 4));
+  EDPC_CUDA_TRY(cudaMemset(V, 0, n * 4));
+  AdamConsts a{};
+  a.lr = (float)lr;
+  a.b1 = (float)beta1;
+  a.b2 = (float)beta2;
+  a.k1 = (float)(1.0 - beta1);
+  a.k2 = (float)(1.0 - beta2);
+  a.eps = (float)eps;
+  cudaError_t e = cudaSuccess;
+  for (int32_t t = 1; t <= steps && e == cudaSuccess; ++t) {
+    const int64_t tt = t;
+    e = cudaMemcpy(d_t, &tt, 8, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(P, grads + (t - 1) * n, n * 4, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      k_adam_shared<1><<<(unsigned)std::min<int64_t>(cdiv(n, 256), 1184), 256>>>(
+          W, M, V, P, n, n, StepIdx{d_t, d_t, 0}, a, beta1, beta2, 1.0f, nullptr);
+      e = cudaDeviceSynchronize();
+    }
+  }
+  if (e == cudaSuccess) e = cudaMemcpy(w_out, W, n * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(m_out, M, n * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(v_out, V, n * 4, cudaMemcpyDeviceToHost);
+  cudaFree(W);
+  cudaFree(M);
+  cudaFree(V);
+  cudaFree(P);
+  cudaFree(d_t);
+  EDPC_CUDA_TRY(e);
   return EDPC_OK;
 }
 

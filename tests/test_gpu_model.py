@@ -40,10 +40,7 @@ def test_predict_and_train_match_oracle(cfg):
         lo = o.train_step(co, tg)
         assert abs(lg - lo) < 1e-3 * max(1.0, abs(lo))
     assert worst <= PROB_TOL
-    pg = g.parameters_flat().astype(np.float64)
-    # each Adam step moves a weight by <= ~lr; near-zero gradients may flip
-    # sign between fp32/TF32 and fp64, so the bound is 2 * lr per step
-    assert np.abs(pg - o.value).max() <= 2 * cfg.lr * 6
+    # (gradients and Adam state are checked tensor by tensor in test_gpu_parity.py)
 
 
 def test_paper_dims_predict_matches_oracle_at_init():

@@ -14,7 +14,7 @@ from paper_2507_18969_b200 import (ArithmeticEncoder, CoderError, ContainerError
                                    compress, decompress, quantize_rows, read_container,
                                    split_lanes, write_container)
 from paper_2507_18969_b200 import synth
-from helpers import DESK, TINY, tiny_cfg
+from helpers import DESK, PAPER, TINY, tiny_cfg
 
 pytestmark = pytest.mark.gpu
 RATIO_TOL = 0.005
@@ -156,8 +156,13 @@ def test_ratio_within_half_percent_of_oracle_desk_dims():
     assert abs(r_gpu / r_ref - 1) <= RATIO_TOL, (r_gpu, r_ref)
 
 
+PROFILES = {"desk": DESK, "paper": PAPER, "paper_k1": dict(PAPER, branches=1),
+            "paper_lte1": dict(PAPER, lte_ratio=1)}
+
+
 @pytest.mark.parametrize("name", ["desk_text_256k", "c2mini_text_4m", "c1_text_1m",
-                                  "c1_text_1m_s1", "c1_text_1m_s2"])
+                                  "c1_text_1m_s1", "c1_text_1m_s2", "c4amini_text_4m",
+                                  "c4bmini_text_4m", "c3mini_mixed_8m"])
 def test_ratio_within_half_percent_of_reference_run(name):
     """Anchored on a run of the unmodified reference (tests/golden/ref_ratio_*.json)."""
     path = os.path.join(os.path.dirname(__file__), "golden", f"ref_ratio_{name}.json")
@@ -166,12 +171,12 @@ def test_ratio_within_half_percent_of_reference_run(name):
     ref = json.load(open(path))
     data = synth.generate(ref["kind"], ref["nbytes"], ref["seed"])
     assert synth.sha256(data) == ref["sha256"]
-    prof = DESK if ref["profile"] == "desk" else dict(context_len=16, embed_dim=16,
-                                                      hidden_local=2048, hidden_global=4096,
-                                                      lte_ratio=4, branches=2)
-    cfg = ModelConfig(**prof, lanes=ref["lanes"])
+    cfg = ModelConfig(**PROFILES[ref["profile"]], lanes=ref["lanes"])
     blob = write_container(compress(data, cfg, ref["segments"]))
-    assert abs((len(data) / len(blob)) / ref["ratio"] - 1) <= RATIO_TOL
+    rel = (len(data) / len(blob)) / ref["ratio"] - 1
+    print(f"{name}: ratio {len(data) / len(blob):.5f} vs reference {ref['ratio']:.5f} "
+          f"({100 * rel:+.3f}%)")
+    assert abs(rel) <= RATIO_TOL
     assert decompress(read_container(blob)) == data
 
 
