@@ -111,6 +111,8 @@ int edpc_ctx_destroy(edpc_ctx* ctx);
 #define EDPC_NUM_TCGEN05 1   /* tcgen05 tensor-core GEMMs (tf32 operands)          */
 #define EDPC_NUM_FP16 2      /* fp16 operands for the MBRB branch / out-projection */
 #define EDPC_NUM_LTE_FUSED 4 /* fused LTE forward kernel (mma.sync tf32, rna)      */
+#define EDPC_NUM_RND_TF32 8  /* tf32 GEMM operands rounded to nearest (a rounded   */
+                             /* weight shadow; producers store rounded operands)   */
 int edpc_ctx_numerics(edpc_ctx* ctx, int32_t* flags);
 int edpc_ctx_info(edpc_ctx* ctx, int64_t* lane_len, int64_t* n_params, int64_t* n_shared);
 

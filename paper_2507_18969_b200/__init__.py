@@ -15,6 +15,8 @@ from .config import (ModelConfig, dense_mixer_param_count, lte_param_count, mode
 from .container import (BadMagicError, BadVersionError, ChecksumError, ContainerError,
                         EdpcContainer, FORMAT_VERSION, Header, InvalidHeaderError,
                         TruncatedError, header_size, read_container, write_container)
+from .archive import (ArchiveHeader, compress_chunked, decompress_chunked, is_archive,
+                      read_archive, write_archive)
 from .lanes import LaneSplit, join_lanes, split_lanes
 from .model import EdpcModel
 from .pipeline import compress, decompress
@@ -30,4 +32,6 @@ __all__ = [
     "InvalidHeaderError", "EdpcContainer", "Header", "FORMAT_VERSION", "header_size",
     "read_container", "write_container",
     "LaneSplit", "split_lanes", "join_lanes", "EdpcModel", "compress", "decompress",
+    "ArchiveHeader", "compress_chunked", "decompress_chunked", "is_archive", "read_archive",
+    "write_archive",
 ]

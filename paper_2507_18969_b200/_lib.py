@@ -17,8 +17,8 @@ LIB_PATH = os.path.join(PKG, "_edpc_b200.so")
 
 OK, ERR_INVALID, ERR_CUDA, ERR_CODER, ERR_STATE, ERR_NOMEM = range(6)
 # numerics flags (include/edpc_b200.h EDPC_NUM_*), recorded in the container
-NUM_TCGEN05, NUM_FP16, NUM_LTE_FUSED = 1, 2, 4
-NUMERICS_MASK = 7
+NUM_TCGEN05, NUM_FP16, NUM_LTE_FUSED, NUM_RND_TF32 = 1, 2, 4, 8
+NUMERICS_MASK = 15
 REGIONS = ["gemm", "fdm_fwd", "fdm_bwd_adam", "adam_shared", "softmax_quant", "encode",
            "decode", "colsum", "elementwise", "embed_grad"]
 

@@ -221,15 +221,22 @@ struct EpiBiasResid {
   const float* bias;
   const float* resid;
   int64_t ldr;
+  int rt = 0;  // output rounded to tf32 (it feeds a tf32 GEMM)
+  __device__ float rnd(float x) const {
+    if (!rt) return x;
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return __uint_as_float(r);
+  }
   __device__ void operator()(int, int, int m, int n, float acc) const {
-    C[(int64_t)m * ldc + n] = (acc + bias[n]) + resid[(int64_t)m * ldr + n];
+    C[(int64_t)m * ldc + n] = rnd((acc + bias[n]) + resid[(int64_t)m * ldr + n]);
   }
   __device__ void row32(int, int, int m, int n0, float (&v)[32]) const {
     float b[32], r[32];
     load32(bias + n0, b);
     load32(resid + (int64_t)m * ldr + n0, r);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = (v[j] + b[j]) + r[j];
+    for (int j = 0; j < 32; ++j) v[j] = rnd((v[j] + b[j]) + r[j]);
     store32(C + (int64_t)m * ldc + n0, v);
   }
   __device__ void tile(const float* T, int, int, int m_base, int n0, int M) const {
@@ -244,7 +251,7 @@ struct EpiBiasResid {
       rv[r] = m_base + r < M ? R[(int64_t)(m_base + r) * ldr + n] : 0.f;
 #pragma unroll
     for (int r = 0; r < 32; ++r)
-      if (m_base + r < M) O[(int64_t)(m_base + r) * ldc + n] = (T[r * 32 + (lane ^ r)] + b) + rv[r];
+      if (m_base + r < M) O[(int64_t)(m_base + r) * ldc + n] = rnd((T[r * 32 + (lane ^ r)] + b) + rv[r]);
   }
 };
 

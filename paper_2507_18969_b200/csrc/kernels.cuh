@@ -28,6 +28,17 @@ struct StepIdx {
   __device__ __forceinline__ int64_t T() const { return *t + off; }
 };
 
+// fp32 -> the nearest tf32 value (10-bit mantissa, ties away from zero),
+// returned as fp32.  tcgen05 kind::tf32 *truncates* fp32 operands, a bias of
+// -2^-12 per operand that does not average out over a K-long dot product
+// (measured: max |dp| 3e-3 vs the fp64 oracle on a trained C4a model); GEMM
+// operands are therefore stored pre-rounded (numerics bit EDPC_NUM_RND_TF32).
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 // GeLU and its derivative together (_kernels.py:35-51, exact-erf GeLU):
 //   GeLU(x) = x Phi(x),  GeLU'(x) = Phi(x) + x phi(x),  Phi(x) = (1 + erf(x/sqrt2)) / 2.
 // erf by Abramowitz & Stegun 7.1.26 (|error| <= 1.5e-7), whose e^{-x^2/2}
@@ -69,7 +80,7 @@ __global__ void __launch_bounds__(256)
 k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE, int F, int Bl,
            float* __restrict__ x, const float* __restrict__ gain, const float* __restrict__ bias,
            float* __restrict__ xhat, float* __restrict__ rstd, float* __restrict__ x0,
-           __half* __restrict__ x0h) {
+           __half* __restrict__ x0h, int rt) {
   pdl_entry();
   const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -104,7 +115,7 @@ k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE,
       if (x0h)
         x0h[(int64_t)b * F + f] = __float2half_rn(v);
       else
-        x0[(int64_t)b * F + f] = v;
+        x0[(int64_t)b * F + f] = rt ? tf32_rna(v) : v;
     }
     if (lane == 0) rstd[b] = r;
     return;
@@ -153,8 +164,8 @@ k_embed_ln(ByteCols src, StepIdx si, int T, const float* __restrict__ E, int DE,
       const float o = h * gain[f] + bias[f];
       if (x0h)  // fp16 GEMM path: x0 only feeds the branch GEMM and its weight gradient
         x0h[(int64_t)b * F + f] = __float2half_rn(o);
-      else
-        x0[(int64_t)b * F + f] = o;
+      else  // tf32 GEMM operand: stored rounded to nearest (rt)
+        x0[(int64_t)b * F + f] = rt ? tf32_rna(o) : o;
     }
   }
   if (lane == 0) rstd[b] = r;
@@ -166,7 +177,8 @@ constexpr int kMaxBranches = 8;
 // ff = GeLU(prod_z H_z) (model.py:98-101, _kernels.py:35-42).  H_z is then
 // overwritten with D_z = GeLU'(prod) * prod_{j != z} H_j, everything the
 // backward product rule needs (model.py:107-119): g_H_z = g_ff * D_z.
-__global__ void k_mbrb_act(float* __restrict__ H, int K, int64_t plane, float* __restrict__ ff) {
+__global__ void k_mbrb_act(float* __restrict__ H, int K, int64_t plane, float* __restrict__ ff,
+                           int rt) {
   pdl_entry();
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= plane) return;
@@ -179,7 +191,7 @@ __global__ void k_mbrb_act(float* __restrict__ H, int K, int64_t plane, float* _
   }
   float fv, dg;
   gelu_pair(p, fv, dg);
-  ff[e] = fv;
+  ff[e] = rt ? tf32_rna(fv) : fv;  // out-projection GEMM operand
   for (int z = 0; z < K; ++z) {
     float d = dg;
     for (int j = 0; j < K; ++j)
@@ -198,6 +210,7 @@ struct EpiBranchAct {
   float* ff;        // [M][N]
   const float* b0;  // bias of branch 0; branch z at b0 + z*sBias
   int64_t sBias, N, plane;
+  int rt = 0;       // ff stored rounded to tf32 (it is the out-projection's A operand)
   // map 0: D_z as (n, m, z); map 1: ff
   bool store_maps(const TcShape& s, TcStoreMap& c, TcStoreMap& d) const {
     c = TcStoreMap{H, {(uint64_t)N, (uint64_t)s.M, (uint64_t)ZIN, 1}, {(uint64_t)N, (uint64_t)plane, 0}};
@@ -221,6 +234,7 @@ struct EpiBranchAct {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         gelu_pair(p[j], f[j], p[j]);
+        if (rt) f[j] = tf32_rna(f[j]);
       }
       io.put(1, f, 0, 0);
     }
@@ -252,6 +266,7 @@ struct EpiBranchAct {
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       gelu_pair(p[j], f[j], p[j]);
+      if (rt) f[j] = tf32_rna(f[j]);
     }
     store32(ff + (int64_t)m * N + n0, f);
 #pragma unroll
@@ -292,7 +307,7 @@ struct EpiBranchAct {
       }
       float fv, dg;
       gelu_pair(p, fv, dg);
-      ff[e] = fv;
+      ff[e] = rt ? tf32_rna(fv) : fv;
 #pragma unroll
       for (int z = 0; z < ZIN; ++z) {
         float d = dg;
@@ -400,6 +415,7 @@ struct EpiBranchActH {
   __half* ff;       // [M][N]
   const float* b0;  // bias of branch 0; branch z at b0 + z*sBias
   int64_t sBias, N, plane;
+  int rt = 0;       // ff stored rounded to tf32 (it is the out-projection's A operand)
   bool store_maps(const TcShape& s, TcStoreMap& c, TcStoreMap& d) const {
     c = TcStoreMap{H, {(uint64_t)N, (uint64_t)s.M, (uint64_t)ZIN, 1}, {(uint64_t)N, (uint64_t)plane, 0}, 1};
     d = TcStoreMap{ff, {(uint64_t)N, (uint64_t)s.M, 1, 1}, {(uint64_t)N, 0, 0}, 1};
@@ -698,7 +714,7 @@ k_colsum_groups(const float* __restrict__ src, int64_t ld, int64_t sz,
 // mixed_b = down_b . U_b (nn.py:168-174); one warp per lane
 __global__ void __launch_bounds__(256)
 k_fdm_fwd(const float* __restrict__ down, const float* __restrict__ U, float* __restrict__ mixed,
-          int FP, int Bl) {
+          int FP, int Bl, int rt) {
   pdl_entry();
   const int b = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -708,7 +724,7 @@ k_fdm_fwd(const float* __restrict__ down, const float* __restrict__ U, float* __
   for (int j = lane; j < FP; j += 32) {
     float acc = 0.f;
     for (int i = 0; i < FP; ++i) acc = fmaf(d[i], u[(int64_t)i * FP + j], acc);
-    mixed[(int64_t)b * FP + j] = acc;
+    mixed[(int64_t)b * FP + j] = rt ? tf32_rna(acc) : acc;  // up-projection operand
   }
 }
 
@@ -800,7 +816,7 @@ struct FdmGeo {
 template <int FP>
 __global__ void __launch_bounds__(256)
 k_fdm_fwd_v(const float* __restrict__ down, const float* __restrict__ U, float* __restrict__ mixed,
-            int Bl) {
+            int Bl, int rt) {
   pdl_entry();
   using G = FdmGeo<FP>;
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -827,7 +843,13 @@ k_fdm_fwd_v(const float* __restrict__ down, const float* __restrict__ U, float* 
   }
   float4* out = reinterpret_cast<float4*>(mixed + (int64_t)b * FP);
 #pragma unroll
-  for (int v = 0; v < G::kNV; ++v) out[v * G::kTPR + t] = acc[v];
+  for (int v = 0; v < G::kNV; ++v) {
+    if (rt) {  // up-projection operand
+      acc[v].x = tf32_rna(acc[v].x); acc[v].y = tf32_rna(acc[v].y);
+      acc[v].z = tf32_rna(acc[v].z); acc[v].w = tf32_rna(acc[v].w);
+    }
+    out[v * G::kTPR + t] = acc[v];
+  }
 }
 
 // GX: g_down_b = U_b g_b with the old U (nn.py:177-179); ADAM: U_b's
@@ -1051,6 +1073,13 @@ __global__ void k_embed_grad_reduce(const float* __restrict__ sub, const int* __
 
 // ------------------------------------------------------- fp16 helpers
 
+__global__ void k_to_tf32(const float* __restrict__ src, float* __restrict__ dst, int64_t n) {
+  pdl_entry();
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    dst[e] = tf32_rna(src[e]);
+}
+
 __global__ void k_to_half(const float* __restrict__ src, __half* __restrict__ dst, int64_t n) {
   pdl_entry();
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
@@ -1082,7 +1111,7 @@ template <int NL>
 __global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, float* __restrict__ V,
                               const float* __restrict__ P, int64_t n, int64_t pstride, StepIdx si,
                               AdamConsts c, double b1d, double b2d, float ginv,
-                              __half* __restrict__ Wh) {
+                              __half* __restrict__ Wh, float* __restrict__ Wt) {
   pdl_entry();
   float bc1, bc2;
   adam_bc(c, b1d, b2d, si.T(), bc1, bc2);
@@ -1096,6 +1125,7 @@ __global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, floa
     adam_elem(w, m, v, grad, c, bc1, bc2);
     W[e] = w;
     if (Wh) Wh[e] = __float2half_rn(w);  // fp16 shadow for the fp16 GEMMs
+    if (Wt) Wt[e] = tf32_rna(w);         // tf32-rounded shadow for the tf32 GEMMs
     M[e] = m;
     V[e] = v;
   }
@@ -1273,6 +1303,20 @@ __global__ void k_encode_finish_all(int64_t* __restrict__ enc_state, uint32_t* _
   stp[3] = (int64_t)w.bitpos;
 }
 
+// Container assembly on the device: segment s's finished
+// bitstream (its bytes, in stream order, at words + s * cap_words) is copied to
+// out + off[s], so the whole payload area of the container leaves the GPU in
+// one D2H copy instead of one per segment.  One block per segment.
+__global__ void k_pack_payloads(const uint32_t* __restrict__ words, int64_t cap_words,
+                                const int64_t* __restrict__ off, uint8_t* __restrict__ out, int Sl) {
+  pdl_entry();
+  const int s = blockIdx.x;
+  if (s >= Sl) return;
+  const uint8_t* src = reinterpret_cast<const uint8_t*>(words + (int64_t)s * cap_words);
+  const int64_t o = off[s], nb = off[s + 1] - o;
+  for (int64_t k = threadIdx.x; k < nb; k += blockDim.x) out[o + k] = src[k];
+}
+
 __global__ void k_decoder_init_all(int64_t* __restrict__ dec_state, const uint8_t* __restrict__ pay,
                                    const int64_t* __restrict__ pay_off,
                                    const int64_t* __restrict__ bits, int Sl) {
@@ -1390,7 +1434,7 @@ struct EpiSplit {
 // the reduction of a split-K GEMM, fused with its bias/residual epilogue.
 __global__ void k_splitk_reduce(const float* __restrict__ ws, int nsplit, int64_t plane, int N,
                                 const float* __restrict__ bias, const float* __restrict__ resid,
-                                float* __restrict__ out) {
+                                float* __restrict__ out, int rt) {
   pdl_entry();
   const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (e >= plane) return;
@@ -1418,6 +1462,9 @@ __global__ void k_splitk_reduce(const float* __restrict__ ws, int nsplit, int64_
   }
   if (resid) {
     a.x += r.x; a.y += r.y; a.z += r.z; a.w += r.w;
+  }
+  if (rt) {  // the MBRB output feeds a tf32 GEMM (LTE down-projection / head)
+    a.x = tf32_rna(a.x); a.y = tf32_rna(a.y); a.z = tf32_rna(a.z); a.w = tf32_rna(a.w);
   }
   *reinterpret_cast<float4*>(out + e) = a;
 }

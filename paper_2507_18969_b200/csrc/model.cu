@@ -222,6 +222,10 @@ struct edpc_ctx {
   // fp16 GEMM path for the MBRB branch / out-projection GEMMs (see ctx_create)
   bool h16 = false;
   bool lte_fwd = false;  // fused LTE forward kernel (numerics bit 2)
+  // tf32 GEMM operands rounded to nearest (numerics bit 3): weights from the
+  // tf32-rounded shadow Wt, activations stored rounded by their producers
+  bool rt = false;
+  float* Wt = nullptr;
   int gs_log2 = 0;                                  // gradient scale 2^gs_log2 (k_dlogits)
   __half* Wh = nullptr;                             // fp16 shadow of the shared weights
   __half *guph_l = nullptr, *guph_g = nullptr;      // fp16 copies of g_up per MBRB
@@ -264,6 +268,8 @@ struct edpc_ctx {
   uint32_t* enc_words = nullptr;
   int64_t enc_cap_words = 0;
   uint8_t* payload = nullptr;
+  uint8_t* packed = nullptr;  // assembled payload area (compress_finish)
+  int64_t packed_bytes = 0;
   int64_t *pay_off = nullptr, *bit_len = nullptr;
   int* dec_err = nullptr;
   // host bookkeeping
@@ -322,7 +328,11 @@ namespace edpc {
 
 constexpr int kTf32MinLanes = 1024;
 // numerics flags (edpc_ctx_numerics / edpc_ctx_create_ex, container header)
-constexpr int kNumTc = 1, kNumF16 = 2, kNumLteFused = 4, kNumericsMask = 7;
+constexpr int kNumTc = 1, kNumF16 = 2, kNumLteFused = 4, kNumRndTf32 = 8, kNumericsMask = 15;
+
+// B operand of a tf32 GEMM: the tf32-rounded weight shadow when the context
+// rounds tf32 operands (numerics bit 3), else the fp32 master weights
+static const float* wt(const edpc_ctx* c) { return c->rt ? c->Wt : c->W; }
 
 constexpr int kFdmWarps = 2;  // warps per block of the per-lane FDM kernels
 
@@ -413,11 +423,11 @@ static bool use_split(int N, int64_t Ktot, int Kd) {
 }
 
 static cudaError_t splitk_reduce(edpc_ctx* c, int N, const float* bias, const float* resid,
-                                 float* out) {
+                                 float* out, int rt) {
   const int64_t plane = (int64_t)c->Bl * N;
   Scope sc(c, kRegElem, c->st);
   pdl_launch(k_splitk_reduce, (unsigned)cdiv(plane / 4, 256), 256, 0, c->st, c->ws, kSplitK, plane, N, bias,
-                                                                    resid, out);
+                                                                    resid, out, rt);
   return cudaGetLastError();
 }
 
@@ -427,7 +437,7 @@ static cudaError_t splitk_reduce(edpc_ctx* c, int N, const float* bias, const fl
 // stay resident to reduce hold SMs the side-stream weight-gradient GEMMs need.)
 template <bool AMN, bool BMN, bool H = false>
 static cudaError_t split_gemm(edpc_ctx* c, const TcShape& s, const TcOperand& a, const TcOperand& b,
-                              const float* bias, const float* resid, float* out) {
+                              const float* bias, const float* resid, float* out, int rt = 0) {
   const int N = s.N;
   const int64_t plane = (int64_t)c->Bl * N;
   {
@@ -435,7 +445,7 @@ static cudaError_t split_gemm(edpc_ctx* c, const TcShape& s, const TcOperand& a,
     int st = tc_gemm<AMN, BMN, H>(s, a, b, EpiSplit{c->ws, N, plane}, c->st);
     if (st != EDPC_OK) return cudaErrorUnknown;
   }
-  return splitk_reduce(c, N, bias, resid, out);
+  return splitk_reduce(c, N, bias, resid, out, rt);
 }
 
 // out[Bl][N] = A[Bl][Kd] . W[Kd][N] (+ bias) over nzb batches (weights at
@@ -447,11 +457,12 @@ static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, cons
     TcOperand a{A, lda, 0, 1}, b{w, N, sW, nzb};
     if (nzb == 1 && M == c->Bl && use_split(N, Kd, Kd)) {
       TcShape s{M, N, Kd, 1, 1, kBatchNone, kBatchNone, 2, kSplitK, 0, 0, 0};
-      return split_gemm<false, true>(c, s, a, b, bias, resid, out);
+      return split_gemm<false, true>(c, s, a, b, bias, resid, out, resid ? c->rt : 0);
     }
     Scope sc(c, kRegGemm, c->st);
     TcShape s{M, N, Kd, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 0, 1, 0, 0, 0};
-    if (resid) return as_cuda(tc_gemm<false, true>(s, a, b, EpiBiasResid{out, N, bias, resid, N}, c->st));
+    if (resid)
+      return as_cuda(tc_gemm<false, true>(s, a, b, EpiBiasResid{out, N, bias, resid, N, c->rt}, c->st));
     return as_cuda(tc_gemm<false, true>(s, a, b, EpiBias{out, N, sOut, bias, sW}, c->st));
   }
   Scope sc(c, kRegGemm, c->st);
@@ -466,7 +477,7 @@ static cudaError_t fwd_linear(edpc_ctx* c, const float* A, int lda, int Kd, cons
   g.sB = sW;
   g.nzb = nzb;
   g.nsum = 1;
-  if (resid) return gemm_simt<false, false>(g, EpiBiasResid{out, N, bias, resid, N}, c->st);
+  if (resid) return gemm_simt<false, false>(g, EpiBiasResid{out, N, bias, resid, N, c->rt}, c->st);
   return gemm_simt<false, false>(g, EpiBias{out, N, sOut, bias, sW}, c->st);
 }
 
@@ -608,12 +619,13 @@ static cudaError_t fwd_linear_h(edpc_ctx* c, const __half* A, int Kd, const __ha
   TcOperand a{A, Kd, 0, 1}, b{w, N, 0, 1};
   if (N <= 256 && N % 4 == 0 && Kd >= 1024 && Kd % (kSplitK * tc_bk<true>()) == 0) {
     TcShape s{M, N, Kd, 1, 1, kBatchNone, kBatchNone, 2, kSplitK, 0, 0, 0};
-    return split_gemm<false, true, true>(c, s, a, b, bias, resid, out);
+    return split_gemm<false, true, true>(c, s, a, b, bias, resid, out, resid ? c->rt : 0);
   }
   Scope sc(c, kRegGemm, c->st);
   TcShape s{M, N, Kd, 1, 1, kBatchNone, kBatchNone, 0, 1, 0, 0, 0};
   if (resid)
-    return as_cuda(tc_gemm<false, true, true>(s, a, b, EpiBiasResid{out, N, bias, resid, N}, c->st));
+    return as_cuda(
+        tc_gemm<false, true, true>(s, a, b, EpiBiasResid{out, N, bias, resid, N, c->rt}, c->st));
   return as_cuda(tc_gemm<false, true, true>(s, a, b, EpiBias{out, N, 0, bias, 0}, c->st));
 }
 
@@ -680,11 +692,11 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
     if (gather)
       pdl_launch(k_embed_ln<true>, g8, 256, 0, c->st, src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
                                               c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0,
-                                              x0h);
+                                              x0h, (int)c->rt);
     else
       pdl_launch(k_embed_ln<false>, g8, 256, 0, c->st, src, c->si(), L.T, c->W + L.emb, L.DE, F, Bl, b.x,
                                                c->W + o.ln_g, c->W + o.ln_b, b.xhat, b.rstd, b.x0,
-                                               x0h);
+                                               x0h, (int)c->rt);
     CK(cudaGetLastError());
   }
   const int64_t plane = (int64_t)Bl * H;
@@ -706,24 +718,28 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
   // branch GEMMs with the product + GeLU fused into the epilogue when all
   // branches of a tile fit one CTA's TMEM (k = 2, 3); else GEMM + k_mbrb_act
   if ((L.K == 2 || L.K == 3) && H % 128 == 0 &&
-      tc_ok_m(c, 1, H, F, {b.x0, c->W + o.w0, b.H, b.ff, c->W + o.b0}, {F, H, o.wstride, plane})) {
+      tc_ok_m(c, 1, H, F, {b.x0, wt(c) + o.w0, b.H, b.ff, c->W + o.b0}, {F, H, o.wstride, plane})) {
     Scope sc(c, kRegGemm, c->st);
     TcShape s{Bl, H, F, L.K, 1, kBatchNone, kBatchZ, 0, 1, 0, 0, 0};
-    TcOperand a{b.x0, F, 0, 1}, bw{c->W + o.w0, H, o.wstride, L.K};
+    TcOperand a{b.x0, F, 0, 1}, bw{wt(c) + o.w0, H, o.wstride, L.K};
+    const int rt = c->rt;
     const int st =
         L.K == 2 ? tc_launch_zin<128, 2, true>(
-                       s, a, bw, EpiBranchAct<2>{b.H, b.ff, c->W + o.b0, o.wstride, H, plane}, c->st)
+                       s, a, bw, EpiBranchAct<2>{b.H, b.ff, c->W + o.b0, o.wstride, H, plane, rt},
+                       c->st)
                  : tc_launch_zin<64, 3, true>(
-                       s, a, bw, EpiBranchAct<3>{b.H, b.ff, c->W + o.b0, o.wstride, H, plane}, c->st);
+                       s, a, bw, EpiBranchAct<3>{b.H, b.ff, c->W + o.b0, o.wstride, H, plane, rt},
+                       c->st);
     if (st != EDPC_OK) return st;
   } else {
-    CK(fwd_linear(c, b.x0, F, F, c->W + o.w0, H, L.K, o.wstride, b.H, plane, c->W + o.b0, nullptr,
+    CK(fwd_linear(c, b.x0, F, F, wt(c) + o.w0, H, L.K, o.wstride, b.H, plane, c->W + o.b0, nullptr,
                   Bl));
     Scope sc_(c, kRegElem, c->st);
-    pdl_launch(k_mbrb_act, (unsigned)cdiv(plane, 256), 256, 0, c->st, b.H, L.K, plane, b.ff);
+    pdl_launch(k_mbrb_act, (unsigned)cdiv(plane, 256), 256, 0, c->st, b.H, L.K, plane, b.ff,
+               (int)c->rt);
     CK(cudaGetLastError());
   }
-  CK(fwd_linear(c, b.ff, H, H, c->W + o.out_w, F, 1, 0, b.out, 0, c->W + o.out_b, b.x, Bl));
+  CK(fwd_linear(c, b.ff, H, H, wt(c) + o.out_w, F, 1, 0, b.out, 0, c->W + o.out_b, b.x, Bl));
   return EDPC_OK;
 }
 
@@ -758,7 +774,7 @@ static int forward(edpc_ctx* c, ByteCols src) {
                c->down, c->mixed, c->x_lte, Bl);
     CK(cudaGetLastError());
   } else {
-  CK(fwd_linear(c, c->x_local, L.F, L.F, c->W + L.down_w, L.FP, 1, 0, c->down, 0,
+  CK(fwd_linear(c, c->x_local, L.F, L.F, wt(c) + L.down_w, L.FP, 1, 0, c->down, 0,
                 c->W + L.down_b, nullptr, Bl));
   {
     Scope sc_(c, kRegFdmFwd, c->st);
@@ -768,22 +784,26 @@ static int forward(edpc_ctx* c, ByteCols src) {
     const int lpw = 32 / std::min(32, L.FP / 4);
     const unsigned blocks = (unsigned)cdiv(cdiv(Bl, lpw), kFdmWarps);
     if (L.FP == 64)
-      pdl_launch(k_fdm_fwd_v<64>, blocks, 32 * kFdmWarps, 0, c->st, c->down, c->U, c->mixed, Bl);
+      pdl_launch(k_fdm_fwd_v<64>, blocks, 32 * kFdmWarps, 0, c->st, c->down, c->U, c->mixed, Bl,
+                 (int)c->rt);
     else if (L.FP == 128)
-      pdl_launch(k_fdm_fwd_v<128>, blocks, 32 * kFdmWarps, 0, c->st, c->down, c->U, c->mixed, Bl);
+      pdl_launch(k_fdm_fwd_v<128>, blocks, 32 * kFdmWarps, 0, c->st, c->down, c->U, c->mixed, Bl,
+                 (int)c->rt);
     else
-      pdl_launch(k_fdm_fwd_v<256>, blocks, 32 * kFdmWarps, 0, c->st, c->down, c->U, c->mixed, Bl);
+      pdl_launch(k_fdm_fwd_v<256>, blocks, 32 * kFdmWarps, 0, c->st, c->down, c->U, c->mixed, Bl,
+                 (int)c->rt);
   } else {
-    pdl_launch(k_fdm_fwd, (unsigned)cdiv(Bl, 8), 256, 0, c->st, c->down, c->U, c->mixed, L.FP, Bl);
+    pdl_launch(k_fdm_fwd, (unsigned)cdiv(Bl, 8), 256, 0, c->st, c->down, c->U, c->mixed, L.FP, Bl,
+               (int)c->rt);
   }
   }
   CK(cudaGetLastError());
-  CK(fwd_linear(c, c->mixed, L.FP, L.FP, c->W + L.up_w, L.F, 1, 0, c->x_lte, 0, c->W + L.up_b,
+  CK(fwd_linear(c, c->mixed, L.FP, L.FP, wt(c) + L.up_w, L.F, 1, 0, c->x_lte, 0, c->W + L.up_b,
                 nullptr, Bl));
   }
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
   EDPC_TRY(mbrb_forward(c, L.glo, gb, false, src));
-  CK(fwd_linear(c, c->x_global, L.F, L.F, c->W + L.head_w, 256, 1, 0, c->logits, 0,
+  CK(fwd_linear(c, c->x_global, L.F, L.F, wt(c) + L.head_w, 256, 1, 0, c->logits, 0,
                 c->W + L.head_b, nullptr, Bl));
   return EDPC_OK;
 }
@@ -836,13 +856,13 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
     CK(dgrad_h(c, GHh, H, K, plane, c->Wh + o.w0, o.wstride, F, c->gx0));
   } else {
   // g_ff = g_up . out_w^T, epilogue -> GH[z] (product rule + GeLU')
-  CK(dgrad(c, g_up, F, 1, 0, c->W + o.out_w, 0, H, EpiBwdAct{b.H, GH, K, plane, H}));
+  CK(dgrad(c, g_up, F, 1, 0, wt(c) + o.out_w, 0, H, EpiBwdAct{b.H, GH, K, plane, H}));
   // weight gradients on the side stream: out_w/out_b, branch weights/biases
   CK(fork_aux(c));
   CK(wgrad(c, b.ff, H, g_up, F, 1, 0, o.out_w, 0, o.out_b));
   CK(wgrad(c, b.x0, F, GH, H, K, plane, o.w0, o.wstride, o.b0));
   // g_x0 = sum_z GH[z] . W_z^T
-  CK(dgrad(c, GH, H, K, plane, c->W + o.w0, o.wstride, F, EpiStore{c->gx0, F}));
+  CK(dgrad(c, GH, H, K, plane, wt(c) + o.w0, o.wstride, F, EpiStore{c->gx0, F}));
   }
   // LN backward + residual, with the LN gain / bias gradient partials
   if (F <= kLnMaxF && c->g_count > 0) {
@@ -883,9 +903,9 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
   CK(fork_aux(c));
   CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0, L.head_b));
   if (c->h16)
-    CK(dgrad(c, c->gl, 256, 1, 0, c->W + L.head_w, 0, F, EpiStore2{c->g_head, c->guph_g, F}));
+    CK(dgrad(c, c->gl, 256, 1, 0, wt(c) + L.head_w, 0, F, EpiStore2{c->g_head, c->guph_g, F}));
   else
-    CK(dgrad(c, c->gl, 256, 1, 0, c->W + L.head_w, 0, F, EpiStore{c->g_head, F}));
+    CK(dgrad(c, c->gl, 256, 1, 0, wt(c) + L.head_w, 0, F, EpiStore{c->g_head, F}));
   // global MBRB: d(x_global) -> d(x_lte)
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
   EDPC_TRY(mbrb_backward(c, L.glo, gb, c->g_head, c->g_lte, c->GH_g, c->guph_g));
@@ -897,7 +917,7 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
   CK(fork_aux(c));
   CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
   {
-    CK(dgrad(c, c->g_lte, F, 1, 0, c->W + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
+    CK(dgrad(c, c->g_lte, F, 1, 0, wt(c) + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
     // per-lane FDM: g_down with the old U, then U's Adam step (fused: U read once)
     {
       if (FP == 64 || FP == 128 || FP == 256) {
@@ -930,9 +950,9 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
     CK(fork_aux(c));
     CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
     if (c->h16)
-      CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore2{c->g_loc, c->guph_l, F}));
+      CK(dgrad(c, c->gdown, FP, 1, 0, wt(c) + L.down_w, 0, F, EpiStore2{c->g_loc, c->guph_l, F}));
     else
-      CK(dgrad(c, c->gdown, FP, 1, 0, c->W + L.down_w, 0, F, EpiStore{c->g_loc, F}));
+      CK(dgrad(c, c->gdown, FP, 1, 0, wt(c) + L.down_w, 0, F, EpiStore{c->g_loc, F}));
   }
   if (early_adam(c)) {  // LTE down + up
     CK(fork_aux(c));
@@ -1008,7 +1028,8 @@ static void adam_launch(edpc_ctx* c, int blocks, cudaStream_t st, int64_t off, i
                         int64_t pstride) {
   pdl_launch(k_adam_shared<NL>, blocks, 256, 0, st, c->W + off, c->M + off, c->V + off,
              c->Gp + off, len, pstride, c->si(), c->adam, c->cfg.beta1, c->cfg.beta2,
-             ldexpf(1.0f, -c->gs_log2), c->h16 ? c->Wh + off : nullptr);
+             ldexpf(1.0f, -c->gs_log2), c->h16 ? c->Wh + off : nullptr,
+             c->rt ? c->Wt + off : nullptr);
 }
 
 // Adam over shared params [off, off + len) on stream st; nl leaves at stride
@@ -1112,6 +1133,10 @@ static int exchange_weights(edpc_ctx* c) {
   if (c->h16) {
     e = nccl().allGather(c->Wh + r * s, c->Wh, s, ncclHalf, c->comm, c->st);
     if (e != ncclSuccess) return nccl_fail("ncclAllGather(Wh)", e);
+  }
+  if (c->rt) {
+    e = nccl().allGather(c->Wt + r * s, c->Wt, s, ncclFloat, c->comm, c->st);
+    if (e != ncclSuccess) return nccl_fail("ncclAllGather(Wt)", e);
   }
   return EDPC_OK;
 }
@@ -1306,12 +1331,14 @@ int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t origina
       c->use_tc = tc_ok_cfg && cfg->lanes >= kTf32MinLanes;
       c->h16 = c->use_tc && h16_ok;
       c->lte_fwd = lte_fused_possible(c);
+      c->rt = c->use_tc;
     } else {
       c->use_tc = (numerics & kNumTc) != 0;
       c->h16 = (numerics & kNumF16) != 0;
       c->lte_fwd = (numerics & kNumLteFused) != 0;
+      c->rt = (numerics & kNumRndTf32) != 0;
       const bool ok = (!c->use_tc || tc_ok_cfg) && (!c->h16 || (c->use_tc && h16_ok)) &&
-                      (!c->lte_fwd || lte_fused_possible(c));
+                      (!c->lte_fwd || lte_fused_possible(c)) && (!c->rt || c->use_tc);
       if (!ok) {
         delete c;
         set_error("numerics flags " + std::to_string(numerics) +
@@ -1384,6 +1411,7 @@ int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t origina
   A_(c->g_emb, Bl * F);
   A_(c->GH_g, (int64_t)L.K * Bl * L.HG);
   A_(c->GH_l, (int64_t)L.K * Bl * L.HL);
+  if (c->rt) A_(c->Wt, L.n_shared + kShardPad);
   if (c->h16) {
     A_(c->Wh, L.n_shared + kShardPad);
     A_(c->guph_l, Bl * F);
@@ -1473,7 +1501,8 @@ int edpc_ctx_destroy(edpc_ctx* ctx) {
 
 int edpc_ctx_numerics(edpc_ctx* c, int32_t* flags) {
   EDPC_CHECK_ARG(c && flags, "null argument");
-  *flags = (c->use_tc ? kNumTc : 0) | (c->h16 ? kNumF16 : 0) | (c->lte_fwd ? kNumLteFused : 0);
+  *flags = (c->use_tc ? kNumTc : 0) | (c->h16 ? kNumF16 : 0) | (c->lte_fwd ? kNumLteFused : 0) |
+           (c->rt ? kNumRndTf32 : 0);
   return EDPC_OK;
 }
 
@@ -1497,6 +1526,12 @@ int edpc_load_params(edpc_ctx* c, const float* params, int64_t count) {
                            (L.n_shared - L.ref_lane_mats) * 4, cudaMemcpyHostToDevice));
   EDPC_CUDA_TRY(cudaMemcpy(c->U, params + L.ref_lane_mats + (int64_t)c->lane0 * L.fdm,
                            (int64_t)c->Bl * L.fdm * 4, cudaMemcpyHostToDevice));
+  if (c->rt) {  // the tf32-rounded weight shadow starts from the loaded weights
+    pdl_launch(k_to_tf32, (unsigned)std::min<int64_t>(cdiv(L.n_shared, 256), 148 * 8), 256, 0, c->st,
+               c->W, c->Wt, L.n_shared);
+    EDPC_CUDA_TRY(cudaGetLastError());
+    EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  }
   if (c->h16) {  // the fp16 weight shadow starts from the loaded weights
     pdl_launch(k_to_half, (unsigned)std::min<int64_t>(cdiv(L.n_shared, 256), 148 * 8), 256, 0, c->st, 
         c->W, c->Wh, L.n_shared);
@@ -1653,12 +1688,22 @@ int edpc_compress_finish(edpc_ctx* c, int64_t* bit_lengths, int64_t* total_bytes
   EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
   std::vector<int64_t> es(4 * (size_t)c->Sl);
   EDPC_CUDA_TRY(cudaMemcpy(es.data(), c->enc_state, es.size() * 8, cudaMemcpyDeviceToHost));
-  int64_t tot = 0;
+  std::vector<int64_t> off(c->Sl + 1, 0);
   for (int s = 0; s < c->Sl; ++s) {
     bit_lengths[s] = es[4 * s + 3];
-    tot += (es[4 * s + 3] + 7) / 8;
+    off[s + 1] = off[s] + (es[4 * s + 3] + 7) / 8;
   }
+  const int64_t tot = off[c->Sl];
   if (total_bytes) *total_bytes = tot;
+  // container assembly on the device: the segment payloads packed back to back
+  int r = c->alloc(&c->packed, tot + 1);
+  if (r != EDPC_OK) return r;
+  EDPC_CUDA_TRY(cudaMemcpy(c->pay_off, off.data(), (c->Sl + 1) * 8, cudaMemcpyHostToDevice));
+  pdl_launch(k_pack_payloads, (unsigned)c->Sl, 256, 0, c->st_enc, c->enc_words, c->enc_cap_words,
+             c->pay_off, c->packed, c->Sl);
+  EDPC_CUDA_TRY(cudaGetLastError());
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st_enc));
+  c->packed_bytes = tot;
   c->finished = true;
   return EDPC_OK;
 }
@@ -1670,17 +1715,9 @@ int edpc_get_payloads(edpc_ctx* c, uint8_t* out, int64_t cap) {
     return EDPC_ERR_STATE;
   }
   EDPC_CUDA_TRY(cudaSetDevice(c->device));
-  std::vector<int64_t> es(4 * (size_t)c->Sl);
-  EDPC_CUDA_TRY(cudaMemcpy(es.data(), c->enc_state, es.size() * 8, cudaMemcpyDeviceToHost));
-  int64_t pos = 0;
-  for (int s = 0; s < c->Sl; ++s) {
-    int64_t nb = (es[4 * s + 3] + 7) / 8;
-    EDPC_CHECK_ARG(pos + nb <= cap, "payload buffer too small");
-    if (nb)
-      EDPC_CUDA_TRY(cudaMemcpy(out + pos, c->enc_words + (int64_t)s * c->enc_cap_words, nb,
-                               cudaMemcpyDeviceToHost));
-    pos += nb;
-  }
+  EDPC_CHECK_ARG(c->packed_bytes <= cap, "payload buffer too small");
+  if (c->packed_bytes)  // one D2H of the assembled payload area
+    EDPC_CUDA_TRY(cudaMemcpy(out, c->packed, c->packed_bytes, cudaMemcpyDeviceToHost));
   return EDPC_OK;
 }
 
@@ -1859,7 +1896,8 @@ static int pull_ordered(edpc_ctx* dst, edpc_ctx* src, void* to, const void* from
 }
 
 static bool same_shard_set(const edpc_ctx* a, const edpc_ctx* b) {
-  return a->lay.n_shared == b->lay.n_shared && a->g_count == b->g_count && a->h16 == b->h16;
+  return a->lay.n_shared == b->lay.n_shared && a->g_count == b->g_count && a->h16 == b->h16 &&
+         a->rt == b->rt;
 }
 
 // Sharded-optimizer step 2 without NCCL (dist.ShardSet): dst <- src's subtree
@@ -1885,6 +1923,7 @@ int edpc_weights_pull(edpc_ctx* dst, edpc_ctx* src) {
   if (len <= 0) return EDPC_OK;
   EDPC_TRY(pull_ordered(dst, src, dst->W + off, src->W + off, (size_t)len * 4));
   if (src->h16) EDPC_TRY(pull_ordered(dst, src, dst->Wh + off, src->Wh + off, (size_t)len * 2));
+  if (src->rt) EDPC_TRY(pull_ordered(dst, src, dst->Wt + off, src->Wt + off, (size_t)len * 4));
   return EDPC_OK;
 }
 
@@ -2217,7 +2256,7 @@ int edpc_debug_adam(const float* w0, const float* grads, int64_t n, int32_t step
     if (e == cudaSuccess) e = cudaMemcpy(P, grads + (t - 1) * n, n * 4, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) {
       k_adam_shared<1><<<(unsigned)std::min<int64_t>(cdiv(n, 256), 1184), 256>>>(
-          W, M, V, P, n, n, StepIdx{d_t, d_t, 0}, a, beta1, beta2, 1.0f, nullptr);
+          W, M, V, P, n, n, StepIdx{d_t, d_t, 0}, a, beta1, beta2, 1.0f, nullptr, nullptr);
       e = cudaDeviceSynchronize();
     }
   }

@@ -80,10 +80,10 @@ class DeviceContext:
     def numerics(self) -> dict:
         """GEMM numerics of this context (policy: a function of the config):
         tensor cores (tf32), fp16 operands for the MBRB branch / out-projection
-        GEMMs, the fused LTE forward."""
+        GEMMs, the fused LTE forward, tf32 operands rounded to nearest."""
         f = self.numerics_flags()
         return {"tcgen05": bool(f & _lib.NUM_TCGEN05), "fp16_mbrb": bool(f & _lib.NUM_FP16),
-                "lte_fused": bool(f & _lib.NUM_LTE_FUSED)}
+                "lte_fused": bool(f & _lib.NUM_LTE_FUSED), "rnd_tf32": bool(f & _lib.NUM_RND_TF32)}
 
     def state_checksum(self) -> str:
         """sha256 over the fp32 parameter bytes (the lockstep probe, `model.py:294-300`)."""

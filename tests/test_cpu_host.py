@@ -124,11 +124,11 @@ def test_container_version_separates_numerics():
     c.header.numerics = 7
     b7 = write_container(c)
     assert b7[4] == 0x72 and read_container(b7).header.numerics == 7
-    c.header.numerics = 8
+    c.header.numerics = 16
     with pytest.raises(ContainerError):
         write_container(c)
     bad = bytearray(b7)
-    bad[4] = 0x82  # unknown flag
+    bad[4] = 0x73  # bad low nibble
     with pytest.raises(ContainerError):
         read_container(bytes(bad))
     v1 = write_container(_container(), version=1)
@@ -230,3 +230,29 @@ def test_library_does_not_preload_a_conflicting_nccl():
             "_lib.load(); import torch; print('ok')" % ROOT)
     r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+def test_archive_format_roundtrip_and_corruption():
+    """Chunked multi-container framing (archive.py): index round trip, every
+    single-byte index corruption and every truncation detected."""
+    from paper_2507_18969_b200.archive import (archive_header_size, read_archive,
+                                               write_archive)
+    blobs = [write_container(_container(S)) for S in (1, 2, 3)]
+    arc = write_archive(1000, 2500, blobs)
+    head, got = read_archive(arc)
+    assert got == blobs and head.chunk_count == 3
+    assert [head.chunk_span(k) for k in range(3)] == [(0, 1000), (1000, 2000), (2000, 2500)]
+    hs = archive_header_size(3)
+    for pos in range(hs):
+        bad = bytearray(arc)
+        bad[pos] ^= 0x5A
+        with pytest.raises(ContainerError):
+            read_archive(bytes(bad))
+    for cut in range(0, len(arc)):
+        with pytest.raises(ContainerError):
+            read_archive(arc[:cut])
+    with pytest.raises(ContainerError):
+        read_archive(arc + b"x")
+    with pytest.raises(ContainerError):
+        write_archive(1000, 2500, blobs[:2])  # chunk count must match the length
+    assert read_archive(write_archive(7, 0, []))[1] == []

@@ -29,7 +29,7 @@ def paper1024():
     cfg = ModelConfig(**PAPER, lanes=1024)
     data = synth.text_like(1024 * 56, 5)
     c = compress(data, cfg, 16)
-    assert c.header.numerics == 7, c.header.numerics
+    assert c.header.numerics == 15, c.header.numerics
     return cfg, data, write_container(c)
 
 

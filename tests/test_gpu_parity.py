@@ -34,10 +34,10 @@ ORACLE_LANES = 256  # probability check on an evenly spread lane sample (lanes a
 # (name, model dims, lanes, segments, stream kind, stream bytes, training steps,
 #  expected numerics flags)
 TRAINED = [
-    ("c2", PAPER, 4096, 256, "text", 4 << 20, 300, 7),
-    ("c4a", dict(PAPER, branches=1), 4096, 256, "text", 4 << 20, 300, 5),
-    ("c4b", dict(PAPER, lte_ratio=1), 4096, 256, "text", 4 << 20, 300, 3),
-    ("c3", PAPER, 32768, 1024, "mixed", 8 << 20, 200, 7),
+    ("c2", PAPER, 4096, 256, "text", 4 << 20, 300, 15),
+    ("c4a", dict(PAPER, branches=1), 4096, 256, "text", 4 << 20, 300, 13),
+    ("c4b", dict(PAPER, lte_ratio=1), 4096, 256, "text", 4 << 20, 300, 11),
+    ("c3", PAPER, 32768, 1024, "mixed", 8 << 20, 200, 15),
 ]
 
 
@@ -185,5 +185,6 @@ def test_device_adam_matches_reference_trajectory(golden):
                                            v.ctypes.data))
     # fp32 state vs the fp64 reference: a few ulp of drift per step
     assert np.abs(w - gd["value"]).max() <= 1e-6 + 1e-6 * np.abs(gd["value"]).max()
-    assert np.allclose(m, gd["m"], rtol=1e-5, atol=1e-9)
-    assert np.allclose(v, gd["v"], rtol=1e-5, atol=1e-12)
+    # moments: relative to their scale (m cancels through zero for some entries)
+    assert np.abs(m - gd["m"]).max() <= 1e-5 * np.abs(gd["m"]).max()
+    assert np.abs(v - gd["v"]).max() <= 1e-5 * np.abs(gd["v"]).max()

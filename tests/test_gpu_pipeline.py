@@ -209,3 +209,19 @@ def test_cli_round_trip_and_metrics(tmp_path):
     (corpus / "a.txt").write_bytes(data[:20_000])
     (corpus / "b.bin").write_bytes(_synth.generate("image", 20_000, 1))
     assert cli.main(["bench", "-i", str(corpus), *flags]) == cli.EXIT_OK
+
+
+def test_chunked_archive_roundtrip_replicas():
+    """§8f rank 3: one container per chunk; chunks spread over devices (here
+    two host threads on GPU 0) give the same archive as one device, and each
+    chunk equals the stand-alone container of its bytes."""
+    from paper_2507_18969_b200 import compress_chunked, decompress_chunked, read_archive
+    data = synth.generate("text", 70_000, 9)
+    cfg = ModelConfig(**DESK, lanes=32)
+    a1 = compress_chunked(data, cfg, 8, chunk_bytes=25_000)
+    a2 = compress_chunked(data, cfg, 8, chunk_bytes=25_000, devices=[0, 0])
+    assert a1 == a2
+    head, blobs = read_archive(a1)
+    assert head.chunk_count == 3
+    assert blobs[1] == write_container(compress(data[25_000:50_000], cfg, 8))
+    assert decompress_chunked(a2, devices=[0, 0]) == data

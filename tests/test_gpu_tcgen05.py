@@ -23,7 +23,7 @@ def _flags(cfg, tc: bool, f16: bool) -> int:
     fp16 MBRB operands, and the fused LTE forward wherever the tcgen05 path
     would use it (paper dims F = 256, F' = 64)."""
     lte = tc and cfg.feature_dim == 256 and cfg.feature_dim // cfg.lte_ratio == 64
-    return ((_lib.NUM_TCGEN05 if tc else 0) | (_lib.NUM_FP16 if f16 else 0)
+    return ((_lib.NUM_TCGEN05 | _lib.NUM_RND_TF32 if tc else 0) | (_lib.NUM_FP16 if f16 else 0)
             | (_lib.NUM_LTE_FUSED if lte else 0))
 
 
@@ -61,9 +61,10 @@ def test_f16_matches(ref):
     cfg = ModelConfig(**PAPER, lanes=1024)
     a = _ctx(cfg, True, f16=True)
     b = _ctx(cfg, ref == "tf32", f16=False)
-    assert a.numerics() == {"tcgen05": True, "fp16_mbrb": True, "lte_fused": True}
+    assert a.numerics() == {"tcgen05": True, "fp16_mbrb": True, "lte_fused": True,
+                            "rnd_tf32": True}
     assert b.numerics() == {"tcgen05": ref == "tf32", "fp16_mbrb": False,
-                            "lte_fused": ref == "tf32"}
+                            "lte_fused": ref == "tf32", "rnd_tf32": ref == "tf32"}
     _compare(cfg, a, b)
 
 
