@@ -197,6 +197,14 @@ int edpc_sync(edpc_ctx* ctx);
  * 11 shared Adam v, 12 per-lane FDM U.  count must equal the buffer's
  * element count. */
 int edpc_debug_read(edpc_ctx* ctx, int32_t which, float* out, int64_t count);
+/* IFR analytics (ifr.py:59-104 ksg_mi): KSG neighbour
+ * counts of already-jittered fp64 samples z [n][dz], y [n][dy] (dims <= 16,
+ * 1 <= k <= 32) under the Chebyshev norm, on `device`: count_z/count_y [n]
+ * (strict inequality against each sample's k-th joint distance, self
+ * excluded) and the number of samples whose k-th distance is 0. */
+int edpc_ksg_counts(const double* z, int32_t dz, const double* y, int32_t dy, int64_t n,
+                    int32_t k, int32_t device, int64_t* count_z, int64_t* count_y,
+                    int64_t* degenerate);
 /* the shared-parameter Adam kernel on host arrays: `steps` updates of w0 by
  * grads[t][n] (_kernels.py:18-32 adam_update; tests pin it to the reference) */
 int edpc_debug_adam(const float* w0, const float* grads, int64_t n, int32_t steps, double lr,

@@ -16,7 +16,10 @@ by calling the reference's own public functions on seeded inputs:
   and the lockstep checksums (``param_probe``);
 * pipeline.npz  -- whole v1 containers written by ``edpc.compress`` for the
   reference test-suite's tiny configuration on assorted inputs;
-* adam.npz      -- the fused Adam kernel's trajectory on a random buffer.
+* adam.npz      -- the fused Adam kernel's trajectory on a random buffer;
+* ifr.npz       -- ``edpc.ifr.ksg_mi`` estimates on seeded sample matrices
+  (correlated, scalar, duplicate-heavy and degenerate cases) and
+  ``edpc.ifr.digamma`` values.
 
 Files are small (< 1 MB total) and committed; their sha256s are in
 tests/golden/MANIFEST.json.
@@ -175,12 +178,41 @@ def gen_adam(rng):
     return dict(value0=v0, grads=grads, value=value, m=m, v=v)
 
 
+def gen_ifr(_rng):
+    from edpc.ifr import digamma, ksg_mi
+    rng = np.random.Generator(np.random.PCG64(7))
+    out = {}
+    cases = []
+    z = rng.standard_normal((700, 2))
+    cases.append((z, np.concatenate([0.8 * z[:, :1] + 0.6 * rng.standard_normal((700, 1)),
+                                     rng.standard_normal((700, 2))], 1), 5, 0))
+    z = rng.standard_normal((500, 1))
+    cases.append((z, 0.5 * z + rng.standard_normal((500, 1)), 1, 3))
+    z = np.round(rng.standard_normal((400, 1)), 1)
+    cases.append((z, np.round(z + 0.1 * rng.standard_normal((400, 1)), 1), 4, 0))
+    z = rng.standard_normal((300, 2))
+    cases.append((z, z.copy(), 5, 0))
+    z = rng.standard_normal((1200, 8))
+    cases.append((z, z[:, :8] * 0.3 + rng.standard_normal((1200, 8)), 5, 11))
+    for i, (a, b, k, js) in enumerate(cases):
+        est = ksg_mi(a, b, k, jitter_seed=js)
+        out[f"z{i}"], out[f"y{i}"] = a, b
+        out[f"meta{i}"] = np.array([k, js], np.int64)
+        out[f"value{i}"] = np.array(est.value)
+        out[f"flagged{i}"] = np.array(est.flagged)
+    xs = np.concatenate([rng.uniform(1e-3, 1.0, 40), rng.uniform(1.0, 100.0, 40),
+                         np.arange(1, 2001, dtype=np.float64)])
+    out["digamma_x"] = xs
+    out["digamma"] = digamma(xs)
+    return out
+
+
 def main():
     os.makedirs(GOLD, exist_ok=True)
     rng = np.random.Generator(np.random.PCG64(20250718))
     manifest = {}
     for name, fn in (("quantize", gen_quantize), ("coder", gen_coder), ("model", gen_model),
-                     ("pipeline", gen_pipeline), ("adam", gen_adam)):
+                     ("pipeline", gen_pipeline), ("adam", gen_adam), ("ifr", gen_ifr)):
         arrs = fn(rng)
         path = os.path.join(GOLD, f"{name}.npz")
         np.savez_compressed(path, **arrs)

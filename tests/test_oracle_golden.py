@@ -112,3 +112,21 @@ def test_adam_matches_reference(golden):
         assert not grad.any()
     assert np.array_equal(value, g["value"])
     assert np.array_equal(m, g["m"]) and np.array_equal(v, g["v"])
+
+
+def test_ksg_oracle_matches_reference(golden):
+    """oracle/ifr.py (KSG restatement) reproduces the reference's estimates
+    bit for bit; the product's host digamma equals the reference's."""
+    from oracle import ifr as oi
+    from paper_2507_18969_b200.ifr import digamma
+    g = golden("ifr")
+    i = 0
+    while f"z{i}" in g:
+        k, js = (int(v) for v in g[f"meta{i}"])
+        value, flagged = oi.ksg_mi(g[f"z{i}"], g[f"y{i}"], k, js)
+        assert value == float(g[f"value{i}"]), i
+        assert flagged == bool(g[f"flagged{i}"]), i
+        i += 1
+    assert i == 5
+    assert np.array_equal(digamma(g["digamma_x"]), g["digamma"])
+    assert np.array_equal(oi.digamma(g["digamma_x"]), g["digamma"])
