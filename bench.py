@@ -15,9 +15,11 @@ of predict -> quantize -> encode -> backward -> Adam.
                 (the encoder stream is joined before the stop event).
 * ``decompress_MBps``  the mirrored decode loop on the same columns (output
                 verified bit-exact against the input).
-* ``e2e``       compress through the C ABI with host buffers: each step copies
-                its input columns from pinned host memory (H2D) and reads the
-                step's coded intervals back (D2H).
+* ``e2e``       the whole stream through the public API: ``compress(bytes)``
+                + ``write_container`` (context setup, parameter upload,
+                streaming H2D of the lane columns, graph-replayed steps, device
+                payload assembly, payload D2H); ``full_stream_*`` adds the
+                full ``decompress`` and its lossless check.
 * ``bits_per_byte`` / ``ref_bits_per_byte``: the full C2-mini stream (4 MiB,
                 same B/S/dims) compressed end to end by the public API vs the
                 unmodified reference's run of the same stream
@@ -136,8 +138,15 @@ class Clocks:
 
 # --------------------------------------------------------------- CPU oracle
 
-def cpu_sample(wl, min_seconds: float, max_steps: int, warm: int = 1, exact: bool = False):
-    """Step-sampled CPU oracle at the workload's exact (B, dims)."""
+def cpu_sample(wl, min_seconds: float, max_steps: int, warm: int = 1, exact: bool = False,
+               blas_threads: int | None = None):
+    """Step-sampled CPU oracle at the workload's exact (B, dims).  BLAS runs on
+    all host cores by default -- a non-default override: the reference pins
+    OpenBLAS to one thread (`__init__.py:15-22`); blas_threads=1 restores that."""
+    if blas_threads is not None:
+        import threadpoolctl
+        with threadpoolctl.threadpool_limits(blas_threads):
+            return cpu_sample(wl, min_seconds, max_steps, warm, exact)
     from oracle import coder as oc
     from oracle.model import OracleModel
     from paper_2507_18969_b200.config import ModelConfig
@@ -178,7 +187,9 @@ def cpu_sample(wl, min_seconds: float, max_steps: int, warm: int = 1, exact: boo
     return dict(value=B * n / dt / 1e6, unit="MB/s", cores=int(cores), kind="port",
                 sample=f"{n} model steps x {B} lanes ({wl['desc']}), fp64 numpy/OpenBLAS + C coder,"
                        f" after {warm} warm-up step; {dt:.1f} s",
-                seconds_per_step=dt / n)
+                seconds_per_step=dt / n, blas_threads=int(cores),
+                blas_note="reference default" if cores == 1 else
+                "non-default override: the reference pins BLAS to 1 thread (__init__.py:15-22)")
 
 
 def run_reference(args, wl):
@@ -186,7 +197,9 @@ def run_reference(args, wl):
     if rank != 0:
         return
     B = wl["lanes"]
-    r = cpu_sample(wl, min_seconds=0.0, max_steps=args.steps, warm=args.warmup, exact=True)
+    # a bounded sample: up to --steps model steps, stopping after ~60 s
+    r = cpu_sample(wl, min_seconds=60.0, max_steps=args.steps, warm=min(args.warmup, 1))
+    r1 = cpu_sample(wl, min_seconds=0.0, max_steps=min(args.steps, 2), blas_threads=1)
     # treat each model step as one bench step (a bounded sample of the workload)
     line = dict(metric=METRIC, value=r["value"], unit="MB/s", n_gpus=args.gpus, steps=args.steps,
                 warmup=args.warmup, ms_per_step=r["seconds_per_step"] * 1e3,
@@ -195,7 +208,9 @@ def run_reference(args, wl):
                 config=dict(workload=wl["desc"], lanes=B, segments=wl["segments"],
                             columns_per_step=1),
                 cpu_baseline=dict(value=r["value"], unit="MB/s", cores=r["cores"], kind="port",
-                                  sample=r["sample"]),
+                                  sample=r["sample"], blas_note=r["blas_note"],
+                                  one_thread=dict(value=r1["value"], cores=1, sample=r1["sample"],
+                                                  blas_note=r1["blas_note"])),
                 e2e=dict(value=r["value"], unit="MB/s", h2d_bytes_per_step=0,
                          d2h_bytes_per_step=0))
     print(json.dumps(line), flush=True)
@@ -299,36 +314,32 @@ def run_ours(args, wl):
     lossless = bool(np.array_equal(got, want.reshape(B, L)[:, :C]))
     dctx.close()
 
-    # ---- e2e through the C ABI with host buffers (pinned)
-    e2e = None
+    # ---- e2e: the whole stream through the public API (host bytes in,
+    # container bytes out): context setup, parameter upload, streaming column
+    # H2D, graph-replayed model steps, device payload assembly + D2H, container
+    # write; then the full decompress, checked lossless
+    e2e, full = None, {}
     if not args.no_e2e:
-        import torch
-        pinned = torch.empty(n, dtype=torch.uint8, pin_memory=True)
-        pinned.numpy()[:] = buf
-        hp = pinned.data_ptr()
-        out_iv = torch.empty(chunk * B, dtype=torch.int32, pin_memory=True)
-        ectx = DeviceContext(cfg, S, n, 0)
-        ectx.load_flat(params)
-
-        def e2e_cols(c0, c1):
-            _lib.check(lib.edpc_set_input_columns(ectx.h, hp, n, c0, c1))
-            _lib.check(lib.edpc_compress_steps(ectx.h, c0, c1))
-            _lib.check(lib.edpc_get_intervals(ectx.h, c0, c1, out_iv.data_ptr()))
-
-        e2e_cols(0, T)
-        col = T
-        for _ in range(W):
-            e2e_cols(col, col + chunk)
-            col += chunk
-        e_start = col
-        _lib.check(lib.edpc_sync(ectx.h))
-        e_ms, _, _ = timed_loop(ectx, lambda k: e2e_cols(e_start + k * chunk,
-                                                         e_start + (k + 1) * chunk), K, False)
-        ectx.close()
-        e2e = dict(value=B * chunk * K / (e_ms / 1e3) / 1e6, unit="MB/s",
-                   h2d_bytes_per_step=B * chunk, d2h_bytes_per_step=B * chunk * 4,
-                   path="edpc_set_input_columns (pinned H2D) + edpc_compress_steps + "
-                        "edpc_get_intervals (D2H) per step")
+        from paper_2507_18969_b200 import compress, decompress, read_container, write_container
+        e_n = min(n, args.e2e_bytes) if args.e2e_bytes else n
+        stream = bytes(data[:e_n])
+        t0 = time.perf_counter()
+        blob = write_container(compress(stream, cfg, S))
+        ce_s = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        back = decompress(read_container(blob))
+        de_s = time.perf_counter() - t0
+        ok = back == stream
+        e2e = dict(value=e_n / ce_s / 1e6, unit="MB/s", h2d_bytes_per_step=e_n,
+                   d2h_bytes_per_step=len(blob), steps=1,
+                   path="public compress(bytes) -> write_container of the whole "
+                        f"{e_n >> 20} MiB stream (one step = the stream): context setup, "
+                        "parameter upload, streaming column H2D, CUDA-graph model steps, "
+                        "device-side payload assembly, one payload D2H, container write")
+        full = dict(full_stream_bytes=e_n, full_stream_compress_MBps=e_n / ce_s / 1e6,
+                    full_stream_decompress_MBps=e_n / de_s / 1e6, full_stream_lossless=ok,
+                    full_stream_bits_per_byte=8.0 * len(blob) / e_n,
+                    full_stream_compress_s=ce_s, full_stream_decompress_s=de_s)
 
     # ---- bits/byte vs the reference's own run of the C2-mini stream
     ratio = {}
@@ -349,7 +360,9 @@ def run_ours(args, wl):
     cpu = None
     if not args.no_cpu:
         r = cpu_sample(wl, min_seconds=args.cpu_seconds, max_steps=20)
-        cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "blas_note")}
+        r1 = cpu_sample(wl, min_seconds=0.0, max_steps=2, blas_threads=1)
+        cpu["one_thread"] = {k: r1[k] for k in ("value", "cores", "sample", "blas_note")}
 
     pk, pk_src = peaks()
     tc, f16 = numerics["tcgen05"], numerics["fp16_mbrb"]
@@ -396,7 +409,7 @@ def run_ours(args, wl):
                     bytes_per_step=B * chunk, model=wl["model"],
                     l2="no flush: per-step working set ~1 GB > 126 MB L2"),
         decompress_MBps=B * chunk * K / (d_ms / 1e3) / 1e6, lossless_region=lossless,
-        region_bits_per_byte=region_bpb, **ratio,
+        region_bits_per_byte=region_bpb, **ratio, **full,
         roofline=dict(bound="tensor",
                       kernel=f"per-step GEMMs ({gemm_kind})",
                       achieved=achieved,
@@ -421,14 +434,20 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: c2 on one GPU, c3 (the multi-GPU config) on N > 1")
     ap.add_argument("--chunk", type=int, default=32)
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-bytes", type=int, default=None,
+                    help="e2e / full-stream leg on this prefix of the stream (default: all)")
     ap.add_argument("--no-ratio", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 1)
+    if args.workload is None:
+        multi = args.gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1
+        args.workload = "c3" if multi else "c2"
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference(args, wl)

@@ -136,6 +136,130 @@ class ShardSet:
                     _lib.check(lib.edpc_weights_pull(dst.h, src.h))
 
 
+# ------------------------------- one host thread per GPU, NCCL in the graphs
+
+def nccl_available() -> bool:
+    """True when the library can reach an NCCL (libnccl.so.2)."""
+    buf = (ctypes.c_uint8 * 128)()
+    return _lib.load().edpc_nccl_unique_id(buf, 128) == _lib.OK
+
+
+def _use_nccl(devices: list[int]) -> bool:
+    """Distinct GPUs (NCCL allows one rank per device) and an NCCL to load;
+    contexts sharing a device (tests on one GPU) use stream-ordered peer
+    copies (ShardSet) instead."""
+    return len(set(devices)) == len(devices) and _lib.device_count() >= len(devices) and \
+        nccl_available()
+
+
+def _run_ranks(devices: list[int], fn) -> list:
+    """fn(rank, device) on one host thread per device (each thread owns its
+    context: the C ABI calls block only their own device's stream, and the
+    NCCL collectives inside every rank's captured step graphs meet on the
+    devices); exceptions are re-raised on the caller."""
+    import threading
+    out: list = [None] * len(devices)
+    errs: list = []
+
+    def run(r):
+        try:
+            out[r] = fn(r, devices[r])
+        except BaseException as exc:
+            errs.append(exc)
+
+    ts = [threading.Thread(target=run, args=(r,)) for r in range(len(devices))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    if errs:
+        raise errs[0]
+    return out
+
+
+def _nccl_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _lib.check(_lib.load().edpc_nccl_unique_id(buf, 128))
+    return bytes(buf)
+
+
+def _join(ctx: DeviceContext, uid: bytes, world: int, rank: int) -> None:
+    arr = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    _lib.check(_lib.load().edpc_ctx_set_comm(ctx.h, arr, world, rank))
+
+
+def _compress_nccl(data: bytes, cfg: ModelConfig, segments: int, devices: list[int],
+                   chunk: int = 512) -> tuple[list, int]:
+    """One context per GPU joined to an NCCL communicator; each rank's thread
+    runs the same column blocks as the single-GPU pipeline (CUDA-graph model
+    steps with the sharded optimizer's send/recv + all-gather captured inside)."""
+    n = len(data)
+    plan = lane_plan(cfg, segments, len(devices))
+    uid = _nccl_id()
+    buf = np.frombuffer(bytes(data), dtype=np.uint8)
+    params = init_params_f32(cfg)
+    spl = cfg.lanes // segments
+    lib = _lib.load()
+
+    def rank_fn(r, dev):
+        lb, lc = plan[r]
+        ctx = DeviceContext(cfg, segments, n, dev, lb, lc)
+        try:
+            ctx.load_flat(params)
+            _join(ctx, uid, len(devices), r)
+            L = ctx.lane_len
+            for i0 in range(0, L, chunk):
+                i1 = min(L, i0 + chunk)
+                _lib.check(lib.edpc_set_input_columns(ctx.h, buf.ctypes.data, n, i0, i1))
+                _lib.check(lib.edpc_compress_steps(ctx.h, i0, i1))
+            bits = np.zeros(lc // spl, dtype=np.int64)
+            tot = ctypes.c_int64()
+            _lib.check(lib.edpc_compress_finish(ctx.h, bits.ctypes.data, ctypes.byref(tot)))
+            pay = np.zeros(max(tot.value, 1), dtype=np.uint8)
+            _lib.check(lib.edpc_get_payloads(ctx.h, pay.ctypes.data, pay.size))
+            return bits.tolist(), _split_payloads(bits, pay), ctx.numerics_flags()
+        finally:
+            ctx.close()
+
+    res = _run_ranks(devices, rank_fn)
+    return [(b, p) for b, p, _ in res], res[0][2]
+
+
+def _decompress_nccl(container: EdpcContainer, devices: list[int], chunk: int = 512) -> bytes:
+    h = container.header
+    cfg = h.model_config()
+    n, segments = h.original_len, h.segment_count
+    plan = lane_plan(cfg, segments, len(devices))
+    uid = _nccl_id()
+    params = init_params_f32(cfg)
+    spl = cfg.lanes // segments
+    lib = _lib.load()
+
+    def rank_fn(r, dev):
+        lb, lc = plan[r]
+        ctx = DeviceContext(cfg, segments, n, dev, lb, lc, numerics=h.numerics)
+        try:
+            ctx.load_flat(params)
+            _join(ctx, uid, len(devices), r)
+            s0, s1 = lb // spl, (lb + lc) // spl
+            pays = np.frombuffer(b"".join(container.segments[s0:s1]) or b"\0", dtype=np.uint8)
+            bits = np.ascontiguousarray(h.bit_lengths[s0:s1], dtype=np.int64)
+            _lib.check(lib.edpc_set_payloads(ctx.h, pays.ctypes.data, bits.ctypes.data))
+            L = ctx.lane_len
+            for i0 in range(0, L, chunk):
+                _lib.check(lib.edpc_decompress_steps(ctx.h, i0, min(L, i0 + chunk)))
+            out = np.empty(lc * L, dtype=np.uint8)
+            st = lib.edpc_get_output(ctx.h, out.ctypes.data, out.size)
+            if st == _lib.ERR_CODER:
+                raise CoderError(lib.edpc_last_error().decode())
+            _lib.check(st)
+            return out
+        finally:
+            ctx.close()
+
+    return np.concatenate(_run_ranks(devices, rank_fn))[:n].tobytes()
+
+
 def compress_multi(data: bytes, cfg: ModelConfig, segments: int, devices: list[int], *,
                    stats: dict | None = None) -> EdpcContainer:
     t0 = time.perf_counter()
@@ -144,6 +268,15 @@ def compress_multi(data: bytes, cfg: ModelConfig, segments: int, devices: list[i
         return EdpcContainer(header=Header.from_config(cfg, 0, []), segments=[])
     for d in set(devices):
         _lib.require_device(d)
+    lane_plan(cfg, segments, len(devices))  # geometry errors before any context
+    if _use_nccl(list(devices)):
+        shards, numerics = _compress_nccl(data, cfg, segments, list(devices))
+        if stats is not None:
+            stats.update(steps=max(0, lane_len_for(n, cfg.lanes) - cfg.context_len),
+                         predict_s=0.0, train_s=0.0, encode_s=0.0, mode="nccl",
+                         wall_s=time.perf_counter() - t0, peak_queue_depth=0,
+                         devices=list(devices))
+        return assemble(cfg, n, shards, numerics)
     ss = ShardSet(cfg, segments, n, list(devices))
     lib = ss.lib
     try:
@@ -185,6 +318,12 @@ def decompress_multi(container: EdpcContainer, devices: list[int], *,
     segments = h.segment_count
     for d in set(devices):
         _lib.require_device(d)
+    if _use_nccl(list(devices)):
+        out = _decompress_nccl(container, list(devices))
+        if stats is not None:
+            stats.update(steps=max(0, lane_len_for(n, cfg.lanes) - cfg.context_len), mode="nccl",
+                         wall_s=time.perf_counter() - t0, devices=list(devices))
+        return out
     ss = ShardSet(cfg, segments, n, list(devices), numerics=h.numerics)
     lib = ss.lib
     try:
@@ -240,10 +379,11 @@ def torch_broadcast_id(uid):
 
 
 def bench_multi(args, wl, clocks_cls=None, peaks=None, flops_per_lane=None) -> None:
-    """bench.py at N GPUs under torchrun: weak scaling (the single-GPU
-    workload's lanes per GPU), the sharded optimizer's two NCCL exchanges per
-    model step inside the captured step graph; the step time is the max over
-    ranks of CUDA-event time."""
+    """bench.py at N GPUs under torchrun: the workload as defined (C3: fixed
+    B, S and stream; per-GPU lanes B/G; identical container bytes at every G),
+    the sharded optimizer's two NCCL exchanges per model step inside the
+    captured step graph; the step time is the max over ranks of CUDA-event
+    time."""
     import json
 
     import torch
@@ -258,22 +398,22 @@ def bench_multi(args, wl, clocks_cls=None, peaks=None, flops_per_lane=None) -> N
     if not dist.is_initialized():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = _lib.load()
-    # weak scaling: the single-GPU workload per rank (B, S and stream bytes x N)
-    cfg = ModelConfig(**wl["model"], lanes=wl["lanes"] * world)
-    S = wl["segments"] * world
-    n = wl["nbytes"] * world
+    # the workload as defined (C3: fixed B = 32768 lanes, S = 1024 segments,
+    # 1 GiB): rank r runs lanes [r B/G, (r+1) B/G) -- per-GPU M = B/G -- and the
+    # container bytes are the same at every G (strong scaling)
+    cfg = ModelConfig(**wl["model"], lanes=wl["lanes"])
+    S = wl["segments"]
+    n = wl["nbytes"]
     plan = lane_plan(cfg, S, world)
     lb, lc = plan[rank]
     T = cfg.context_len
     chunk, K, W = args.chunk, args.steps, args.warmup
     L = lane_len_for(n, cfg.lanes)
-    # each rank synthesises only its own lanes' bytes (seed + rank); content
-    # does not change the per-step work, which is shape-determined
-    mine = np.frombuffer(synth.generate(wl["kind"], lc * L, wl["seed"] + rank), dtype=np.uint8)
+    stream = np.frombuffer(synth.generate(wl["kind"], n, wl["seed"]), dtype=np.uint8)
     ctx = DeviceContext(cfg, S, n, local, lb, lc)
     ctx.load_flat(init_params_f32(cfg))
     numerics = ctx.numerics()
-    _lib.check(lib.edpc_set_input_local(ctx.h, mine.ctypes.data, mine.size))
+    _lib.check(lib.edpc_set_input(ctx.h, stream.ctypes.data, n, 0))  # this rank's lane slice
     nccl_join(ctx, rank, world, torch_broadcast_id)
     _lib.check(lib.edpc_compress_steps(ctx.h, 0, T))
     col = T
@@ -313,12 +453,12 @@ def bench_multi(args, wl, clocks_cls=None, peaks=None, flops_per_lane=None) -> N
         line = dict(metric="compress/decompress MB/s at 1/2/4/8 B200 + bits/byte vs CPU ref",
                     value=total_bytes / (ms_max / 1e3) / 1e6, unit="MB/s", n_gpus=world,
                     steps=K, warmup=W, ms_per_step=ms_max / K, higher_is_better=True,
-                    scaling="weak", vs_baseline=None, numerics=numerics, clocks=clocks,
+                    scaling="strong", vs_baseline=None, numerics=numerics, clocks=clocks,
                     roofline=roof, cpu_baseline=None,
                     e2e=None, e2e_note="multi-GPU lines time the device-resident loop only",
-                    dtype=dtype, data=f"synthetic {wl['kind']}-like (PCG64 seed {wl['seed']} + rank)",
-                    config=dict(workload=f"{wl['desc']} per GPU; {world} GPUs: B={cfg.lanes}, "
-                                         f"S={S}, {n >> 20} MiB (C3-style weak scaling)",
+                    dtype=dtype, data=f"synthetic {wl['kind']}-like (PCG64 seed {wl['seed']})",
+                    config=dict(workload=f"{wl['desc']}; {world} GPUs: B={cfg.lanes}, S={S}, "
+                                         f"{n >> 20} MiB, {lc} lanes per GPU (strong scaling)",
                                 lanes=cfg.lanes, segments=S,
                                 lanes_per_gpu=lc, columns_per_step=chunk,
                                 exchange="sharded optimizer per model step, inside the step "

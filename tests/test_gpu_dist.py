@@ -50,3 +50,25 @@ def test_lane_plan_rejects_straddling_geometry():
         dist.lane_plan(TINY, 2, 4)                           # 4-lane segments over 2-lane shares
     with pytest.raises(ValueError):
         dist.lane_plan(TINY, 4, 3)                           # 3 does not divide 8
+
+
+def _gpus():
+    from paper_2507_18969_b200 import _lib
+    return _lib.device_count()
+
+
+@pytest.mark.skipif("_gpus() < 2")
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_nccl_ranks_match_single_gpu(paper1024, world):
+    """One host thread per GPU, NCCL send/recv + all-gather captured in every
+    rank's step graphs (dist._compress_nccl): the single-GPU container, bit
+    for bit, and its decompression."""
+    if _gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    cfg, data, ref = paper1024
+    assert dist._use_nccl(list(range(world)))
+    stats = {}
+    got = write_container(dist.compress_multi(data, cfg, 16, list(range(world)), stats=stats))
+    assert stats["mode"] == "nccl"
+    assert got == ref
+    assert dist.decompress_multi(read_container(got), list(range(world))) == data
