@@ -410,7 +410,9 @@ struct EpiBwdAct {
 template <int ZIN>
 struct EpiBranchActH {
   static constexpr bool kTmaStore = true, kRequireTs = true;
-  static constexpr int kTsSlots = 2;
+  // fp16 boxes (2 KB): 4 slots in the 8 KB per warp that 2 fp32 slots took --
+  // the 3 stores of a chunk (ff, D_0, D_1) no longer wait on each other
+  static constexpr int kTsSlots = 4, kTsSlotBytes = 2048;
   __half* H;        // D_z [ZIN][M][N]
   __half* ff;       // [M][N]
   const float* b0;  // bias of branch 0; branch z at b0 + z*sBias

@@ -314,15 +314,26 @@ struct EpiTsIn<Epi, std::void_t<decltype(Epi::kTsIn)>> {
   static constexpr int value = Epi::kTsIn;
 };
 constexpr int kTsBoxBytes = 32 * 32 * 4;
+// bytes per TMA-store slot: a 32x32 fp32 box by default; epilogues that only
+// move fp16 boxes (2 KB) declare kTsSlotBytes = 2048 and get twice the slots
+// -- twice the stores in flight -- in the same shared memory
+template <class Epi, class = void>
+struct EpiTsSlotBytes {
+  static constexpr int value = kTsBoxBytes;
+};
+template <class Epi>
+struct EpiTsSlotBytes<Epi, std::void_t<decltype(Epi::kTsSlotBytes)>> {
+  static constexpr int value = Epi::kTsSlotBytes;
+};
 constexpr int kStagesMax = 4;
 
-template <int BN, int ZIN = 1, bool TR = true, int EW = 8, int TSLOTS = 0>
+template <int BN, int ZIN = 1, bool TR = true, int EW = 8, int TSLOTS = 0, int TSB = kTsBoxBytes>
 struct TcSmem {
   static constexpr int kABytes = kTcBM * kTcBK * 4;  // 16 KB
   static constexpr int kBBytes = BN * kTcBK * 4;
   static constexpr int kStageBytes = kABytes + ZIN * kBBytes;
   static constexpr int kTrBytes = TR ? EW * ZIN * kTcTileFloats * 4 : 0;
-  static constexpr int kTsBytes = EW * TSLOTS * kTsBoxBytes;
+  static constexpr int kTsBytes = EW * TSLOTS * TSB;
   static constexpr int kEpiBytes = kTrBytes > kTsBytes ? kTrBytes : kTsBytes;
   static constexpr int kFixed = 1024 /*align*/ + 512 /*barriers*/ + kEpiBytes;
   static constexpr int kStages = (4 * kStageBytes + kFixed <= 232448)   ? 4
@@ -337,7 +348,7 @@ struct TcSmem {
 };
 
 // Per-warp box writer of a TMA-store epilogue (see EpiTmaStore).
-template <int NS>
+template <int NS, int SF = 1024>  // NS slots of SF floats
 struct TsIo {
   float* slots;  // NS boxes of 32x32 floats
   const CUtensorMap* maps[2];
@@ -347,7 +358,7 @@ struct TsIo {
   // row `lane` of box `slot`: 16-byte chunk j at j ^ (lane & 7) (SWIZZLE_128B)
   __device__ __forceinline__ void write_row(int slot, const float (&v)[32]) const {
     const int lane = threadIdx.x & 31;
-    float* box = slots + slot * 1024 + lane * 32;
+    float* box = slots + slot * SF + lane * 32;
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       *reinterpret_cast<float4*>(box + ((j ^ (lane & 7)) << 2)) =
@@ -355,7 +366,7 @@ struct TsIo {
   }
   __device__ __forceinline__ void in(int slot, float (&v)[32]) const {
     const int lane = threadIdx.x & 31;
-    const float* box = slots + (ib + slot) * 1024 + lane * 32;
+    const float* box = slots + (ib + slot) * SF + lane * 32;
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const float4 q = *reinterpret_cast<const float4*>(box + ((j ^ (lane & 7)) << 2));
@@ -366,7 +377,7 @@ struct TsIo {
     fence_async_smem();
     __syncwarp();
     if ((threadIdx.x & 31) == 0) {
-      tma_store_4d(maps[map], slots + slot * 1024, n0, m0, c2, c3);  // rows past M are clipped
+      tma_store_4d(maps[map], slots + slot * SF, n0, m0, c2, c3);  // rows past M are clipped
       bulk_commit();
     }
   }
@@ -374,7 +385,7 @@ struct TsIo {
   // row r at j ^ ((r >> 1) & 3) -- conflict-free for 8 rows per phase
   __device__ __forceinline__ void write_row_h(int slot, const float (&v)[32]) const {
     const int lane = threadIdx.x & 31;
-    uint8_t* row = reinterpret_cast<uint8_t*>(slots + slot * 1024) + lane * 64;
+    uint8_t* row = reinterpret_cast<uint8_t*>(slots + slot * SF) + lane * 64;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       uint4 q;
@@ -391,7 +402,7 @@ struct TsIo {
   }
   __device__ __forceinline__ void in_h(int slot, float (&v)[32]) const {
     const int lane = threadIdx.x & 31;
-    const uint8_t* row = reinterpret_cast<const uint8_t*>(slots + (ib + slot) * 1024) + lane * 64;
+    const uint8_t* row = reinterpret_cast<const uint8_t*>(slots + (ib + slot) * SF) + lane * 64;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const uint4 q = *reinterpret_cast<const uint4*>(row + ((j ^ ((lane >> 1) & 3)) << 4));
@@ -481,6 +492,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   static_assert(TcSmem<BN, ZIN>::kCols <= 512, "TMEM holds 512 columns");
   constexpr bool TS = EpiTmaStore<Epi>::value;
   constexpr int kTsSlots = TS ? EpiTsSlots<Epi>::value : 0;
+  constexpr int kTsSB = EpiTsSlotBytes<Epi>::value;
   constexpr int kTsIn = EpiTsIn<Epi>::value;
   static_assert(kTsIn == 0 || 2 * kTsIn == kTsSlots,
                 "input boxes are double-buffered in the TMA-store slots");
@@ -489,7 +501,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   constexpr int kTcEpiWarps = EW;  // epilogue warps: EW / 4 per TMEM lane quadrant
   static_assert(EW % 4 == 0, "whole TMEM lane quadrants per epilogue warp group");
   extern __shared__ uint8_t smem_raw[];
-  using SM = TcSmem<BN, ZIN, TR, EW, kTsSlots>;
+  using SM = TcSmem<BN, ZIN, TR, EW, kTsSlots, kTsSB>;
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   constexpr int kStages = SM::kStages;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + SM::kBarOffset);
@@ -685,7 +697,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
     uint32_t ts_wph = 0;   // phases of this warp's two input-box barriers (bit = slot pair)
     int ts_pair = 0;       // slot pair holding the current block's input boxes
     float* const ts_slots = reinterpret_cast<float*>(smem + SM::kEpiOffset) +
-                            (warp - 2) * (kTsSlots > 0 ? kTsSlots : 1) * (kTsBoxBytes / 4);
+                            (warp - 2) * (kTsSlots > 0 ? kTsSlots : 1) * (kTsSB / 4);
     // TMA loads of the input boxes of block (tile tq, column cq) into slot pair `pair`
     auto ts_issue = [&](int tq, int cq, int pair) {
       if constexpr (kTsIn > 0) {
@@ -697,7 +709,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
         for (int i = 0; i < kTsIn; ++i) {
           int c2, c3;
           epi.ts_in(i, zb, zg, c2, c3);
-          tma_load_4d(ts_slots + (pair * kTsIn + i) * (kTsBoxBytes / 4), &tma_d, bar,
+          tma_load_4d(ts_slots + (pair * kTsIn + i) * (kTsSB / 4), &tma_d, bar,
                       tn * BN + cq, tm * kTcBM + quad * 32, c2, c3);
         }
       }
@@ -759,7 +771,7 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
               ib = ts_pair * kTsIn;
               ts_pair ^= 1;
             }
-            TsIo<kTsSlots> io{slots, {&tma_c, &tma_d}, n0 + c, m_base, &ts_next, ib};
+            TsIo<kTsSlots, kTsSB / 4> io{slots, {&tma_c, &tma_d}, n0 + c, m_base, &ts_next, ib};
             epi.ts_chunk(io, zb, zg, m, n0 + c, v);
             continue;
           }
@@ -1142,7 +1154,8 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
                      cudaStream_t st) {
   constexpr bool kTS = EpiTmaStore<Epi>::value;
   constexpr int kSmem =
-      TcSmem<BN, 1, EpiTransposed<Epi>::value, 8, kTS ? EpiTsSlots<Epi>::value : 0>::kBytes;
+      TcSmem<BN, 1, EpiTransposed<Epi>::value, 8, kTS ? EpiTsSlots<Epi>::value : 0,
+             EpiTsSlotBytes<Epi>::value>::kBytes;
   const int n_tm = cdiv(s.M, kTcBM);
   const int cl = (cluster_enabled() && n_tm % 2 == 0) ? 2 : 1;
   CUtensorMap ta, tb, tc{}, td{};
@@ -1209,7 +1222,8 @@ inline int tc_launch_zin(const TcShape& s, const TcOperand& A, const TcOperand& 
   // the TMA-store form keeps its registers with 8
   constexpr bool kTS = EpiTmaStore<Epi>::value;
   constexpr int kZinEW = (!kTS && BN % 128 == 0) ? 16 : 8;
-  constexpr int kSmem = TcSmem<BN, ZIN, true, kZinEW, kTS ? EpiTsSlots<Epi>::value : 0>::kBytes;
+  constexpr int kSmem = TcSmem<BN, ZIN, true, kZinEW, kTS ? EpiTsSlots<Epi>::value : 0,
+                               EpiTsSlotBytes<Epi>::value>::kBytes;
   const int n_tm = cdiv(s.M, kTcBM);
   const int cl = (cluster_enabled() && n_tm % 2 == 0) ? 2 : 1;
   CUtensorMap ta, tb;

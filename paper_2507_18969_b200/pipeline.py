@@ -81,6 +81,7 @@ def compress(data: bytes, cfg: ModelConfig, segments: int = 4, *,
     try:
         ctx.load_flat(init_params_f32(cfg))
         numerics = ctx.numerics_flags()
+        setup_s = time.perf_counter() - t0
         buf = np.frombuffer(bytes(data), dtype=np.uint8)
         L = ctx.lane_len
         T = cfg.context_len
@@ -124,7 +125,9 @@ def compress(data: bytes, cfg: ModelConfig, segments: int = 4, *,
         pos += nb
     _stats(stats, steps=max(0, L - T), predict_s=loop_s, train_s=0.0,
            encode_s=time.perf_counter() - te, wall_s=time.perf_counter() - t0,
-           peak_queue_depth=0)
+           peak_queue_depth=0, setup_s=setup_s, device_loop_s=loop_s,
+           note="predict, quantize, encode and train run as one device schedule: "
+                "predict_s is the whole device loop, train_s is inside it")
     return EdpcContainer(header=Header.from_config(cfg, n, bits.tolist(), numerics),
                          segments=payloads)
 
