@@ -1,0 +1,391 @@
+// Fused MBRB forward (model.py:95-103) on the tcgen05 tensor cores: the two
+// branch GEMMs, the product / GeLU epilogue and the out-projection GEMM in one
+// kernel, the hidden tile never leaving the SM between the two GEMMs.
+//
+//   H_z  = x0 . W_z + b_z        (z = 0, 1; x0 = LN(x), fp16 [Bl][F])
+//   ff   = GeLU(H_0 * H_1)       (stored fp16: the out-proj weight gradient)
+//   D_z  = GeLU'(H_0 H_1) H_{1-z} (stored fp16: the backward's product rule)
+//   part[s] = ff[:, hs] . W_out[hs, :]   over the CTA's slice hs of H
+//
+// A CTA owns one 128-row tile of lanes and one of kFusedSplit equal slices of
+// the hidden dimension H, walked in chunks of kHC = 64 columns:
+//   warp 0       TMA producer: x0 tile once (resident, 64 KB), per chunk the
+//                two branch-weight boxes of each 64-deep k-block (ring of
+//                kB1Stages) and the chunk's 64 x 256 out-projection weight rows
+//   warp 1       TMEM allocation + single-thread MMA issuer:
+//                  MMA1(c): acc1[c & 1][z] = x0 . W_z[:, chunk c]   (N = 64)
+//                  MMA2(c-1): acc2 += ff(c-1) . W_out[chunk c-1, :] (N = 256)
+//                MMA1 runs a chunk ahead so the epilogue of chunk c overlaps
+//                the MMAs of chunk c+1 (acc1 double-buffered in TMEM)
+//   warps 2-9    epilogue: tcgen05.ld of both branches (acc1 released right
+//                after the load), bias / product / GeLU / GeLU', then ff into
+//                the shared-memory A operand of MMA2 (K-major, 128B swizzle)
+//                and D_z into staging tiles; one thread TMA-stores ff and D_z
+//                from those same tiles.  After the last chunk the 128 x 256
+//                fp32 accumulator acc2 goes to the split-K workspace; the
+//                existing k_splitk_reduce adds the slices in a fixed order
+//                with bias and residual.
+// TMEM: acc1 2 x 2 x 64 columns + acc2 256 columns = 512.
+//
+// The arithmetic is the unfused path's, operation for operation: the branch
+// GEMM accumulates K = F in 16-deep steps, the epilogue is EpiBranchActH's,
+// the out-projection accumulates each H slice in the same 16-deep steps as the
+// kFusedSplit-way split-K GEMM it replaces, and the slices are reduced by the
+// same kernel -- so the containers are bit-identical to the unfused path.
+#pragma once
+
+#include "kernels.cuh"
+#include "tc_gemm.cuh"
+
+namespace edpc {
+
+namespace mf {
+constexpr int kBM = 128;
+constexpr int kF = 256;          // feature width (x0 row, out-projection N)
+constexpr int kHC = 64;          // hidden chunk
+constexpr int kB1Stages = 4;
+constexpr int kEW = 8;           // epilogue warps
+constexpr int kThreads = 32 * (2 + kEW);
+constexpr int kA1Bytes = kBM * kF * 2;             // 64 KB resident x0 tile
+constexpr int kB1Stage = 2 * kHC * 64 * 2;          // both branches, one 64-deep k-block: 16 KB
+constexpr int kB2Bytes = kHC * kF * 2;              // 32 KB
+constexpr int kA2Bytes = kBM * kHC * 2;             // 16 KB
+constexpr int kDBytes = 2 * kBM * kHC * 2;          // 32 KB (D_0, D_1)
+constexpr int kOffA1 = 0;
+constexpr int kOffB1 = kOffA1 + kA1Bytes;
+constexpr int kOffB2 = kOffB1 + kB1Stages * kB1Stage;
+constexpr int kOffA2 = kOffB2 + kB2Bytes;
+constexpr int kOffD = kOffA2 + kA2Bytes;
+constexpr int kOffBar = kOffD + kDBytes;
+constexpr int kSmemBytes = 1024 + kOffBar + 256;
+}  // namespace mf
+
+constexpr int kFusedSplit = 4;  // = kSplitK of the unfused out-projection
+
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1,
+                                             int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+// 32 fp32 values -> fp16, into 64 bytes of a K-major SWIZZLE_128B row (row r
+// of a 128-byte-row tile): 16-byte chunk j (8 halves) at (j ^ (r & 7)).
+__device__ __forceinline__ void put_row_h_sw128(uint8_t* tile, int r, int j0, const float (&v)[32]) {
+  uint8_t* row = tile + r * 128;
+#pragma unroll
+  for (int jj = 0; jj < 4; ++jj) {
+    uint4 q;
+    __half2 h0 = __floats2half2_rn(v[8 * jj], v[8 * jj + 1]);
+    __half2 h1 = __floats2half2_rn(v[8 * jj + 2], v[8 * jj + 3]);
+    __half2 h2 = __floats2half2_rn(v[8 * jj + 4], v[8 * jj + 5]);
+    __half2 h3 = __floats2half2_rn(v[8 * jj + 6], v[8 * jj + 7]);
+    q.x = *reinterpret_cast<uint32_t*>(&h0);
+    q.y = *reinterpret_cast<uint32_t*>(&h1);
+    q.z = *reinterpret_cast<uint32_t*>(&h2);
+    q.w = *reinterpret_cast<uint32_t*>(&h3);
+    *reinterpret_cast<uint4*>(row + (((j0 + jj) ^ (r & 7)) << 4)) = q;
+  }
+}
+
+// grid: (ceil(Bl / 128) * kFusedSplit); tile t = blockIdx.x / kFusedSplit,
+// slice s = blockIdx.x % kFusedSplit
+__global__ void __launch_bounds__(mf::kThreads, 1)
+k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant__ CUtensorMap tm_wb,
+                 const __grid_constant__ CUtensorMap tm_wo, const __grid_constant__ CUtensorMap tm_ff,
+                 const __grid_constant__ CUtensorMap tm_d, const float* __restrict__ b0,
+                 int64_t sBias, int Bl, int H, float* __restrict__ ws) {
+  using namespace mf;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA1 = smem + kOffA1;
+  uint8_t* sB1 = smem + kOffB1;
+  uint8_t* sB2 = smem + kOffB2;
+  uint8_t* sA2 = smem + kOffA2;
+  uint8_t* sD = smem + kOffD;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* a1full = bar;
+  uint64_t* b1full = bar + 1;
+  uint64_t* b1empty = b1full + kB1Stages;
+  uint64_t* b2full = b1empty + kB1Stages;
+  uint64_t* b2empty = b2full + 1;
+  uint64_t* tfull1 = b2empty + 1;   // [2]
+  uint64_t* tempty1 = tfull1 + 2;   // [2]
+  uint64_t* a2full = tempty1 + 2;
+  uint64_t* a2empty = a2full + 1;
+  uint64_t* t2full = a2empty + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t2full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x / kFusedSplit, split = blockIdx.x % kFusedSplit;
+  const int m0 = tile * kBM;
+  const int hs = H / kFusedSplit;           // hidden columns of this slice
+  const int h_begin = split * hs;
+  const int nc = hs / kHC;                  // chunks
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_x0) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_wb) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_wo) : "memory");
+    mbar_init(a1full, 1);
+    for (int s = 0; s < kB1Stages; ++s) {
+      mbar_init(&b1full[s], 1);
+      mbar_init(&b1empty[s], 1);
+    }
+    mbar_init(b2full, 1);
+    mbar_init(b2empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull1[b], 1);
+      mbar_init(&tempty1[b], kEW);
+    }
+    mbar_init(a2full, 1);
+    mbar_init(a2empty, 1);
+    mbar_init(t2full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_entry();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      mbar_expect_tx(a1full, kA1Bytes);
+#pragma unroll
+      for (int kb = 0; kb < kF / 64; ++kb) tma_load_3d(sA1 + kb * 16384, &tm_x0, a1full, kb * 64, m0, 0);
+      int it = 0;
+      for (int c = 0; c < nc; ++c) {
+        const int h0 = h_begin + c * kHC;
+        for (int kb = 0; kb < kF / 64; ++kb, ++it) {
+          const int st = it % kB1Stages;
+          mbar_wait(&b1empty[st], ((uint32_t)(it / kB1Stages) & 1u) ^ 1u);
+          mbar_expect_tx(&b1full[st], kB1Stage);
+          uint8_t* dst = sB1 + st * kB1Stage;
+          tma_load_3d(dst, &tm_wb, &b1full[st], h0, kb * 64, 0);
+          tma_load_3d(dst + kHC * 128, &tm_wb, &b1full[st], h0, kb * 64, 1);
+        }
+        mbar_wait(b2empty, ((uint32_t)c & 1u) ^ 1u);
+        mbar_expect_tx(b2full, kB2Bytes);
+#pragma unroll
+        for (int j = 0; j < kF / 64; ++j) tma_load_3d(sB2 + j * 8192, &tm_wo, b2full, j * 64, h0, 0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t id1 = idesc_f16(kBM, kHC, 0, 1);
+      constexpr uint32_t id2 = idesc_f16(kBM, kF, 0, 1);
+      const uint32_t a1 = smem_u32(sA1), a2 = smem_u32(sA2), b2 = smem_u32(sB2);
+      mbar_wait(a1full, 0);
+      tc_fence_after();
+      int it = 0;
+      for (int c = 0; c <= nc; ++c) {
+        if (c < nc) {  // MMA1(c)
+          const int b = c & 1;
+          mbar_wait(&tempty1[b], ((uint32_t)(c >> 1) & 1u) ^ 1u);
+          tc_fence_after();
+          for (int kb = 0; kb < kF / 64; ++kb, ++it) {
+            const int st = it % kB1Stages;
+            mbar_wait(&b1full[st], (uint32_t)(it / kB1Stages) & 1u);
+            tc_fence_after();
+            const uint32_t sb = smem_u32(sB1 + st * kB1Stage);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t ad = sdesc(a1 + kb * 16384 + kk * 32, 16, 1024, kLayoutSW128);
+#pragma unroll
+              for (int z = 0; z < 2; ++z) {
+                const uint64_t bd = sdesc(sb + z * (kHC * 128) + kk * 2048, 8192, 1024, kLayoutSW128);
+                tc_mma_f16(tmem + (uint32_t)(b * 2 * kHC + z * kHC), ad, bd, id1,
+                           (kb > 0 || kk > 0) ? 1u : 0u);
+              }
+            }
+            tc_commit(&b1empty[st]);
+          }
+          tc_commit(&tfull1[b]);
+        }
+        if (c >= 1) {  // MMA2(c-1): acc2 += ff(c-1) . W_out[chunk c-1]
+          const int p = c - 1;
+          mbar_wait(a2full, (uint32_t)p & 1u);
+          mbar_wait(b2full, (uint32_t)p & 1u);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t ad = sdesc(a2 + kk * 32, 16, 1024, kLayoutSW128);
+            const uint64_t bd = sdesc(b2 + kk * 2048, 8192, 1024, kLayoutSW128);
+            tc_mma_f16(tmem + 256u, ad, bd, id2, (p > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(b2empty);
+          tc_commit(a2empty);
+          if (p == nc - 1) tc_commit(t2full);
+        }
+      }
+    }
+  } else {
+    // ---------------- epilogue (TMEM lane quadrant = warp % 4)
+    const int quad = warp & 3;
+    const int half = (warp - 2) >> 2;  // columns half*32 .. +32 of each chunk
+    const int r = quad * 32 + lane;    // tile row
+    const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
+    const int et = threadIdx.x - 64;   // 0 .. 255
+    for (int c = 0; c < nc; ++c) {
+      const int b = c & 1;
+      const int h0 = h_begin + c * kHC;
+      const int n0 = h0 + half * 32;
+      mbar_wait(&tfull1[b], (uint32_t)(c >> 1) & 1u);
+      tc_fence_after();
+      float v0[32], v1[32];
+      tmem_ld32(tq + (uint32_t)(b * 2 * kHC + half * 32), v0);
+      tmem_ld32(tq + (uint32_t)(b * 2 * kHC + kHC + half * 32), v1);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty1[b]);  // acc1[b] may take chunk c+2
+      // EpiBranchActH's arithmetic, in its order
+      {
+        float bb[32];
+        load32(b0 + n0, bb);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v0[j] = v0[j] + bb[j];
+        load32(b0 + sBias + n0, bb);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v1[j] = v1[j] + bb[j];
+      }
+      float f[32], p[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        p[j] = v0[j] * v1[j];
+        gelu_pair(p[j], f[j], p[j]);
+      }
+      // staging free: MMA2(c-1) done reading ff, the TMA stores of c-1 done
+      // reading ff / D
+      mbar_wait(a2empty, ((uint32_t)c & 1u) ^ 1u);
+      if (et == 0) bulk_wait_read<0>();
+      named_bar(2, 32 * kEW);
+      put_row_h_sw128(sA2, r, half * 4, f);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) f[j] = p[j] * v1[j];  // D_0 = GeLU' * H_1
+      put_row_h_sw128(sD, r, half * 4, f);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) f[j] = p[j] * v0[j];  // D_1 = GeLU' * H_0
+      put_row_h_sw128(sD + kBM * 128, r, half * 4, f);
+      fence_async_smem();
+      named_bar(3, 32 * kEW);
+      if (et == 0) {
+        mbar_arrive(a2full);
+        tma_store_3d(&tm_ff, sA2, h0, m0, 0);
+        tma_store_3d(&tm_d, sD, h0, m0, 0);
+        tma_store_3d(&tm_d, sD + kBM * 128, h0, m0, 1);
+        bulk_commit();
+      }
+    }
+    // out-projection slice -> split-K workspace [split][Bl][F]
+    mbar_wait(t2full, 0);
+    tc_fence_after();
+    const int m = m0 + r;
+#pragma unroll 1
+    for (int cb = half * 128; cb < half * 128 + 128; cb += 32) {
+      float v[32];
+      tmem_ld32(tq + 256u + (uint32_t)cb, v);
+      if (m < Bl) {
+        float4* dst = reinterpret_cast<float4*>(ws + ((int64_t)split * Bl + m) * kF + cb);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      }
+    }
+    if (et == 0) bulk_wait_all();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// fp16 [c2][rows][inner] store map, box {64, 128, 1}, 128B swizzle (the
+// K-major MMA operand layout of one 64-wide chunk)
+inline bool make_store_map_h64(CUtensorMap* map, const void* base, uint64_t inner, uint64_t rows,
+                               uint64_t batch) {
+  cuuint64_t dims[3] = {inner, rows, batch};
+  cuuint64_t strides[2] = {inner * 2, inner * rows * 2};
+  cuuint32_t box[3] = {64, 128, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  PfnEncodeTiled enc = encode_tiled_fn();
+  return enc && enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, (void*)base, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) ==
+                    CUDA_SUCCESS;
+}
+
+struct FusedMapCache {
+  std::mutex mu;
+  std::map<std::tuple<const void*, uint64_t, uint64_t, uint64_t>, CUtensorMap> maps;
+  bool get(CUtensorMap* out, const void* base, uint64_t inner, uint64_t rows, uint64_t batch) {
+    auto key = std::make_tuple(base, inner, rows, batch);
+    std::lock_guard<std::mutex> g(mu);
+    auto it = maps.find(key);
+    if (it == maps.end()) {
+      CUtensorMap m{};
+      if (!make_store_map_h64(&m, base, inner, rows, batch)) return false;
+      it = maps.emplace(key, m).first;
+    }
+    *out = it->second;
+    return true;
+  }
+};
+
+inline FusedMapCache& fused_map_cache() {
+  static FusedMapCache c;
+  return c;
+}
+
+// shapes the fused kernel covers (else the caller takes the unfused path)
+inline bool mbrb_fused_ok(int F, int H, int K) {
+  return K == 2 && F == mf::kF && H % (kFusedSplit * mf::kHC) == 0;
+}
+
+// x0h [Bl][F] fp16, Wb = branch-0 weight [F][H] fp16 (branch 1 at + sW),
+// Wo [H][F] fp16, b0 fp32 bias of branch 0 (branch 1 at + sW); writes ff
+// [Bl][H], D [2][Bl][H] (fp16) and the split-K partials ws [kFusedSplit][Bl][F].
+inline int mbrb_fwd_fused(const __half* x0h, const __half* Wb, int64_t sW, const __half* Wo,
+                          const float* b0, int Bl, int H, __half* ff, __half* D, float* ws,
+                          cudaStream_t st) {
+  using namespace mf;
+  CUtensorMap tx, tw, to, tf, td;
+  int r = tmap_cache().get(&tx, x0h, kF, (uint64_t)Bl, 1, kF, 0, 64, kBM, 2);
+  if (r == EDPC_OK) r = tmap_cache().get(&tw, Wb, (uint64_t)H, kF, 2, (uint64_t)H, (uint64_t)sW, 64, 64, 3);
+  if (r == EDPC_OK) r = tmap_cache().get(&to, Wo, kF, (uint64_t)H, 1, kF, 0, 64, 64, 3);
+  if (r != EDPC_OK) return r;
+  if (!fused_map_cache().get(&tf, ff, (uint64_t)H, (uint64_t)Bl, 1) ||
+      !fused_map_cache().get(&td, D, (uint64_t)H, (uint64_t)Bl, 2)) {
+    set_error("mbrb_fwd_fused: fp16 store maps not encodable");
+    return EDPC_ERR_CUDA;
+  }
+  static bool attr[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 15]) {
+    cudaFuncSetAttribute(k_mbrb_fwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    attr[dev & 15] = true;
+  }
+  const unsigned grid = (unsigned)(cdiv(Bl, kBM) * kFusedSplit);
+  cudaError_t e = pdl_launch(k_mbrb_fwd_fused, grid, kThreads, kSmemBytes, st, tx, tw, to, tf, td, b0,
+                             sW, Bl, H, ws);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("k_mbrb_fwd_fused launch: ") + cudaGetErrorString(e));
+    return EDPC_ERR_CUDA;
+  }
+  return EDPC_OK;
+}
+
+}  // namespace edpc

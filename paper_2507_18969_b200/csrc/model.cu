@@ -25,6 +25,7 @@
 #include "kernels.cuh"
 #include "lte.cuh"
 #include "tc_gemm.cuh"
+#include "mbrb_fused.cuh"
 
 namespace edpc {
 
@@ -677,6 +678,17 @@ static cudaError_t wgrad_h(edpc_ctx* c, const __half* X, int Mw, const __half* G
 
 // --------------------------------------------------------------- forward
 
+// The fused MBRB forward (mbrb_fused.cuh) is bit-identical to the two-GEMM
+// path; EDPC_MBRB_FUSED=0 selects the latter for A/B timing.
+static bool mbrb_fused_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EDPC_MBRB_FUSED");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 struct MbrbBufs {
   float *x, *xhat, *rstd, *x0, *H, *ff, *out;
 };
@@ -704,6 +716,19 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
     __half* x0h = reinterpret_cast<__half*>(b.x0);
     __half* ffh = reinterpret_cast<__half*>(b.ff);
     __half* Dh = reinterpret_cast<__half*>(b.H);
+    if (mbrb_fused_enabled() && mbrb_fused_ok(F, H, L.K)) {
+      // branch GEMMs + product/GeLU + out-projection in one kernel (hidden
+      // tile on chip), then the fixed-order split reduction with bias and
+      // residual -- bit-identical to the two-GEMM path below
+      {
+        Scope sc(c, kRegGemm, c->st);
+        const int st = mbrb_fwd_fused(x0h, c->Wh + o.w0, o.wstride, c->Wh + o.out_w, c->W + o.b0,
+                                      Bl, H, ffh, Dh, c->ws, c->st);
+        if (st != EDPC_OK) return st;
+      }
+      CK(splitk_reduce(c, F, c->W + o.out_b, b.x, b.out, (int)c->rt));
+      return EDPC_OK;
+    }
     {
       Scope sc(c, kRegGemm, c->st);
       TcShape s{Bl, H, F, 2, 1, kBatchNone, kBatchZ, 0, 1, 0, 0, 0};

@@ -153,3 +153,27 @@ def test_tc_gemm_f16_unit(M, N, K, a_mn, b_mn):
     ref = A.astype(np.float64) @ B.astype(np.float64)
     err = np.abs(C - ref).max() / np.abs(ref).max()
     assert err < 1e-5, (err, C[:2, :4], ref[:2, :4])
+
+
+def test_fused_mbrb_forward_is_bit_identical():
+    """The fused MBRB forward (branch GEMMs + GeLU + out-projection in one
+    kernel, mbrb_fused.cuh) gives exactly the two-GEMM path's container
+    (EDPC_MBRB_FUSED=0, run in a subprocess: the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    from paper_2507_18969_b200 import compress, synth, write_container
+    cfg = ModelConfig(**PAPER, lanes=1024)
+    data = synth.text_like(1024 * 40, 1)
+    blob = write_container(compress(data, cfg, 64))
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = ("import sys; sys.path.insert(0, %r)\n"
+            "from paper_2507_18969_b200 import ModelConfig, compress, synth, write_container\n"
+            "cfg = ModelConfig(context_len=16, embed_dim=16, hidden_local=2048,\n"
+            "                  hidden_global=4096, lte_ratio=4, branches=2, lanes=1024)\n"
+            "sys.stdout.buffer.write(write_container(compress(synth.text_like(1024 * 40, 1), cfg, 64)))\n"
+            % root)
+    env = dict(os.environ, EDPC_MBRB_FUSED="0", PYTHONPATH=root)
+    ref = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
+                         timeout=600).stdout
+    assert blob == ref
