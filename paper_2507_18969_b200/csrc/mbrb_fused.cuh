@@ -11,7 +11,10 @@
 // the hidden dimension H, walked in chunks of kHC = 64 columns:
 //   warp 0       TMA producer: x0 tile once (resident, 64 KB), per chunk the
 //                two branch-weight boxes of each 64-deep k-block (ring of
-//                kB1Stages) and the chunk's 64 x 256 out-projection weight rows
+//                kB1Stages), running ahead of the epilogue
+//   warp 10      TMA producer of the chunk's 64 x 256 out-projection weight
+//                rows (its own thread, so the branch-weight ring never waits
+//                behind the out-projection's buffer)
 //   warp 1       TMEM allocation + single-thread MMA issuer:
 //                  MMA1(c): acc1[c & 1][z] = x0 . W_z[:, chunk c]   (N = 64)
 //                  MMA2(c-1): acc2 += ff(c-1) . W_out[chunk c-1, :] (N = 256)
@@ -45,7 +48,7 @@ constexpr int kF = 256;          // feature width (x0 row, out-projection N)
 constexpr int kHC = 64;          // hidden chunk
 constexpr int kB1Stages = 4;
 constexpr int kEW = 8;           // epilogue warps
-constexpr int kThreads = 32 * (2 + kEW);
+constexpr int kThreads = 32 * (2 + kEW + 1);  // + the out-projection weight producer
 constexpr int kA1Bytes = kBM * kF * 2;             // 64 KB resident x0 tile
 constexpr int kB1Stage = 2 * kHC * 64 * 2;          // both branches, one 64-deep k-block: 16 KB
 constexpr int kB2Bytes = kHC * kF * 2;              // 32 KB
@@ -127,7 +130,6 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
   if (warp == 0 && lane == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_x0) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_wb) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_wo) : "memory");
     mbar_init(a1full, 1);
     for (int s = 0; s < kB1Stages; ++s) {
       mbar_init(&b1full[s], 1);
@@ -174,6 +176,13 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
           tma_load_3d(dst, &tm_wb, &b1full[st], h0, kb * 64, 0);
           tma_load_3d(dst + kHC * 128, &tm_wb, &b1full[st], h0, kb * 64, 1);
         }
+      }
+    }
+  } else if (warp == 2 + kEW) {
+    if (lane == 0) {
+      // ---------------- out-projection weight producer
+      for (int c = 0; c < nc; ++c) {
+        const int h0 = h_begin + c * kHC;
         mbar_wait(b2empty, ((uint32_t)c & 1u) ^ 1u);
         mbar_expect_tx(b2full, kB2Bytes);
 #pragma unroll
@@ -230,7 +239,7 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
         }
       }
     }
-  } else {
+  } else if (warp < 2 + kEW) {
     // ---------------- epilogue (TMEM lane quadrant = warp % 4)
     const int quad = warp & 3;
     const int half = (warp - 2) >> 2;  // columns half*32 .. +32 of each chunk
