@@ -12,7 +12,7 @@
 //   warp 0       TMA producer: x0 tile once (resident, 64 KB), per chunk the
 //                two branch-weight boxes of each 64-deep k-block (ring of
 //                kB1Stages), running ahead of the epilogue
-//   warp 10      TMA producer of the chunk's 64 x 256 out-projection weight
+//   warp 2+kEW   TMA producer of the chunk's 64 x 256 out-projection weight
 //                rows (its own thread, so the branch-weight ring never waits
 //                behind the out-projection's buffer)
 //   warp 1       TMEM allocation + single-thread MMA issuer:
@@ -20,7 +20,8 @@
 //                  MMA2(c-1): acc2 += ff(c-1) . W_out[chunk c-1, :] (N = 256)
 //                MMA1 runs a chunk ahead so the epilogue of chunk c overlaps
 //                the MMAs of chunk c+1 (acc1 double-buffered in TMEM)
-//   warps 2-9    epilogue: tcgen05.ld of both branches (acc1 released right
+//   warps 2..    kEW = 16 epilogue warps (4 per TMEM lane quadrant, 16 columns
+//                of a chunk each): tcgen05.ld of both branches (acc1 released right
 //                after the load), bias / product / GeLU / GeLU', then ff into
 //                the shared-memory A operand of MMA2 (K-major, 128B swizzle)
 //                and D_z into staging tiles; one thread TMA-stores ff and D_z
@@ -47,7 +48,8 @@ constexpr int kBM = 128;
 constexpr int kF = 256;          // feature width (x0 row, out-projection N)
 constexpr int kHC = 64;          // hidden chunk
 constexpr int kB1Stages = 4;
-constexpr int kEW = 8;           // epilogue warps
+constexpr int kEW = 16;          // epilogue warps (kEW / 4 per TMEM lane quadrant)
+constexpr int kCW = kHC / (kEW / 4);  // columns of a chunk per epilogue warp
 constexpr int kThreads = 32 * (2 + kEW + 1);  // + the out-projection weight producer
 constexpr int kA1Bytes = kBM * kF * 2;             // 64 KB resident x0 tile
 constexpr int kB1Stage = 2 * kHC * 64 * 2;          // both branches, one 64-deep k-block: 16 KB
@@ -73,12 +75,36 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
       : "memory");
 }
 
-// 32 fp32 values -> fp16, into 64 bytes of a K-major SWIZZLE_128B row (row r
+// 32 lanes x 16 consecutive fp32 TMEM columns -> 16 registers per thread
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+        "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, float (&v)[N]) {
+  if constexpr (N == 32)
+    tmem_ld32(taddr, v);
+  else
+    tmem_ld16(taddr, v);
+}
+
+// N fp32 values -> fp16, into 2N bytes of a K-major SWIZZLE_128B row (row r
 // of a 128-byte-row tile): 16-byte chunk j (8 halves) at (j ^ (r & 7)).
-__device__ __forceinline__ void put_row_h_sw128(uint8_t* tile, int r, int j0, const float (&v)[32]) {
+template <int N>
+__device__ __forceinline__ void put_row_h_sw128(uint8_t* tile, int r, int j0, const float (&v)[N]) {
   uint8_t* row = tile + r * 128;
 #pragma unroll
-  for (int jj = 0; jj < 4; ++jj) {
+  for (int jj = 0; jj < N / 8; ++jj) {
     uint4 q;
     __half2 h0 = __floats2half2_rn(v[8 * jj], v[8 * jj + 1]);
     __half2 h1 = __floats2half2_rn(v[8 * jj + 2], v[8 * jj + 3]);
@@ -242,35 +268,38 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
   } else if (warp < 2 + kEW) {
     // ---------------- epilogue (TMEM lane quadrant = warp % 4)
     const int quad = warp & 3;
-    const int half = (warp - 2) >> 2;  // columns half*32 .. +32 of each chunk
+    const int half = (warp - 2) >> 2;  // columns half*kCW .. +kCW of each chunk
     const int r = quad * 32 + lane;    // tile row
     const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
-    const int et = threadIdx.x - 64;   // 0 .. 255
+    const int et = threadIdx.x - 64;   // 0 .. 32*kEW-1
     for (int c = 0; c < nc; ++c) {
       const int b = c & 1;
       const int h0 = h_begin + c * kHC;
-      const int n0 = h0 + half * 32;
+      const int n0 = h0 + half * kCW;
       mbar_wait(&tfull1[b], (uint32_t)(c >> 1) & 1u);
       tc_fence_after();
-      float v0[32], v1[32];
-      tmem_ld32(tq + (uint32_t)(b * 2 * kHC + half * 32), v0);
-      tmem_ld32(tq + (uint32_t)(b * 2 * kHC + kHC + half * 32), v1);
+      float v0[kCW], v1[kCW];
+      tmem_ldn<kCW>(tq + (uint32_t)(b * 2 * kHC + half * kCW), v0);
+      tmem_ldn<kCW>(tq + (uint32_t)(b * 2 * kHC + kHC + half * kCW), v1);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty1[b]);  // acc1[b] may take chunk c+2
       // EpiBranchActH's arithmetic, in its order
       {
-        float bb[32];
-        load32(b0 + n0, bb);
+        const float4* q0 = reinterpret_cast<const float4*>(b0 + n0);
+        const float4* q1 = reinterpret_cast<const float4*>(b0 + sBias + n0);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) v0[j] = v0[j] + bb[j];
-        load32(b0 + sBias + n0, bb);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v1[j] = v1[j] + bb[j];
+        for (int j = 0; j < kCW / 4; ++j) {
+          const float4 a = q0[j], bq = q1[j];
+          v0[4 * j] = v0[4 * j] + a.x; v0[4 * j + 1] = v0[4 * j + 1] + a.y;
+          v0[4 * j + 2] = v0[4 * j + 2] + a.z; v0[4 * j + 3] = v0[4 * j + 3] + a.w;
+          v1[4 * j] = v1[4 * j] + bq.x; v1[4 * j + 1] = v1[4 * j + 1] + bq.y;
+          v1[4 * j + 2] = v1[4 * j + 2] + bq.z; v1[4 * j + 3] = v1[4 * j + 3] + bq.w;
+        }
       }
-      float f[32], p[32];
+      float f[kCW], p[kCW];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
+      for (int j = 0; j < kCW; ++j) {
         p[j] = v0[j] * v1[j];
         gelu_pair(p[j], f[j], p[j]);
       }
@@ -279,13 +308,13 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
       mbar_wait(a2empty, ((uint32_t)c & 1u) ^ 1u);
       if (et == 0) bulk_wait_read<0>();
       named_bar(2, 32 * kEW);
-      put_row_h_sw128(sA2, r, half * 4, f);
+      put_row_h_sw128<kCW>(sA2, r, half * kCW / 8, f);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) f[j] = p[j] * v1[j];  // D_0 = GeLU' * H_1
-      put_row_h_sw128(sD, r, half * 4, f);
+      for (int j = 0; j < kCW; ++j) f[j] = p[j] * v1[j];  // D_0 = GeLU' * H_1
+      put_row_h_sw128<kCW>(sD, r, half * kCW / 8, f);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) f[j] = p[j] * v0[j];  // D_1 = GeLU' * H_0
-      put_row_h_sw128(sD + kBM * 128, r, half * 4, f);
+      for (int j = 0; j < kCW; ++j) f[j] = p[j] * v0[j];  // D_1 = GeLU' * H_0
+      put_row_h_sw128<kCW>(sD + kBM * 128, r, half * kCW / 8, f);
       fence_async_smem();
       named_bar(3, 32 * kEW);
       if (et == 0) {
@@ -301,7 +330,7 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
     tc_fence_after();
     const int m = m0 + r;
 #pragma unroll 1
-    for (int cb = half * 128; cb < half * 128 + 128; cb += 32) {
+    for (int cb = half * (kF * 4 / kEW); cb < (half + 1) * (kF * 4 / kEW); cb += 32) {
       float v[32];
       tmem_ld32(tq + 256u + (uint32_t)cb, v);
       if (m < Bl) {
