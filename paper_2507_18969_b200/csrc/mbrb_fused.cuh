@@ -47,7 +47,8 @@ namespace mf {
 constexpr int kBM = 128;
 constexpr int kF = 256;          // feature width (x0 row, out-projection N)
 constexpr int kHC = 64;          // hidden chunk
-constexpr int kB1Stages = 4;
+constexpr int kB1Stages = 5;
+constexpr int kPrefetch = 2;     // chunks of weights prefetched into L2 ahead of the ring
 constexpr int kEW = 16;          // epilogue warps (kEW / 4 per TMEM lane quadrant)
 constexpr int kCW = kHC / (kEW / 4);  // columns of a chunk per epilogue warp
 constexpr int kThreads = 32 * (2 + kEW + 1);  // + the out-projection weight producer
@@ -66,6 +67,13 @@ constexpr int kSmemBytes = 1024 + kOffBar + 256;
 }  // namespace mf
 
 constexpr int kFusedSplit = 4;  // = kSplitK of the unfused out-projection
+
+// L2 prefetch of a TMA box (no shared memory, no completion tracking)
+__device__ __forceinline__ void tma_prefetch_3d(const CUtensorMap* map, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 
 __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1,
                                              int c2) {
@@ -192,8 +200,14 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
 #pragma unroll
       for (int kb = 0; kb < kF / 64; ++kb) tma_load_3d(sA1 + kb * 16384, &tm_x0, a1full, kb * 64, m0, 0);
       int it = 0;
+      for (int c = 0; c < kPrefetch && c < nc; ++c)
+        for (int kb = 0; kb < kF / 64; ++kb)
+          for (int z = 0; z < 2; ++z) tma_prefetch_3d(&tm_wb, h_begin + c * kHC, kb * 64, z);
       for (int c = 0; c < nc; ++c) {
         const int h0 = h_begin + c * kHC;
+        if (c + kPrefetch < nc)  // the ring's source, kPrefetch chunks ahead, into L2
+          for (int kb = 0; kb < kF / 64; ++kb)
+            for (int z = 0; z < 2; ++z) tma_prefetch_3d(&tm_wb, h0 + kPrefetch * kHC, kb * 64, z);
         for (int kb = 0; kb < kF / 64; ++kb, ++it) {
           const int st = it % kB1Stages;
           mbar_wait(&b1empty[st], ((uint32_t)(it / kB1Stages) & 1u) ^ 1u);
@@ -209,6 +223,8 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
       // ---------------- out-projection weight producer
       for (int c = 0; c < nc; ++c) {
         const int h0 = h_begin + c * kHC;
+        if (c + 1 < nc)
+          for (int j = 0; j < kF / 64; ++j) tma_prefetch_3d(&tm_wo, j * 64, h0 + kHC, 0);
         mbar_wait(b2empty, ((uint32_t)c & 1u) ^ 1u);
         mbar_expect_tx(b2full, kB2Bytes);
 #pragma unroll
