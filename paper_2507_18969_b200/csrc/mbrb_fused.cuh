@@ -16,7 +16,8 @@
 //                rows (its own thread, so the branch-weight ring never waits
 //                behind the out-projection's buffer)
 //   warp 1       TMEM allocation + single-thread MMA issuer:
-//                  MMA1(c): acc1[c & 1][z] = x0 . W_z[:, chunk c]   (N = 64)
+//                  MMA1(c): acc1[c & 1][z] = x0 . W_z[:, chunk c]   (both
+//                           branches in one N = 128 instruction)
 //                  MMA2(c-1): acc2 += ff(c-1) . W_out[chunk c-1, :] (N = 256)
 //                MMA1 runs a chunk ahead so the epilogue of chunk c overlaps
 //                the MMAs of chunk c+1 (acc1 double-buffered in TMEM)
@@ -234,9 +235,16 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer
-      constexpr uint32_t id1 = idesc_f16(kBM, kHC, 0, 1);
+      // MMA1 computes both branches in one N = 128 instruction: the two 64-wide
+      // branch boxes of a stage sit 8 KB apart, i.e. two MN atoms (LBO 8192),
+      // landing in acc1 columns [0, 64) and [64, 128).  Descriptors are
+      // built once; the per-step offsets go into the 14-bit address field.
+      constexpr uint32_t id1 = idesc_f16(kBM, 2 * kHC, 0, 1);
       constexpr uint32_t id2 = idesc_f16(kBM, kF, 0, 1);
-      const uint32_t a1 = smem_u32(sA1), a2 = smem_u32(sA2), b2 = smem_u32(sB2);
+      const uint64_t d_a1 = sdesc(smem_u32(sA1), 16, 1024, kLayoutSW128);
+      const uint64_t d_b1 = sdesc(smem_u32(sB1), 8192, 1024, kLayoutSW128);
+      const uint64_t d_a2 = sdesc(smem_u32(sA2), 16, 1024, kLayoutSW128);
+      const uint64_t d_b2 = sdesc(smem_u32(sB2), 8192, 1024, kLayoutSW128);
       mbar_wait(a1full, 0);
       tc_fence_after();
       int it = 0;
@@ -249,17 +257,12 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
             const int st = it % kB1Stages;
             mbar_wait(&b1full[st], (uint32_t)(it / kB1Stages) & 1u);
             tc_fence_after();
-            const uint32_t sb = smem_u32(sB1 + st * kB1Stage);
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const uint64_t ad = sdesc(a1 + kb * 16384 + kk * 32, 16, 1024, kLayoutSW128);
-#pragma unroll
-              for (int z = 0; z < 2; ++z) {
-                const uint64_t bd = sdesc(sb + z * (kHC * 128) + kk * 2048, 8192, 1024, kLayoutSW128);
-                tc_mma_f16(tmem + (uint32_t)(b * 2 * kHC + z * kHC), ad, bd, id1,
-                           (kb > 0 || kk > 0) ? 1u : 0u);
-              }
-            }
+            for (int kk = 0; kk < 4; ++kk)
+              tc_mma_f16(tmem + (uint32_t)(b * 2 * kHC),
+                         d_a1 + (uint64_t)((kb * 16384 + kk * 32) >> 4),
+                         d_b1 + (uint64_t)((st * kB1Stage + kk * 2048) >> 4), id1,
+                         (kb > 0 || kk > 0) ? 1u : 0u);
             tc_commit(&b1empty[st]);
           }
           tc_commit(&tfull1[b]);
@@ -270,11 +273,9 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
           mbar_wait(b2full, (uint32_t)p & 1u);
           tc_fence_after();
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = sdesc(a2 + kk * 32, 16, 1024, kLayoutSW128);
-            const uint64_t bd = sdesc(b2 + kk * 2048, 8192, 1024, kLayoutSW128);
-            tc_mma_f16(tmem + 256u, ad, bd, id2, (p > 0 || kk > 0) ? 1u : 0u);
-          }
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma_f16(tmem + 256u, d_a2 + (uint64_t)((kk * 32) >> 4),
+                       d_b2 + (uint64_t)((kk * 2048) >> 4), id2, (p > 0 || kk > 0) ? 1u : 0u);
           tc_commit(b2empty);
           tc_commit(a2empty);
           if (p == nc - 1) tc_commit(t2full);
