@@ -21,12 +21,13 @@
 //                  MMA2(c-1): acc2 += ff(c-1) . W_out[chunk c-1, :] (N = 256)
 //                MMA1 runs a chunk ahead so the epilogue of chunk c overlaps
 //                the MMAs of chunk c+1 (acc1 double-buffered in TMEM)
+//   warp 3+kEW   store warp: TMA-stores each chunk's staged ff / D_z tiles and
+//                hands the staging back (mbarriers, no CTA-wide barriers)
 //   warps 2..    kEW = 16 epilogue warps (4 per TMEM lane quadrant, 16 columns
 //                of a chunk each): tcgen05.ld of both branches (acc1 released right
 //                after the load), bias / product / GeLU / GeLU', then ff into
 //                the shared-memory A operand of MMA2 (K-major, 128B swizzle)
-//                and D_z into staging tiles; one thread TMA-stores ff and D_z
-//                from those same tiles.  After the last chunk the 128 x 256
+//                and D_z into staging tiles, which the store warp copies out.  After the last chunk the 128 x 256
 //                fp32 accumulator acc2 goes to the split-K workspace; the
 //                existing k_splitk_reduce adds the slices in a fixed order
 //                with bias and residual.
@@ -48,11 +49,13 @@ namespace mf {
 constexpr int kBM = 128;
 constexpr int kF = 256;          // feature width (x0 row, out-projection N)
 constexpr int kHC = 64;          // hidden chunk
-constexpr int kB1Stages = 5;
+constexpr int kB1Stages = 4;
+constexpr int kMaxSlice = 1024;  // hidden columns per CTA whose branch biases sit in smem
 constexpr int kPrefetch = 2;     // chunks of weights prefetched into L2 ahead of the ring
 constexpr int kEW = 16;          // epilogue warps (kEW / 4 per TMEM lane quadrant)
 constexpr int kCW = kHC / (kEW / 4);  // columns of a chunk per epilogue warp
-constexpr int kThreads = 32 * (2 + kEW + 1);  // + the out-projection weight producer
+// + the out-projection weight producer and the store warp
+constexpr int kThreads = 32 * (2 + kEW + 2);
 constexpr int kA1Bytes = kBM * kF * 2;             // 64 KB resident x0 tile
 constexpr int kB1Stage = 2 * kHC * 64 * 2;          // both branches, one 64-deep k-block: 16 KB
 constexpr int kB2Bytes = kHC * kF * 2;              // 32 KB
@@ -63,7 +66,8 @@ constexpr int kOffB1 = kOffA1 + kA1Bytes;
 constexpr int kOffB2 = kOffB1 + kB1Stages * kB1Stage;
 constexpr int kOffA2 = kOffB2 + kB2Bytes;
 constexpr int kOffD = kOffA2 + kA2Bytes;
-constexpr int kOffBar = kOffD + kDBytes;
+constexpr int kOffBias = kOffD + kDBytes;              // [2][kMaxSlice] fp32
+constexpr int kOffBar = kOffBias + 2 * kMaxSlice * 4;
 constexpr int kSmemBytes = 1024 + kOffBar + 256;
 }  // namespace mf
 
@@ -142,6 +146,7 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
   uint8_t* sB2 = smem + kOffB2;
   uint8_t* sA2 = smem + kOffA2;
   uint8_t* sD = smem + kOffD;
+  float* sBiasT = reinterpret_cast<float*>(smem + kOffBias);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* a1full = bar;
   uint64_t* b1full = bar + 1;
@@ -150,9 +155,10 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
   uint64_t* b2empty = b2full + 1;
   uint64_t* tfull1 = b2empty + 1;   // [2]
   uint64_t* tempty1 = tfull1 + 2;   // [2]
-  uint64_t* a2full = tempty1 + 2;
-  uint64_t* a2empty = a2full + 1;
-  uint64_t* t2full = a2empty + 1;
+  uint64_t* staged = tempty1 + 2;   // ff / D_z of a chunk written (one arrive per epilogue warp)
+  uint64_t* a2empty = staged + 1;   // MMA2 done reading ff
+  uint64_t* sfree = a2empty + 1;    // the chunk's TMA stores done reading the staging tiles
+  uint64_t* t2full = sfree + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t2full + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -176,8 +182,9 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
       mbar_init(&tfull1[b], 1);
       mbar_init(&tempty1[b], kEW);
     }
-    mbar_init(a2full, 1);
+    mbar_init(staged, kEW);
     mbar_init(a2empty, 1);
+    mbar_init(sfree, 1);
     mbar_init(t2full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -232,6 +239,25 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
         for (int j = 0; j < kF / 64; ++j) tma_load_3d(sB2 + j * 8192, &tm_wo, b2full, j * 64, h0, 0);
       }
     }
+  } else if (warp == 3 + kEW) {
+    if (lane == 0) {
+      // ---------------- store warp: ff and D_z of each chunk to global once the
+      // epilogue warps have staged them; frees the staging tiles for the next
+      // chunk once the copies have read them
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_ff) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_d) : "memory");
+      for (int c = 0; c < nc; ++c) {
+        const int h0 = h_begin + c * kHC;
+        mbar_wait(staged, (uint32_t)c & 1u);
+        tma_store_3d(&tm_ff, sA2, h0, m0, 0);
+        tma_store_3d(&tm_d, sD, h0, m0, 0);
+        tma_store_3d(&tm_d, sD + kBM * 128, h0, m0, 1);
+        bulk_commit();
+        bulk_wait_read<0>();
+        mbar_arrive(sfree);
+      }
+      bulk_wait_all();
+    }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer
@@ -269,7 +295,7 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
         }
         if (c >= 1) {  // MMA2(c-1): acc2 += ff(c-1) . W_out[chunk c-1]
           const int p = c - 1;
-          mbar_wait(a2full, (uint32_t)p & 1u);
+          mbar_wait(staged, (uint32_t)p & 1u);
           mbar_wait(b2full, (uint32_t)p & 1u);
           tc_fence_after();
 #pragma unroll
@@ -288,11 +314,24 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
     const int half = (warp - 2) >> 2;  // columns half*kCW .. +kCW of each chunk
     const int r = quad * 32 + lane;    // tile row
     const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
-    const int et = threadIdx.x - 64;   // 0 .. 32*kEW-1
+    // the slice's branch biases, staged once in shared memory (global loads
+    // right behind the TMEM loads exposed their L2 latency every chunk)
+    for (int e = threadIdx.x - 64; e < 2 * hs; e += 32 * kEW)
+      sBiasT[e] = b0[(e >= hs ? sBias : 0) + h_begin + (e >= hs ? e - hs : e)];
+    named_bar(2, 32 * kEW);
     for (int c = 0; c < nc; ++c) {
       const int b = c & 1;
       const int h0 = h_begin + c * kHC;
-      const int n0 = h0 + half * kCW;
+      float4 bc0[kCW / 4], bc1[kCW / 4];
+      {
+        const float4* q0 = reinterpret_cast<const float4*>(sBiasT + c * kHC + half * kCW);
+        const float4* q1 = reinterpret_cast<const float4*>(sBiasT + hs + c * kHC + half * kCW);
+#pragma unroll
+        for (int j = 0; j < kCW / 4; ++j) {
+          bc0[j] = q0[j];
+          bc1[j] = q1[j];
+        }
+      }
       mbar_wait(&tfull1[b], (uint32_t)(c >> 1) & 1u);
       tc_fence_after();
       float v0[kCW], v1[kCW];
@@ -302,17 +341,13 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty1[b]);  // acc1[b] may take chunk c+2
       // EpiBranchActH's arithmetic, in its order
-      {
-        const float4* q0 = reinterpret_cast<const float4*>(b0 + n0);
-        const float4* q1 = reinterpret_cast<const float4*>(b0 + sBias + n0);
 #pragma unroll
-        for (int j = 0; j < kCW / 4; ++j) {
-          const float4 a = q0[j], bq = q1[j];
-          v0[4 * j] = v0[4 * j] + a.x; v0[4 * j + 1] = v0[4 * j + 1] + a.y;
-          v0[4 * j + 2] = v0[4 * j + 2] + a.z; v0[4 * j + 3] = v0[4 * j + 3] + a.w;
-          v1[4 * j] = v1[4 * j] + bq.x; v1[4 * j + 1] = v1[4 * j + 1] + bq.y;
-          v1[4 * j + 2] = v1[4 * j + 2] + bq.z; v1[4 * j + 3] = v1[4 * j + 3] + bq.w;
-        }
+      for (int j = 0; j < kCW / 4; ++j) {
+        const float4 a = bc0[j], bq = bc1[j];
+        v0[4 * j] = v0[4 * j] + a.x; v0[4 * j + 1] = v0[4 * j + 1] + a.y;
+        v0[4 * j + 2] = v0[4 * j + 2] + a.z; v0[4 * j + 3] = v0[4 * j + 3] + a.w;
+        v1[4 * j] = v1[4 * j] + bq.x; v1[4 * j + 1] = v1[4 * j + 1] + bq.y;
+        v1[4 * j + 2] = v1[4 * j + 2] + bq.z; v1[4 * j + 3] = v1[4 * j + 3] + bq.w;
       }
       float f[kCW], p[kCW];
 #pragma unroll
@@ -323,8 +358,7 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
       // staging free: MMA2(c-1) done reading ff, the TMA stores of c-1 done
       // reading ff / D
       mbar_wait(a2empty, ((uint32_t)c & 1u) ^ 1u);
-      if (et == 0) bulk_wait_read<0>();
-      named_bar(2, 32 * kEW);
+      mbar_wait(sfree, ((uint32_t)c & 1u) ^ 1u);
       put_row_h_sw128<kCW>(sA2, r, half * kCW / 8, f);
 #pragma unroll
       for (int j = 0; j < kCW; ++j) f[j] = p[j] * v1[j];  // D_0 = GeLU' * H_1
@@ -332,15 +366,9 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
 #pragma unroll
       for (int j = 0; j < kCW; ++j) f[j] = p[j] * v0[j];  // D_1 = GeLU' * H_0
       put_row_h_sw128<kCW>(sD + kBM * 128, r, half * kCW / 8, f);
-      fence_async_smem();
-      named_bar(3, 32 * kEW);
-      if (et == 0) {
-        mbar_arrive(a2full);
-        tma_store_3d(&tm_ff, sA2, h0, m0, 0);
-        tma_store_3d(&tm_d, sD, h0, m0, 0);
-        tma_store_3d(&tm_d, sD + kBM * 128, h0, m0, 1);
-        bulk_commit();
-      }
+      fence_async_smem();  // generic-proxy writes -> the MMA / TMA (async proxy)
+      __syncwarp();
+      if (lane == 0) mbar_arrive(staged);
     }
     // out-projection slice -> split-K workspace [split][Bl][F]
     mbar_wait(t2full, 0);
@@ -356,7 +384,6 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
         for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
       }
     }
-    if (et == 0) bulk_wait_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -405,7 +432,8 @@ inline FusedMapCache& fused_map_cache() {
 
 // shapes the fused kernel covers (else the caller takes the unfused path)
 inline bool mbrb_fused_ok(int F, int H, int K) {
-  return K == 2 && F == mf::kF && H % (kFusedSplit * mf::kHC) == 0;
+  return K == 2 && F == mf::kF && H % (kFusedSplit * mf::kHC) == 0 &&
+         H / kFusedSplit <= mf::kMaxSlice;
 }
 
 // x0h [Bl][F] fp16, Wb = branch-0 weight [F][H] fp16 (branch 1 at + sW),
