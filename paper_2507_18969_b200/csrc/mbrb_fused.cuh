@@ -15,12 +15,13 @@
 //   warp 2+kEW   TMA producer of the chunk's 64 x 256 out-projection weight
 //                rows (its own thread, so the branch-weight ring never waits
 //                behind the out-projection's buffer)
-//   warp 1       TMEM allocation + single-thread MMA issuer:
+//   warp 1       TMEM allocation + MMA1 issuer (one thread):
 //                  MMA1(c): acc1[c & 1][z] = x0 . W_z[:, chunk c]   (both
-//                           branches in one N = 128 instruction)
-//                  MMA2(c-1): acc2 += ff(c-1) . W_out[chunk c-1, :] (N = 256)
-//                MMA1 runs a chunk ahead so the epilogue of chunk c overlaps
-//                the MMAs of chunk c+1 (acc1 double-buffered in TMEM)
+//                           branches in one N = 128 instruction), issued as
+//                           soon as the epilogue has loaded acc1[c & 1] of
+//                           chunk c-2 (acc1 double-buffered in TMEM)
+//   warp 4+kEW   MMA2 issuer (one thread): acc2 += ff(c) . W_out[chunk c, :]
+//                (N = 256) once the epilogue has staged ff(c)
 //   warp 3+kEW   store warp: TMA-stores each chunk's staged ff / D_z tiles and
 //                hands the staging back (mbarriers, no CTA-wide barriers)
 //   warps 2..    kEW = 16 epilogue warps (4 per TMEM lane quadrant, 16 columns
@@ -54,8 +55,8 @@ constexpr int kMaxSlice = 1024;  // hidden columns per CTA whose branch biases s
 constexpr int kPrefetch = 2;     // chunks of weights prefetched into L2 ahead of the ring
 constexpr int kEW = 16;          // epilogue warps (kEW / 4 per TMEM lane quadrant)
 constexpr int kCW = kHC / (kEW / 4);  // columns of a chunk per epilogue warp
-// + the out-projection weight producer and the store warp
-constexpr int kThreads = 32 * (2 + kEW + 2);
+// + the out-projection weight producer, the store warp and the MMA2 issuer
+constexpr int kThreads = 32 * (2 + kEW + 3);
 constexpr int kA1Bytes = kBM * kF * 2;             // 64 KB resident x0 tile
 constexpr int kB1Stage = 2 * kHC * 64 * 2;          // both branches, one 64-deep k-block: 16 KB
 constexpr int kB2Bytes = kHC * kF * 2;              // 32 KB
@@ -115,19 +116,18 @@ __device__ __forceinline__ void tmem_ldn(uint32_t taddr, float (&v)[N]) {
 // of a 128-byte-row tile): 16-byte chunk j (8 halves) at (j ^ (r & 7)).
 template <int N>
 __device__ __forceinline__ void put_row_h_sw128(uint8_t* tile, int r, int j0, const float (&v)[N]) {
-  uint8_t* row = tile + r * 128;
+  const uint32_t row = smem_u32(tile) + (uint32_t)(r * 128);
 #pragma unroll
   for (int jj = 0; jj < N / 8; ++jj) {
-    uint4 q;
     __half2 h0 = __floats2half2_rn(v[8 * jj], v[8 * jj + 1]);
     __half2 h1 = __floats2half2_rn(v[8 * jj + 2], v[8 * jj + 3]);
     __half2 h2 = __floats2half2_rn(v[8 * jj + 4], v[8 * jj + 5]);
     __half2 h3 = __floats2half2_rn(v[8 * jj + 6], v[8 * jj + 7]);
-    q.x = *reinterpret_cast<uint32_t*>(&h0);
-    q.y = *reinterpret_cast<uint32_t*>(&h1);
-    q.z = *reinterpret_cast<uint32_t*>(&h2);
-    q.w = *reinterpret_cast<uint32_t*>(&h3);
-    *reinterpret_cast<uint4*>(row + (((j0 + jj) ^ (r & 7)) << 4)) = q;
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                     row + (uint32_t)(((j0 + jj) ^ (r & 7)) << 4)),
+                 "r"(*reinterpret_cast<uint32_t*>(&h0)), "r"(*reinterpret_cast<uint32_t*>(&h1)),
+                 "r"(*reinterpret_cast<uint32_t*>(&h2)), "r"(*reinterpret_cast<uint32_t*>(&h3))
+                 : "memory");
   }
 }
 
@@ -274,39 +274,47 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
       mbar_wait(a1full, 0);
       tc_fence_after();
       int it = 0;
-      for (int c = 0; c <= nc; ++c) {
-        if (c < nc) {  // MMA1(c)
-          const int b = c & 1;
-          mbar_wait(&tempty1[b], ((uint32_t)(c >> 1) & 1u) ^ 1u);
-          tc_fence_after();
-          for (int kb = 0; kb < kF / 64; ++kb, ++it) {
-            const int st = it % kB1Stages;
-            mbar_wait(&b1full[st], (uint32_t)(it / kB1Stages) & 1u);
-            tc_fence_after();
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              tc_mma_f16(tmem + (uint32_t)(b * 2 * kHC),
-                         d_a1 + (uint64_t)((kb * 16384 + kk * 32) >> 4),
-                         d_b1 + (uint64_t)((st * kB1Stage + kk * 2048) >> 4), id1,
-                         (kb > 0 || kk > 0) ? 1u : 0u);
-            tc_commit(&b1empty[st]);
-          }
-          tc_commit(&tfull1[b]);
-        }
-        if (c >= 1) {  // MMA2(c-1): acc2 += ff(c-1) . W_out[chunk c-1]
-          const int p = c - 1;
-          mbar_wait(staged, (uint32_t)p & 1u);
-          mbar_wait(b2full, (uint32_t)p & 1u);
+      for (int c = 0; c < nc; ++c) {  // MMA1(c), as soon as acc1[c & 1] is free
+        const int b = c & 1;
+        mbar_wait(&tempty1[b], ((uint32_t)(c >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        for (int kb = 0; kb < kF / 64; ++kb, ++it) {
+          const int st = it % kB1Stages;
+          mbar_wait(&b1full[st], (uint32_t)(it / kB1Stages) & 1u);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            tc_mma_f16(tmem + 256u, d_a2 + (uint64_t)((kk * 32) >> 4),
-                       d_b2 + (uint64_t)((kk * 2048) >> 4), id2, (p > 0 || kk > 0) ? 1u : 0u);
-          tc_commit(b2empty);
-          tc_commit(a2empty);
-          if (p == nc - 1) tc_commit(t2full);
+            tc_mma_f16(tmem + (uint32_t)(b * 2 * kHC),
+                       d_a1 + (uint64_t)((kb * 16384 + kk * 32) >> 4),
+                       d_b1 + (uint64_t)((st * kB1Stage + kk * 2048) >> 4), id1,
+                       (kb > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(&b1empty[st]);
         }
+        tc_commit(&tfull1[b]);
       }
+      (void)id2;
+      (void)d_a2;
+      (void)d_b2;
+    }
+  } else if (warp == 4 + kEW) {
+    if (lane == 0) {
+      // ---------------- MMA2 issuer (its own thread: MMA1 never waits behind
+      // an epilogue hand-off; the two write disjoint TMEM accumulators)
+      constexpr uint32_t id2 = idesc_f16(kBM, kF, 0, 1);
+      const uint64_t d_a2 = sdesc(smem_u32(sA2), 16, 1024, kLayoutSW128);
+      const uint64_t d_b2 = sdesc(smem_u32(sB2), 8192, 1024, kLayoutSW128);
+      for (int p = 0; p < nc; ++p) {  // acc2 += ff(p) . W_out[chunk p]
+        mbar_wait(staged, (uint32_t)p & 1u);
+        mbar_wait(b2full, (uint32_t)p & 1u);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc_mma_f16(tmem + 256u, d_a2 + (uint64_t)((kk * 32) >> 4),
+                     d_b2 + (uint64_t)((kk * 2048) >> 4), id2, (p > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(b2empty);
+        tc_commit(a2empty);
+      }
+      tc_commit(t2full);
     }
   } else if (warp < 2 + kEW) {
     // ---------------- epilogue (TMEM lane quadrant = warp % 4)
