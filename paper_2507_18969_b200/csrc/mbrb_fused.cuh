@@ -31,7 +31,9 @@
 //                and D_z into staging tiles, which the store warp copies out.  After the last chunk the 128 x 256
 //                fp32 accumulator acc2 goes to the split-K workspace; the
 //                existing k_splitk_reduce adds the slices in a fixed order
-//                with bias and residual.
+//                with bias and residual -- done in the kernel: the kFusedSplit
+//                CTAs of a row tile are one thread-block cluster and sum their
+//                partials over distributed shared memory in rank order.
 // TMEM: acc1 2 x 2 x 64 columns + acc2 256 columns = 512.
 //
 // The arithmetic is the unfused path's, operation for operation: the branch
@@ -137,7 +139,8 @@ __global__ void __launch_bounds__(mf::kThreads, 1)
 k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constant__ CUtensorMap tm_wb,
                  const __grid_constant__ CUtensorMap tm_wo, const __grid_constant__ CUtensorMap tm_ff,
                  const __grid_constant__ CUtensorMap tm_d, const float* __restrict__ b0,
-                 int64_t sBias, int Bl, int H, float* __restrict__ ws) {
+                 int64_t sBias, int Bl, int H, const float* __restrict__ bias_out,
+                 const float* __restrict__ resid, float* __restrict__ out, int rt) {
   using namespace mf;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -199,6 +202,13 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (warp == 0 && lane == 0) {  // weights into L2 while the predecessor drains
+    for (int c = 0; c < kPrefetch && c < nc; ++c) {
+      for (int kb = 0; kb < kF / 64; ++kb)
+        for (int z = 0; z < 2; ++z) tma_prefetch_3d(&tm_wb, h_begin + c * kHC, kb * 64, z);
+      for (int j = 0; j < kF / 64; ++j) tma_prefetch_3d(&tm_wo, j * 64, h_begin + c * kHC, 0);
+    }
+  }
   pdl_entry();
 
   if (warp == 0) {
@@ -208,9 +218,6 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
 #pragma unroll
       for (int kb = 0; kb < kF / 64; ++kb) tma_load_3d(sA1 + kb * 16384, &tm_x0, a1full, kb * 64, m0, 0);
       int it = 0;
-      for (int c = 0; c < kPrefetch && c < nc; ++c)
-        for (int kb = 0; kb < kF / 64; ++kb)
-          for (int z = 0; z < 2; ++z) tma_prefetch_3d(&tm_wb, h_begin + c * kHC, kb * 64, z);
       for (int c = 0; c < nc; ++c) {
         const int h0 = h_begin + c * kHC;
         if (c + kPrefetch < nc)  // the ring's source, kPrefetch chunks ahead, into L2
@@ -378,23 +385,72 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
       __syncwarp();
       if (lane == 0) mbar_arrive(staged);
     }
-    // out-projection slice -> split-K workspace [split][Bl][F]
+    // acc2 (this slice's out-projection partial) -> own shared memory, fp32
+    // rows padded to kF + 4 floats (conflict-free row-per-thread writes);
+    // every operand buffer is dead by now (t2full: all MMAs done)
     mbar_wait(t2full, 0);
     tc_fence_after();
-    const int m = m0 + r;
+  }
+  tc_fence_before();
+  __syncthreads();  // the store warp has drained its TMA stores, every MMA is done
+  constexpr int kLd = kF + 4;
+  float* sP = reinterpret_cast<float*>(smem);
+  if (warp >= 2 && warp < 2 + kEW) {
+    const int quad = warp & 3, half = (warp - 2) >> 2, r = quad * 32 + lane;
+    const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
     for (int cb = half * (kF * 4 / kEW); cb < (half + 1) * (kF * 4 / kEW); cb += 32) {
       float v[32];
       tmem_ld32(tq + 256u + (uint32_t)cb, v);
-      if (m < Bl) {
-        float4* dst = reinterpret_cast<float4*>(ws + ((int64_t)split * Bl + m) * kF + cb);
+      const uint32_t dst = smem_u32(sP + r * kLd + cb);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) dst[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      for (int j = 0; j < 8; ++j)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16 * j), "f"(v[4 * j]),
+                     "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                     : "memory");
+    }
+  }
+  cluster_sync_all();
+  // the kFusedSplit CTAs of this row tile form the cluster; CTA q sums column
+  // quarter q of the four partials in rank order -- ((p0 + p1) + p2) + p3,
+  // then + bias, then + residual: k_splitk_reduce's order, bit for bit -- and
+  // writes the block output (tf32-rounded when it feeds a tf32 GEMM)
+  {
+    const uint32_t q = cluster_rank();
+    constexpr int kQ = kF / kFusedSplit;       // 64 columns
+    for (int e = threadIdx.x; e < kBM * kQ / 4; e += kThreads) {
+      const int row = e / (kQ / 4), col = (int)q * kQ + 4 * (e % (kQ / 4));
+      const int m = m0 + row;
+      const uint32_t la = smem_u32(sP + row * kLd + col);
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int rk = 0; rk < kFusedSplit; ++rk) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rk));
+        float4 w;
+        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(w.x), "=f"(w.y), "=f"(w.z), "=f"(w.w)
+                     : "r"(ra)
+                     : "memory");
+        if (rk == 0) {
+          a = w;
+        } else {
+          a.x += w.x; a.y += w.y; a.z += w.z; a.w += w.w;
+        }
+      }
+      if (m < Bl) {
+        const float4 b = *reinterpret_cast<const float4*>(bias_out + col);
+        const float4 x = *reinterpret_cast<const float4*>(resid + (int64_t)m * kF + col);
+        a.x += b.x; a.y += b.y; a.z += b.z; a.w += b.w;
+        a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+        if (rt) {
+          a.x = tf32_rna(a.x); a.y = tf32_rna(a.y); a.z = tf32_rna(a.z); a.w = tf32_rna(a.w);
+        }
+        *reinterpret_cast<float4*>(out + (int64_t)m * kF + col) = a;
       }
     }
   }
-  tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // no CTA leaves while a peer may still read its partial
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -446,9 +502,12 @@ inline bool mbrb_fused_ok(int F, int H, int K) {
 
 // x0h [Bl][F] fp16, Wb = branch-0 weight [F][H] fp16 (branch 1 at + sW),
 // Wo [H][F] fp16, b0 fp32 bias of branch 0 (branch 1 at + sW); writes ff
-// [Bl][H], D [2][Bl][H] (fp16) and the split-K partials ws [kFusedSplit][Bl][F].
+// [Bl][H], D [2][Bl][H] (fp16) and out [Bl][F] = ff . Wo + bias_out + resid
+// (rounded to tf32 when rt).  Clusters of kFusedSplit CTAs (the H slices of
+// one row tile) reduce the slices over DSMEM.
 inline int mbrb_fwd_fused(const __half* x0h, const __half* Wb, int64_t sW, const __half* Wo,
-                          const float* b0, int Bl, int H, __half* ff, __half* D, float* ws,
+                          const float* b0, int Bl, int H, __half* ff, __half* D,
+                          const float* bias_out, const float* resid, float* out, int rt,
                           cudaStream_t st) {
   using namespace mf;
   CUtensorMap tx, tw, to, tf, td;
@@ -468,9 +527,22 @@ inline int mbrb_fwd_fused(const __half* x0h, const __half* Wb, int64_t sW, const
     cudaFuncSetAttribute(k_mbrb_fwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
     attr[dev & 15] = true;
   }
-  const unsigned grid = (unsigned)(cdiv(Bl, kBM) * kFusedSplit);
-  cudaError_t e = pdl_launch(k_mbrb_fwd_fused, grid, kThreads, kSmemBytes, st, tx, tw, to, tf, td, b0,
-                             sW, Bl, H, ws);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(cdiv(Bl, kBM) * kFusedSplit));
+  cfg.blockDim = dim3((unsigned)kThreads);
+  cfg.dynamicSmemBytes = (size_t)kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr2[2];
+  attr2[0].id = cudaLaunchAttributeClusterDimension;
+  attr2[0].val.clusterDim.x = (unsigned)kFusedSplit;
+  attr2[0].val.clusterDim.y = 1;
+  attr2[0].val.clusterDim.z = 1;
+  attr2[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr2[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr2;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_mbrb_fwd_fused, tx, tw, to, tf, td, b0, sW, Bl, H,
+                                     bias_out, resid, out, rt);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_mbrb_fwd_fused launch: ") + cudaGetErrorString(e));

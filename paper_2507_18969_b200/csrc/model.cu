@@ -718,16 +718,11 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
     __half* Dh = reinterpret_cast<__half*>(b.H);
     if (mbrb_fused_enabled() && mbrb_fused_ok(F, H, L.K)) {
       // branch GEMMs + product/GeLU + out-projection in one kernel (hidden
-      // tile on chip), then the fixed-order split reduction with bias and
-      // residual -- bit-identical to the two-GEMM path below
-      {
-        Scope sc(c, kRegGemm, c->st);
-        const int st = mbrb_fwd_fused(x0h, c->Wh + o.w0, o.wstride, c->Wh + o.out_w, c->W + o.b0,
-                                      Bl, H, ffh, Dh, c->ws, c->st);
-        if (st != EDPC_OK) return st;
-      }
-      CK(splitk_reduce(c, F, c->W + o.out_b, b.x, b.out, (int)c->rt));
-      return EDPC_OK;
+      // tile on chip; the fixed-order split reduction with bias and residual
+      // over DSMEM in the same kernel) -- bit-identical to the two-GEMM path
+      Scope sc(c, kRegGemm, c->st);
+      return mbrb_fwd_fused(x0h, c->Wh + o.w0, o.wstride, c->Wh + o.out_w, c->W + o.b0, Bl, H, ffh,
+                            Dh, c->W + o.out_b, b.x, b.out, (int)c->rt, c->st);
     }
     {
       Scope sc(c, kRegGemm, c->st);
