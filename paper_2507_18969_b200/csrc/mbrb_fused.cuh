@@ -551,4 +551,358 @@ inline int mbrb_fwd_fused(const __half* x0h, const __half* Wb, int64_t sW, const
   return EDPC_OK;
 }
 
+
+
+// ===================================================================
+// Fused MBRB backward (model.py:105-121): the out-projection dgrad, the
+// product-rule epilogue and the branch dgrad in one kernel.
+//
+//   g_ff  = g_up . W_out^T                      (g_up fp16 [Bl][F], per H chunk)
+//   g_H_z = g_ff * D_z                          (D_z from the forward; stored fp16:
+//                                                the branch weight gradients)
+//   g_x0  = sum_z g_H_z . W_z^T                 (accumulated over the CTA's H slice)
+//
+// Same skeleton as the forward: a CTA owns a 128-row tile and one H slice in
+// chunks of 64; MMA1 (N = 64, K = F) into a double-buffered TMEM accumulator,
+// the epilogue multiplies by the D_z tiles that a loader warp TMA-loads into
+// double-buffered staging tiles and writes g_H_z back in place -- the staging
+// tiles then serve as the A operands of MMA2 (acc2 += g_H_z . W_z^T, N = F)
+// and as the source of the g_H_z TMA stores.  The 4 slices of a row tile are
+// a cluster and reduce over DSMEM in rank order.  MMA2 walks each 64-deep
+// block as branch 0 then branch 1, the order of the unfused split-K dgrad
+// (tc_gemm.cuh kBatchSum), so the result is bit-identical to it.
+namespace mb {
+constexpr int kBM = 128, kF = 256, kHC = 64, kEW = 16, kCW = kHC / (kEW / 4);
+constexpr int kB1Stages = 4;
+constexpr int kThreads = 32 * (2 + kEW + 3);  // + W_z producer, store/D loader, MMA2 issuer
+constexpr int kA1Bytes = kBM * kF * 2;        // g_up tile, 64 KB
+constexpr int kB1Stage = kHC * 64 * 2;        // W_out rows of the chunk, one 64-deep k-block: 8 KB
+constexpr int kB2Bytes = 2 * kF * kHC * 2;    // both branches' W_z^T blocks: 64 KB
+constexpr int kTile = kBM * kHC * 2;          // one 128 x 64 fp16 tile: 16 KB
+constexpr int kOffA1 = 0;
+constexpr int kOffB1 = kOffA1 + kA1Bytes;
+constexpr int kOffB2 = kOffB1 + kB1Stages * kB1Stage;
+constexpr int kOffS = kOffB2 + kB2Bytes;      // staging [2 buffers][2 branches] tiles
+constexpr int kOffBar = kOffS + 4 * kTile;
+constexpr int kSmemBytes = 1024 + kOffBar + 256;
+}  // namespace mb
+
+__global__ void __launch_bounds__(mb::kThreads, 1)
+k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_wo,
+                 const __grid_constant__ CUtensorMap tm_wb, const __grid_constant__ CUtensorMap tm_d,
+                 const __grid_constant__ CUtensorMap tm_gh, int Bl, int H, float* __restrict__ out) {
+  using namespace mb;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA1 = smem + kOffA1;
+  uint8_t* sB1 = smem + kOffB1;
+  uint8_t* sB2 = smem + kOffB2;
+  uint8_t* sS = smem + kOffS;  // buffer u, branch z at sS + (2u + z) * kTile
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* a1full = bar;
+  uint64_t* b1full = bar + 1;
+  uint64_t* b1empty = b1full + kB1Stages;
+  uint64_t* b2full = b1empty + kB1Stages;
+  uint64_t* b2empty = b2full + 1;
+  uint64_t* tfull1 = b2empty + 1;  // [2]
+  uint64_t* tempty1 = tfull1 + 2;  // [2]
+  uint64_t* dfull = tempty1 + 2;   // [2] D tiles of a chunk loaded into staging buffer u
+  uint64_t* staged = dfull + 2;    // g_H of a chunk written (one arrive per epilogue warp)
+  uint64_t* a2empty = staged + 1;  // MMA2 done with a chunk's staging buffer
+  uint64_t* t2full = a2empty + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t2full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tile = blockIdx.x / kFusedSplit, split = blockIdx.x % kFusedSplit;
+  const int m0 = tile * kBM;
+  const int hs = H / kFusedSplit;
+  const int h_begin = split * hs;
+  const int nc = hs / kHC;
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_g) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_wo) : "memory");
+    mbar_init(a1full, 1);
+    for (int s = 0; s < kB1Stages; ++s) {
+      mbar_init(&b1full[s], 1);
+      mbar_init(&b1empty[s], 1);
+    }
+    mbar_init(b2full, 1);
+    mbar_init(b2empty, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tfull1[b], 1);
+      mbar_init(&tempty1[b], kEW);
+      mbar_init(&dfull[b], 1);
+    }
+    mbar_init(staged, kEW);
+    mbar_init(a2empty, 1);
+    mbar_init(t2full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 0 && lane == 0) {  // weights into L2 while the predecessor drains
+    for (int c = 0; c < 2 && c < nc; ++c) {
+      for (int kb = 0; kb < kF / 64; ++kb) tma_prefetch_3d(&tm_wo, kb * 64, h_begin + c * kHC, 0);
+      for (int z = 0; z < 2; ++z) tma_prefetch_3d(&tm_wb, h_begin + c * kHC, 0, z);
+    }
+  }
+  pdl_entry();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- producer: g_up tile once, W_out rows per chunk
+      mbar_expect_tx(a1full, kA1Bytes);
+#pragma unroll
+      for (int kb = 0; kb < kF / 64; ++kb) tma_load_3d(sA1 + kb * 16384, &tm_g, a1full, kb * 64, m0, 0);
+      int it = 0;
+      for (int c = 0; c < nc; ++c) {
+        const int h0 = h_begin + c * kHC;
+        if (c + 2 < nc)
+          for (int kb = 0; kb < kF / 64; ++kb) tma_prefetch_3d(&tm_wo, kb * 64, h0 + 2 * kHC, 0);
+        for (int kb = 0; kb < kF / 64; ++kb, ++it) {
+          const int st = it % kB1Stages;
+          mbar_wait(&b1empty[st], ((uint32_t)(it / kB1Stages) & 1u) ^ 1u);
+          mbar_expect_tx(&b1full[st], kB1Stage);
+          tma_load_3d(sB1 + st * kB1Stage, &tm_wo, &b1full[st], kb * 64, h0, 0);
+        }
+      }
+    }
+  } else if (warp == 2 + kEW) {
+    if (lane == 0) {
+      // ---------------- W_z^T producer (both branches, K-major boxes of 64 x 256)
+      for (int c = 0; c < nc; ++c) {
+        const int h0 = h_begin + c * kHC;
+        if (c + 1 < nc)
+          for (int z = 0; z < 2; ++z) tma_prefetch_3d(&tm_wb, h0 + kHC, 0, z);
+        mbar_wait(b2empty, ((uint32_t)c & 1u) ^ 1u);
+        mbar_expect_tx(b2full, kB2Bytes);
+        for (int z = 0; z < 2; ++z) tma_load_3d(sB2 + z * (kF * 128), &tm_wb, b2full, h0, 0, z);
+      }
+    }
+  } else if (warp == 3 + kEW) {
+    if (lane == 0) {
+      // ---------------- D loader + g_H store warp
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_d) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_gh) : "memory");
+      auto load_d = [&](int c) {
+        const int u = c & 1;
+        mbar_expect_tx(&dfull[u], 2 * kTile);
+        for (int z = 0; z < 2; ++z)
+          tma_load_3d(sS + (2 * u + z) * kTile, &tm_d, &dfull[u], h_begin + c * kHC, m0, z);
+      };
+      for (int c = 0; c < 2 && c < nc; ++c) load_d(c);
+      for (int c = 0; c < nc; ++c) {
+        const int u = c & 1, h0 = h_begin + c * kHC;
+        mbar_wait(staged, (uint32_t)c & 1u);
+        for (int z = 0; z < 2; ++z) tma_store_3d(&tm_gh, sS + (2 * u + z) * kTile, h0, m0, z);
+        bulk_commit();
+        if (c + 2 < nc) {  // buffer u takes chunk c+2 once the stores and MMA2(c) have read it
+          bulk_wait_read<0>();
+          mbar_wait(a2empty, (uint32_t)c & 1u);
+          load_d(c + 2);
+        }
+      }
+      bulk_wait_all();
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA1 issuer: g_ff(c) = g_up . W_out[chunk c]^T
+      constexpr uint32_t id1 = idesc_f16(kBM, kHC, 0, 0);
+      const uint64_t d_a1 = sdesc(smem_u32(sA1), 16, 1024, kLayoutSW128);
+      const uint64_t d_b1 = sdesc(smem_u32(sB1), 16, 1024, kLayoutSW128);
+      mbar_wait(a1full, 0);
+      tc_fence_after();
+      int it = 0;
+      for (int c = 0; c < nc; ++c) {
+        const int b = c & 1;
+        mbar_wait(&tempty1[b], ((uint32_t)(c >> 1) & 1u) ^ 1u);
+        tc_fence_after();
+        for (int kb = 0; kb < kF / 64; ++kb, ++it) {
+          const int st = it % kB1Stages;
+          mbar_wait(&b1full[st], (uint32_t)(it / kB1Stages) & 1u);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma_f16(tmem + (uint32_t)(b * kHC), d_a1 + (uint64_t)((kb * 16384 + kk * 32) >> 4),
+                       d_b1 + (uint64_t)((st * kB1Stage + kk * 32) >> 4), id1,
+                       (kb > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(&b1empty[st]);
+        }
+        tc_commit(&tfull1[b]);
+      }
+    }
+  } else if (warp == 4 + kEW) {
+    if (lane == 0) {
+      // ---------------- MMA2 issuer: acc2 += g_H_0 . W_0^T + g_H_1 . W_1^T per chunk
+      constexpr uint32_t id2 = idesc_f16(kBM, kF, 0, 0);
+      const uint64_t d_s = sdesc(smem_u32(sS), 16, 1024, kLayoutSW128);
+      const uint64_t d_b2 = sdesc(smem_u32(sB2), 16, 1024, kLayoutSW128);
+      for (int c = 0; c < nc; ++c) {
+        const int u = c & 1;
+        mbar_wait(staged, (uint32_t)c & 1u);
+        mbar_wait(b2full, (uint32_t)c & 1u);
+        tc_fence_after();
+#pragma unroll
+        for (int z = 0; z < 2; ++z)
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma_f16(tmem + 256u, d_s + (uint64_t)(((2 * u + z) * kTile + kk * 32) >> 4),
+                       d_b2 + (uint64_t)((z * (kF * 128) + kk * 32) >> 4), id2,
+                       (c > 0 || z > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(b2empty);
+        tc_commit(a2empty);
+      }
+      tc_commit(t2full);
+    }
+  } else if (warp < 2 + kEW) {
+    // ---------------- epilogue: g_H_z = g_ff * D_z, in place in the staging tiles
+    const int quad = warp & 3, half = (warp - 2) >> 2, r = quad * 32 + lane;
+    const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
+    for (int c = 0; c < nc; ++c) {
+      const int b = c & 1, u = c & 1;
+      mbar_wait(&tfull1[b], (uint32_t)(c >> 1) & 1u);
+      tc_fence_after();
+      float g[kCW];
+      tmem_ldn<kCW>(tq + (uint32_t)(b * kHC + half * kCW), g);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty1[b]);
+      mbar_wait(&dfull[u], (uint32_t)(c >> 1) & 1u);
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        const uint32_t row = smem_u32(sS + (2 * u + z) * kTile) + (uint32_t)(r * 128);
+#pragma unroll
+        for (int jj = 0; jj < kCW / 8; ++jj) {
+          const uint32_t a = row + (uint32_t)(((half * kCW / 8 + jj) ^ (r & 7)) << 4);
+          uint32_t w[4];
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                       : "r"(a));
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {  // EpiBwdActH: g_H = g_ff * D, rounded to fp16
+            const float2 d = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
+            __half2 o = __floats2half2_rn(g[8 * jj + 2 * q] * d.x, g[8 * jj + 2 * q + 1] * d.y);
+            w[q] = *reinterpret_cast<uint32_t*>(&o);
+          }
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w[0]), "r"(w[1]),
+                       "r"(w[2]), "r"(w[3])
+                       : "memory");
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(staged);
+    }
+    mbar_wait(t2full, 0);
+    tc_fence_after();
+  }
+  tc_fence_before();
+  __syncthreads();
+  constexpr int kLd = kF + 4;
+  float* sP = reinterpret_cast<float*>(smem);
+  if (warp >= 2 && warp < 2 + kEW) {
+    const int quad = warp & 3, half = (warp - 2) >> 2, r = quad * 32 + lane;
+    const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+    for (int cb = half * (kF * 4 / kEW); cb < (half + 1) * (kF * 4 / kEW); cb += 32) {
+      float v[32];
+      tmem_ld32(tq + 256u + (uint32_t)cb, v);
+      const uint32_t dst = smem_u32(sP + r * kLd + cb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + 16 * j), "f"(v[4 * j]),
+                     "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                     : "memory");
+    }
+  }
+  cluster_sync_all();
+  {  // column quarter q of the 4 slice partials, in rank order (k_splitk_reduce's)
+    const uint32_t q = cluster_rank();
+    constexpr int kQ = kF / kFusedSplit;
+    for (int e = threadIdx.x; e < kBM * kQ / 4; e += kThreads) {
+      const int row = e / (kQ / 4), col = (int)q * kQ + 4 * (e % (kQ / 4));
+      const int m = m0 + row;
+      const uint32_t la = smem_u32(sP + row * kLd + col);
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int rk = 0; rk < kFusedSplit; ++rk) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(la), "r"(rk));
+        float4 w;
+        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(w.x), "=f"(w.y), "=f"(w.z), "=f"(w.w)
+                     : "r"(ra)
+                     : "memory");
+        if (rk == 0) {
+          a = w;
+        } else {
+          a.x += w.x; a.y += w.y; a.z += w.z; a.w += w.w;
+        }
+      }
+      if (m < Bl) *reinterpret_cast<float4*>(out + (int64_t)m * kF + col) = a;
+    }
+  }
+  cluster_sync_all();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// guph [Bl][F] fp16 (the block-output gradient), Wo [H][F] fp16, Wb = branch-0
+// weight [F][H] fp16 (branch 1 at + sW), D [2][Bl][H] fp16 from the forward;
+// writes g_H [2][Bl][H] fp16 and out [Bl][F] fp32 = sum_z g_H_z . W_z^T.
+inline int mbrb_bwd_fused(const __half* guph, const __half* Wo, const __half* Wb, int64_t sW,
+                          const __half* D, __half* GH, int Bl, int H, float* out, cudaStream_t st) {
+  using namespace mb;
+  CUtensorMap tg, to, tw, td, th;
+  int r = tmap_cache().get(&tg, guph, kF, (uint64_t)Bl, 1, kF, 0, 64, kBM, 2);
+  if (r == EDPC_OK) r = tmap_cache().get(&to, Wo, kF, (uint64_t)H, 1, kF, 0, 64, 64, 2);
+  if (r == EDPC_OK) r = tmap_cache().get(&tw, Wb, (uint64_t)H, kF, 2, (uint64_t)H, (uint64_t)sW, 64, 256, 2);
+  if (r != EDPC_OK) return r;
+  if (!fused_map_cache().get(&td, D, (uint64_t)H, (uint64_t)Bl, 2) ||
+      !fused_map_cache().get(&th, GH, (uint64_t)H, (uint64_t)Bl, 2)) {
+    set_error("mbrb_bwd_fused: fp16 tile maps not encodable");
+    return EDPC_ERR_CUDA;
+  }
+  static bool attr[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 15]) {
+    cudaFuncSetAttribute(k_mbrb_bwd_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes);
+    attr[dev & 15] = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(cdiv(Bl, kBM) * kFusedSplit));
+  cfg.blockDim = dim3((unsigned)kThreads);
+  cfg.dynamicSmemBytes = (size_t)kSmemBytes;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)kFusedSplit;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_mbrb_bwd_fused, tg, to, tw, td, th, Bl, H, out);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("k_mbrb_bwd_fused launch: ") + cudaGetErrorString(e));
+    return EDPC_ERR_CUDA;
+  }
+  return EDPC_OK;
+}
+
 }  // namespace edpc

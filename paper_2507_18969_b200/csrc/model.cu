@@ -860,6 +860,22 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
     const __half* Dh = reinterpret_cast<const __half*>(b.H);
     __half* GHh = reinterpret_cast<__half*>(GH);
     // guph: the fp16 copy of g_up, written by the dgrad that produced g_up (EpiStore2)
+    if (mbrb_fused_enabled() && mbrb_fused_ok(F, H, K)) {
+      // out-projection weight gradient on the side stream (needs g_up, ff);
+      // out-proj dgrad + product rule + branch dgrad (+ its split reduction)
+      // in one kernel (bit-identical to the three-launch path below); then the
+      // branch weight gradients from the g_H it stored
+      CK(fork_aux(c));
+      CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0, o.out_b));
+      {
+        Scope sc(c, kRegGemm, c->st);
+        const int st = mbrb_bwd_fused(guph, c->Wh + o.out_w, c->Wh + o.w0, o.wstride, Dh, GHh, Bl,
+                                      H, c->gx0, c->st);
+        if (st != EDPC_OK) return st;
+      }
+      CK(fork_aux(c));
+      CK(wgrad_h(c, x0h, F, GHh, H, K, plane, o.w0, o.wstride, o.b0));
+    } else {
     // g_ff = g_up . out_w^T (out_w [H][F] = K-major B), epilogue -> g_H[z]
     {
       Scope sc(c, kRegGemm, c->st);
@@ -874,6 +890,7 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
     CK(wgrad_h(c, x0h, F, GHh, H, K, plane, o.w0, o.wstride, o.b0));
     // g_x0 = sum_z g_H[z] . W_z^T (W_z [F][H] = K-major B)
     CK(dgrad_h(c, GHh, H, K, plane, c->Wh + o.w0, o.wstride, F, c->gx0));
+    }
   } else {
   // g_ff = g_up . out_w^T, epilogue -> GH[z] (product rule + GeLU')
   CK(dgrad(c, g_up, F, 1, 0, wt(c) + o.out_w, 0, H, EpiBwdAct{b.H, GH, K, plane, H}));

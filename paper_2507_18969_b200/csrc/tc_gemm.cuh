@@ -589,8 +589,11 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
           const int st = it % kStages;
           const uint32_t ph = (uint32_t)(it / kStages) & 1u;
           mbar_wait(&empty[st], ph ^ 1u);
-          const int sub = q / nkb;
-          const int k = kb0 + (q - sub * nkb) * BK;
+          // summed sub-problems (kBatchSum: the MBRB branches of the branch
+          // dgrad) interleave per k-block -- branch 0 then branch 1 of each
+          // 64-deep block, the order of the fused MBRB backward (mbrb_fused.cuh)
+          const int sub = q % s.nsum;
+          const int k = kb0 + (q / s.nsum) * BK;
           const int az = s.a_batch == kBatchZ ? zb : (s.a_batch == kBatchSum ? sub : 0);
           const int bz = s.b_batch == kBatchZ ? zb : (s.b_batch == kBatchSum ? sub : 0);
           uint8_t* sa = smem + st * SM::kStageBytes;
