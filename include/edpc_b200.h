@@ -205,6 +205,10 @@ int edpc_debug_read(edpc_ctx* ctx, int32_t which, float* out, int64_t count);
 int edpc_ksg_counts(const double* z, int32_t dz, const double* y, int32_t dy, int64_t n,
                     int32_t k, int32_t device, int64_t* count_z, int64_t* count_y,
                     int64_t* degenerate);
+/* debug: make the fused weight-gradient/Adam kernels also write the reduced
+ * gradient into partial slot 0 (slots 1..7 zeroed) so edpc_debug_read(0)
+ * keeps returning partials whose canonical tree is the gradient */
+int edpc_debug_keep_grads(edpc_ctx* ctx, int32_t keep);
 /* the shared-parameter Adam kernel on host arrays: `steps` updates of w0 by
  * grads[t][n] (_kernels.py:18-32 adam_update; tests pin it to the reference) */
 int edpc_debug_adam(const float* w0, const float* grads, int64_t n, int32_t steps, double lr,

@@ -96,6 +96,7 @@ _SIGS = {
     "edpc_debug_read": ([_P, _I32, _P, _I64], ctypes.c_int),
     "edpc_ctx_numerics": ([_P, _P], ctypes.c_int),
     "edpc_ksg_counts": ([_P, _I32, _P, _I32, _I64, _I32, _I32, _P, _P, _P], ctypes.c_int),
+    "edpc_debug_keep_grads": ([_P, _I32], ctypes.c_int),
     "edpc_debug_adam": ([_P, _P, _I64, _I32, ctypes.c_double, ctypes.c_double, ctypes.c_double,
                          ctypes.c_double, _P, _P, _P], ctypes.c_int),
     "edpc_debug_gemm": ([_I32, _I32, _I32, _I32, _I32, _P, _P, _P, _I32], ctypes.c_int),

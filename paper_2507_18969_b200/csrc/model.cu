@@ -26,6 +26,7 @@
 #include "lte.cuh"
 #include "tc_gemm.cuh"
 #include "mbrb_fused.cuh"
+#include "wgrad_adam.cuh"
 
 namespace edpc {
 
@@ -227,6 +228,11 @@ struct edpc_ctx {
   // tf32-rounded shadow Wt, activations stored rounded by their producers
   bool rt = false;
   float* Wt = nullptr;
+  // weight gradient + lane-group tree + Adam fused (wgrad_adam.cuh): one
+  // context holding all 8 lane groups on the tensor-core path
+  bool wfuse = false;
+  bool keep_grads = false;  // debug: fused kernels also write the reduced gradient to Gp slot 0
+  int64_t arr = 0;          // W -> M -> V distance (one allocation)
   int gs_log2 = 0;                                  // gradient scale 2^gs_log2 (k_dlogits)
   __half* Wh = nullptr;                             // fp16 shadow of the shared weights
   __half *guph_l = nullptr, *guph_g = nullptr;      // fp16 copies of g_up per MBRB
@@ -527,9 +533,38 @@ static cudaError_t join_aux(edpc_ctx* c) {
   return e;
 }
 
+static WgAdamArgs wgrad_adam_args(edpc_ctx* c, int64_t off, int64_t sOff, int64_t bias_off, int N,
+                                  bool half) {
+  WgAdamArgs a{};
+  a.B_global = c->lay.B;
+  a.lane0 = c->lane0;
+  a.bias_off = bias_off;
+  a.bias_zstride = sOff;
+  a.W = c->W;
+  a.arr = c->arr;
+  a.Wh = half ? c->Wh : nullptr;
+  a.Wt = (!half && c->rt) ? c->Wt : nullptr;
+  a.si = c->si();
+  a.ac = c->adam;
+  a.b1d = c->cfg.beta1;
+  a.b2d = c->cfg.beta2;
+  a.ginv = ldexpf(1.0f, -c->gs_log2);
+  a.keep = c->keep_grads ? c->Gp : nullptr;
+  a.keep_off = off;
+  a.keep_ld = N;
+  a.keep_zs = sOff;
+  return a;
+}
+
 static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, int N, int nzb,
                          int64_t sG, int64_t off, int64_t sOff, int64_t bias_off) {
   if (skip_wgrad_experiment()) return cudaSuccess;
+  if (c->wfuse) {  // gradient + tree + Adam in one kernel (no partials, no Adam launch)
+    Scope sc(c, kRegGemm, wst(c));
+    return as_cuda(wgrad_adam_launch<false>(X, Mw, G, N, nzb, sG,
+                                            wgrad_adam_args(c, off, sOff, bias_off, N, false), off,
+                                            sOff, wst(c)));
+  }
   EpiPartial e{c->Gp, c->lay.n_shared, off, sOff, N, c->g_first};
   cudaStream_t ws = wst(c);
   const int glanes = c->lay.B / kNumGroups;
@@ -665,6 +700,12 @@ static cudaError_t dgrad_h(edpc_ctx* c, const __half* G, int Kd, int nsum, int64
 static cudaError_t wgrad_h(edpc_ctx* c, const __half* X, int Mw, const __half* G, int N, int nzb,
                            int64_t sG, int64_t off, int64_t sOff, int64_t bias_off) {
   if (skip_wgrad_experiment()) return cudaSuccess;
+  if (c->wfuse) {
+    Scope sc(c, kRegGemm, wst(c));
+    return as_cuda(wgrad_adam_launch<true>(X, Mw, G, N, nzb, sG,
+                                           wgrad_adam_args(c, off, sOff, bias_off, N, true), off,
+                                           sOff, wst(c)));
+  }
   EpiPartial e{c->Gp, c->lay.n_shared, off, sOff, N, c->g_first};
   cudaStream_t ws = wst(c);
   Scope sc(c, kRegGemm, ws);
@@ -879,8 +920,6 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
       // out-proj dgrad + product rule + branch dgrad (+ its split reduction)
       // in one kernel (bit-identical to the three-launch path below); then the
       // branch weight gradients from the g_H it stored
-      CK(fork_aux(c));
-      CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0, o.out_b));
       {
         Scope sc(c, kRegGemm, c->st);
         const int st = mbrb_bwd_fused(guph, c->Wh + o.out_w, c->Wh + o.w0, o.wstride, Dh, GHh, Bl,
@@ -888,6 +927,7 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
         if (st != EDPC_OK) return st;
       }
       CK(fork_aux(c));
+      CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0, o.out_b));
       CK(wgrad_h(c, x0h, F, GHh, H, K, plane, o.w0, o.wstride, o.b0));
     } else {
     // g_ff = g_up . out_w^T (out_w [H][F] = K-major B), epilogue -> g_H[z]
@@ -898,22 +938,23 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
       const int st = tc_gemm<false, false, true>(s, a, bw, EpiBwdActH{Dh, GHh, K, plane, H}, c->st);
       if (st != EDPC_OK) return st;
     }
-    // weight gradients (and bias sums from fp32 g_up / fp16 g_H) on the side stream
+    // g_x0 = sum_z g_H[z] . W_z^T (W_z [F][H] = K-major B)
+    CK(dgrad_h(c, GHh, H, K, plane, c->Wh + o.w0, o.wstride, F, c->gx0));
+    // weight gradients (and bias sums from fp32 g_up / fp16 g_H) on the side
+    // stream, after the last reads of these weights
     CK(fork_aux(c));
     CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0, o.out_b));
     CK(wgrad_h(c, x0h, F, GHh, H, K, plane, o.w0, o.wstride, o.b0));
-    // g_x0 = sum_z g_H[z] . W_z^T (W_z [F][H] = K-major B)
-    CK(dgrad_h(c, GHh, H, K, plane, c->Wh + o.w0, o.wstride, F, c->gx0));
     }
   } else {
   // g_ff = g_up . out_w^T, epilogue -> GH[z] (product rule + GeLU')
   CK(dgrad(c, g_up, F, 1, 0, wt(c) + o.out_w, 0, H, EpiBwdAct{b.H, GH, K, plane, H}));
-  // weight gradients on the side stream: out_w/out_b, branch weights/biases
+  // g_x0 = sum_z GH[z] . W_z^T
+  CK(dgrad(c, GH, H, K, plane, wt(c) + o.w0, o.wstride, F, EpiStore{c->gx0, F}));
+  // weight gradients on the side stream (after the last reads of these weights)
   CK(fork_aux(c));
   CK(wgrad(c, b.ff, H, g_up, F, 1, 0, o.out_w, 0, o.out_b));
   CK(wgrad(c, b.x0, F, GH, H, K, plane, o.w0, o.wstride, o.b0));
-  // g_x0 = sum_z GH[z] . W_z^T
-  CK(dgrad(c, GH, H, K, plane, wt(c) + o.w0, o.wstride, F, EpiStore{c->gx0, F}));
   }
   // LN backward + residual, with the LN gain / bias gradient partials
   if (F <= kLnMaxF && c->g_count > 0) {
@@ -950,25 +991,29 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
         c->probs, src, c->si(), Bl, (float)L.B, ldexpf(1.0f, c->gs_log2), c->gl, nll);
   }
   CK(cudaGetLastError());
-  // head
-  CK(fork_aux(c));
-  CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0, L.head_b));
+  // head: the dgrad reads the weights before the side stream may update them
+  // (a fused weight-gradient/Adam kernel writes W in place)
   if (c->h16)
     CK(dgrad(c, c->gl, 256, 1, 0, wt(c) + L.head_w, 0, F, EpiStore2{c->g_head, c->guph_g, F}));
   else
     CK(dgrad(c, c->gl, 256, 1, 0, wt(c) + L.head_w, 0, F, EpiStore{c->g_head, F}));
+  CK(fork_aux(c));
+  CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0, L.head_b));
   // global MBRB: d(x_global) -> d(x_lte)
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
   EDPC_TRY(mbrb_backward(c, L.glo, gb, c->g_head, c->g_lte, c->GH_g, c->guph_g));
-  if (early_adam(c)) {  // global MBRB (its LN backward included) + head: gradients complete
+  if (c->wfuse) {  // global LN gain/bias (partials from k_ln_bwd_fused): complete
+    CK(fork_aux(c));
+    EDPC_TRY(adam_range(c, L.glo.ln_g, 2 * (int64_t)F, wst(c)));
+  } else if (early_adam(c)) {  // global MBRB (its LN backward included) + head: complete
     CK(fork_aux(c));
     EDPC_TRY(adam_range(c, L.glo.ln_g, L.n_shared - L.glo.ln_g, c->st_aux));
   }
   // LTE up
-  CK(fork_aux(c));
-  CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
   {
     CK(dgrad(c, c->g_lte, F, 1, 0, wt(c) + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
+    CK(fork_aux(c));
+    CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
     // per-lane FDM: g_down with the old U, then U's Adam step (fused: U read once)
     {
       if (FP == 64 || FP == 128 || FP == 256) {
@@ -998,21 +1043,21 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
     }
     CK(cudaGetLastError());
     // LTE down
-    CK(fork_aux(c));
-    CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
     if (c->h16)
       CK(dgrad(c, c->gdown, FP, 1, 0, wt(c) + L.down_w, 0, F, EpiStore2{c->g_loc, c->guph_l, F}));
     else
       CK(dgrad(c, c->gdown, FP, 1, 0, wt(c) + L.down_w, 0, F, EpiStore{c->g_loc, F}));
+    CK(fork_aux(c));
+    CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
   }
-  if (early_adam(c)) {  // LTE down + up
+  if (!c->wfuse && early_adam(c)) {  // LTE down + up
     CK(fork_aux(c));
     EDPC_TRY(adam_range(c, L.down_w, L.glo.ln_g - L.down_w, c->st_aux));
   }
   // local MBRB: d(x_local) -> d(x_emb) (gradient w.r.t. the embedded context)
   MbrbBufs lb{c->x_emb, c->l_xhat, c->l_rstd, c->l_x0, c->l_H, c->l_ff, c->x_local};
   EDPC_TRY(mbrb_backward(c, L.loc, lb, c->g_loc, c->g_emb, c->GH_l, c->guph_l));
-  if (early_adam(c)) {  // local MBRB: gradients complete; overlaps the embedding scatter-add
+  if (!c->wfuse && early_adam(c)) {  // local MBRB: complete; overlaps the embedding scatter-add
     CK(fork_aux(c));
     EDPC_TRY(adam_range(c, L.loc.ln_g, L.down_w - L.loc.ln_g, c->st_aux));
   }
@@ -1142,6 +1187,9 @@ static int adam_shared(edpc_ctx* c) {
     shard_range(c, shard_rank(c), &off, &len);
     return adam_range(c, off, len, c->st, G, (int64_t)c->g_count * L.n_shared);
   }
+  // fused weight gradients: only the embedding and the local LN (contiguous)
+  // are left; the global LN went on the side stream after its backward
+  if (c->wfuse) return adam_range(c, 0, L.loc.ln_g + 2 * (int64_t)L.F, c->st);
   if (early_adam(c)) return adam_range(c, 0, L.loc.ln_g, c->st);  // the embedding
   return adam_range(c, 0, L.n_shared, c->st);
 }
@@ -1402,6 +1450,22 @@ int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t origina
     c->gs_log2 = k;
   }
 
+  // fused weight-gradient + Adam kernels: the tensor-core path with all 8
+  // lane groups in this context, 64-lane-multiple groups, every weight
+  // gradient N a multiple of the 64-column tile and 16-byte aligned weights
+  // (numerics-neutral: bit-identical to the partials + k_adam_shared path;
+  // EDPC_WGRAD_FUSED=0 selects that path for A/B runs)
+  {
+    const Layout& L = c->lay;
+    const char* e = getenv("EDPC_WGRAD_FUSED");
+    bool ok = !(e && e[0] == '0') && c->use_tc && c->g_count == kNumGroups && L.B % kNumGroups == 0 &&
+              (L.B / kNumGroups) % 64 == 0;
+    for (int n : {L.F, L.FP, L.HL, L.HG, 256}) ok = ok && n % 64 == 0;
+    for (int64_t o : {L.loc.w0, L.loc.wstride, L.loc.out_w, L.glo.w0, L.glo.wstride, L.glo.out_w,
+                      L.down_w, L.up_w, L.head_w})
+      ok = ok && o % 8 == 0;
+    c->wfuse = ok;
+  }
   auto fail = [&](int code) {
     delete c;
     return code;
@@ -1425,9 +1489,13 @@ int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t origina
     int _r = c->alloc(&(p), (n));       \
     if (_r != EDPC_OK) return fail(_r); \
   } while (0)
-  A_(c->W, L.n_shared + kShardPad);  // padded: in-place all-gather of equal slices
-  A_(c->M, L.n_shared);
-  A_(c->V, L.n_shared);
+  // W, M, V in one allocation at a fixed element distance (one TMA map reaches
+  // all three from the fused weight-gradient/Adam kernel); W padded for the
+  // in-place all-gather of equal slices
+  c->arr = (L.n_shared + kShardPad + 63) / 64 * 64;
+  A_(c->W, 3 * c->arr);
+  c->M = c->W + c->arr;
+  c->V = c->M + c->arr;
   A_(c->Gp, (int64_t)kNumGroups * L.n_shared);
   A_(c->U, (int64_t)Bl * L.fdm);
   A_(c->Um, (int64_t)Bl * L.fdm);
@@ -2035,6 +2103,7 @@ int edpc_ctx_set_comm(edpc_ctx* c, const uint8_t* id, int32_t nranks, int32_t ra
   c->comm = comm;
   c->nranks = nranks;
   c->rank = rank;
+  c->wfuse = false;  // the slice exchange needs the group partials
   for (auto& g : c->graph)  // captured steps must include the collective
     if (g) {
       cudaGraphExecDestroy(g);
@@ -2320,6 +2389,24 @@ int edpc_debug_adam(const float* w0, const float* grads, int64_t n, int32_t step
   cudaFree(P);
   cudaFree(d_t);
   EDPC_CUDA_TRY(e);
+  return EDPC_OK;
+}
+
+// Debug: with fused weight-gradient/Adam kernels the 8 lane-group partials
+// are never materialised; keep = 1 makes those kernels also write the reduced
+// gradient (gradient-scale units) into partial slot 0, slots 1..7 zero, so
+// edpc_debug_read(0) keeps its meaning (tree of the 8 slots = the gradient).
+int edpc_debug_keep_grads(edpc_ctx* c, int32_t keep) {
+  EDPC_CHECK_ARG(c, "null ctx");
+  EDPC_CUDA_TRY(cudaSetDevice(c->device));
+  EDPC_CUDA_TRY(cudaStreamSynchronize(c->st));
+  c->keep_grads = keep != 0;
+  EDPC_CUDA_TRY(cudaMemset(c->Gp, 0, (size_t)kNumGroups * c->lay.n_shared * 4));
+  for (auto& g : c->graph)  // captured launches carry the pointer
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
   return EDPC_OK;
 }
 

@@ -30,6 +30,8 @@ def _flags(cfg, tc: bool, f16: bool) -> int:
 def _ctx(cfg, tc: bool, f16: bool = False):
     c = DeviceContext(cfg, 4, 0, 0, numerics=_flags(cfg, tc, f16))
     c.load_flat(init_params_f32(cfg))
+    # fused weight-gradient/Adam kernels: keep the reduced gradient readable
+    _lib.check(_lib.load().edpc_debug_keep_grads(c.h, 1))
     return c
 
 
@@ -155,10 +157,12 @@ def test_tc_gemm_f16_unit(M, N, K, a_mn, b_mn):
     assert err < 1e-5, (err, C[:2, :4], ref[:2, :4])
 
 
-def test_fused_mbrb_forward_is_bit_identical():
-    """The fused MBRB forward (branch GEMMs + GeLU + out-projection in one
-    kernel, mbrb_fused.cuh) gives exactly the two-GEMM path's container
-    (EDPC_MBRB_FUSED=0, run in a subprocess: the switch is read once)."""
+@pytest.mark.parametrize("switch", ["EDPC_MBRB_FUSED", "EDPC_WGRAD_FUSED"])
+def test_fused_kernels_are_bit_identical(switch):
+    """The fused MBRB forward / backward kernels (mbrb_fused.cuh) and the fused
+    weight-gradient + lane-group tree + Adam kernels (wgrad_adam.cuh) give
+    exactly the unfused paths' container (switch=0, run in a subprocess: the
+    switches are read once per process)."""
     import os
     import subprocess
     import sys
@@ -173,7 +177,8 @@ def test_fused_mbrb_forward_is_bit_identical():
             "                  hidden_global=4096, lte_ratio=4, branches=2, lanes=1024)\n"
             "sys.stdout.buffer.write(write_container(compress(synth.text_like(1024 * 40, 1), cfg, 64)))\n"
             % root)
-    env = dict(os.environ, EDPC_MBRB_FUSED="0", PYTHONPATH=root)
+    env = dict(os.environ, PYTHONPATH=root)
+    env[switch] = "0"
     ref = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
                          timeout=600).stdout
     assert blob == ref
