@@ -72,6 +72,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");                 // producer/MMA warps took ~10% of the issue slots)
 }
 
+// Polling wait (try_wait without a suspend-time hint: the thread re-polls
+// instead of sleeping).  For waits on a tcgen05.commit arrival in latency-
+// critical loops: a thread suspended with the hint was seen to resume late
+// after such arrivals (the fused kernels' epilogues stalled on them).
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAITS_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@p bra DONES_%=;\n\t"
+      "bra WAITS_%=;\n\t"
+      "DONES_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1, int c2) {
   asm volatile(

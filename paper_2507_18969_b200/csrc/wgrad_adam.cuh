@@ -151,7 +151,7 @@ k_wgrad_adam(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ 
         for (int g = 0; g < 8; ++g) {
           int k0, nkb;
           krange(g, k0, nkb);
-          mbar_wait(&gempty[g], ((uint32_t)lu & 1u) ^ 1u);
+          mbar_wait_spin(&gempty[g], ((uint32_t)lu & 1u) ^ 1u);
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(g * kBN);
           for (int q = 0; q < nkb; ++q, ++it) {
@@ -200,7 +200,7 @@ k_wgrad_adam(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ 
       float acc[kCW], s1[kCW], s2[kCW];  // canonical tree, built as the slots complete
 #pragma unroll
       for (int g = 0; g < 8; ++g) {  // unrolled: each step's live set is static
-        mbar_wait(&gfull[g], (uint32_t)lu & 1u);
+        mbar_wait_spin(&gfull[g], (uint32_t)lu & 1u);
         tc_fence_after();
         float v[kCW];
         tmem_ld16(tq + (uint32_t)(g * kBN + c0), v);
