@@ -1450,15 +1450,18 @@ int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t origina
     c->gs_log2 = k;
   }
 
-  // fused weight-gradient + Adam kernels: the tensor-core path with all 8
-  // lane groups in this context, 64-lane-multiple groups, every weight
-  // gradient N a multiple of the 64-column tile and 16-byte aligned weights
-  // (numerics-neutral: bit-identical to the partials + k_adam_shared path;
-  // EDPC_WGRAD_FUSED=0 selects that path for A/B runs)
+  // fused weight-gradient + Adam kernels (wgrad_adam.cuh): the tensor-core
+  // path with all 8 lane groups in this context, 64-lane-multiple groups,
+  // every weight gradient N a multiple of the 64-column tile and 16-byte
+  // aligned weights.  Numerics-neutral (bit-identical to the partials +
+  // k_adam_shared path) but OFF by default: one CTA walking all 8 groups of
+  // a tile is latency-bound in its operand pipeline (ncu: ~60 us per tile,
+  // C2 6.0 vs 8.8 MB/s) -- 8x fewer CTAs than the partial GEMMs, each 8x
+  // longer.  EDPC_WGRAD_FUSED=1 selects it (experiments / A-B tests).
   {
     const Layout& L = c->lay;
     const char* e = getenv("EDPC_WGRAD_FUSED");
-    bool ok = !(e && e[0] == '0') && c->use_tc && c->g_count == kNumGroups && L.B % kNumGroups == 0 &&
+    bool ok = (e && e[0] == '1') && c->use_tc && c->g_count == kNumGroups && L.B % kNumGroups == 0 &&
               (L.B / kNumGroups) % 64 == 0;
     for (int n : {L.F, L.FP, L.HL, L.HG, 256}) ok = ok && n % 64 == 0;
     for (int64_t o : {L.loc.w0, L.loc.wstride, L.loc.out_w, L.glo.w0, L.glo.wstride, L.glo.out_w,
