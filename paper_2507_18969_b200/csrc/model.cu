@@ -920,6 +920,10 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
       // out-proj dgrad + product rule + branch dgrad (+ its split reduction)
       // in one kernel (bit-identical to the three-launch path below); then the
       // branch weight gradients from the g_H it stored
+      if (!c->wfuse) {  // needs only g_up and ff: overlaps the fused kernel
+        CK(fork_aux(c));
+        CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0, o.out_b));
+      }
       {
         Scope sc(c, kRegGemm, c->st);
         const int st = mbrb_bwd_fused(guph, c->Wh + o.out_w, c->Wh + o.w0, o.wstride, Dh, GHh, Bl,
@@ -927,7 +931,7 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
         if (st != EDPC_OK) return st;
       }
       CK(fork_aux(c));
-      CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0, o.out_b));
+      if (c->wfuse) CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0, o.out_b));
       CK(wgrad_h(c, x0h, F, GHh, H, K, plane, o.w0, o.wstride, o.b0));
     } else {
     // g_ff = g_up . out_w^T (out_w [H][F] = K-major B), epilogue -> g_H[z]
@@ -991,14 +995,21 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
         c->probs, src, c->si(), Bl, (float)L.B, ldexpf(1.0f, c->gs_log2), c->gl, nll);
   }
   CK(cudaGetLastError());
-  // head: the dgrad reads the weights before the side stream may update them
-  // (a fused weight-gradient/Adam kernel writes W in place)
+  // head.  The weight gradients go to the side stream as early as possible
+  // (before the dgrad that reads the same weights) -- except with the fused
+  // weight-gradient/Adam kernels, which update W in place: then after it.
+  if (!c->wfuse) {
+    CK(fork_aux(c));
+    CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0, L.head_b));
+  }
   if (c->h16)
     CK(dgrad(c, c->gl, 256, 1, 0, wt(c) + L.head_w, 0, F, EpiStore2{c->g_head, c->guph_g, F}));
   else
     CK(dgrad(c, c->gl, 256, 1, 0, wt(c) + L.head_w, 0, F, EpiStore{c->g_head, F}));
-  CK(fork_aux(c));
-  CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0, L.head_b));
+  if (c->wfuse) {
+    CK(fork_aux(c));
+    CK(wgrad(c, c->x_global, F, c->gl, 256, 1, 0, L.head_w, 0, L.head_b));
+  }
   // global MBRB: d(x_global) -> d(x_lte)
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
   EDPC_TRY(mbrb_backward(c, L.glo, gb, c->g_head, c->g_lte, c->GH_g, c->guph_g));
@@ -1011,9 +1022,15 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
   }
   // LTE up
   {
+    if (!c->wfuse) {
+      CK(fork_aux(c));
+      CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
+    }
     CK(dgrad(c, c->g_lte, F, 1, 0, wt(c) + L.up_w, 0, FP, EpiStore{c->gmix, FP}));
-    CK(fork_aux(c));
-    CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
+    if (c->wfuse) {
+      CK(fork_aux(c));
+      CK(wgrad(c, c->mixed, FP, c->g_lte, F, 1, 0, L.up_w, 0, L.up_b));
+    }
     // per-lane FDM: g_down with the old U, then U's Adam step (fused: U read once)
     {
       if (FP == 64 || FP == 128 || FP == 256) {
@@ -1043,12 +1060,18 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
     }
     CK(cudaGetLastError());
     // LTE down
+    if (!c->wfuse) {
+      CK(fork_aux(c));
+      CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
+    }
     if (c->h16)
       CK(dgrad(c, c->gdown, FP, 1, 0, wt(c) + L.down_w, 0, F, EpiStore2{c->g_loc, c->guph_l, F}));
     else
       CK(dgrad(c, c->gdown, FP, 1, 0, wt(c) + L.down_w, 0, F, EpiStore{c->g_loc, F}));
-    CK(fork_aux(c));
-    CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
+    if (c->wfuse) {
+      CK(fork_aux(c));
+      CK(wgrad(c, c->x_local, F, c->gdown, FP, 1, 0, L.down_w, 0, L.down_b));
+    }
   }
   if (!c->wfuse && early_adam(c)) {  // LTE down + up
     CK(fork_aux(c));
