@@ -231,6 +231,9 @@ struct edpc_ctx {
   // weight gradient + lane-group tree + Adam fused (wgrad_adam.cuh): one
   // context holding all 8 lane groups on the tensor-core path
   bool wfuse = false;
+  // weight gradients as two subtree partials (groups 0-3 -> slot 0, 4-7 ->
+  // slot 4) instead of 8 per-group partials; Adam's top tree level over them
+  bool wsub = false;
   bool keep_grads = false;  // debug: fused kernels also write the reduced gradient to Gp slot 0
   int64_t arr = 0;          // W -> M -> V distance (one allocation)
   int gs_log2 = 0;                                  // gradient scale 2^gs_log2 (k_dlogits)
@@ -556,9 +559,23 @@ static WgAdamArgs wgrad_adam_args(edpc_ctx* c, int64_t off, int64_t sOff, int64_
   return a;
 }
 
+template <bool H>
+static cudaError_t wgrad_sub(edpc_ctx* c, const void* X, int Mw, const void* G, int N, int nzb,
+                             int64_t sG, int64_t off, int64_t sOff, int64_t bias_off) {
+  Scope sc(c, kRegGemm, wst(c));
+  const int B = c->lay.B;
+  const int64_t P = c->lay.n_shared;
+  if (N % 128 == 0)
+    return as_cuda(wgrad_subtree_launch<H, 128>(X, Mw, G, N, nzb, sG, B, c->lane0, c->Gp, P, off,
+                                                sOff, bias_off, wst(c)));
+  return as_cuda(wgrad_subtree_launch<H, 64>(X, Mw, G, N, nzb, sG, B, c->lane0, c->Gp, P, off, sOff,
+                                             bias_off, wst(c)));
+}
+
 static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, int N, int nzb,
                          int64_t sG, int64_t off, int64_t sOff, int64_t bias_off) {
   if (skip_wgrad_experiment()) return cudaSuccess;
+  if (c->wsub) return wgrad_sub<false>(c, X, Mw, G, N, nzb, sG, off, sOff, bias_off);
   if (c->wfuse) {  // gradient + tree + Adam in one kernel (no partials, no Adam launch)
     Scope sc(c, kRegGemm, wst(c));
     return as_cuda(wgrad_adam_launch<false>(X, Mw, G, N, nzb, sG,
@@ -700,6 +717,7 @@ static cudaError_t dgrad_h(edpc_ctx* c, const __half* G, int Kd, int nsum, int64
 static cudaError_t wgrad_h(edpc_ctx* c, const __half* X, int Mw, const __half* G, int N, int nzb,
                            int64_t sG, int64_t off, int64_t sOff, int64_t bias_off) {
   if (skip_wgrad_experiment()) return cudaSuccess;
+  if (c->wsub) return wgrad_sub<true>(c, X, Mw, G, N, nzb, sG, off, sOff, bias_off);
   if (c->wfuse) {
     Scope sc(c, kRegGemm, wst(c));
     return as_cuda(wgrad_adam_launch<true>(X, Mw, G, N, nzb, sG,
@@ -942,23 +960,39 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
       const int st = tc_gemm<false, false, true>(s, a, bw, EpiBwdActH{Dh, GHh, K, plane, H}, c->st);
       if (st != EDPC_OK) return st;
     }
+    // weight gradients (and bias sums from fp32 g_up / fp16 g_H) on the side
+    // stream -- after the branch dgrad's reads of W_z when they update W in
+    // place (fused weight-gradient/Adam mode)
+    if (!c->wfuse) {
+      CK(fork_aux(c));
+      CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0, o.out_b));
+      CK(wgrad_h(c, x0h, F, GHh, H, K, plane, o.w0, o.wstride, o.b0));
+    }
     // g_x0 = sum_z g_H[z] . W_z^T (W_z [F][H] = K-major B)
     CK(dgrad_h(c, GHh, H, K, plane, c->Wh + o.w0, o.wstride, F, c->gx0));
-    // weight gradients (and bias sums from fp32 g_up / fp16 g_H) on the side
-    // stream, after the last reads of these weights
-    CK(fork_aux(c));
-    CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0, o.out_b));
-    CK(wgrad_h(c, x0h, F, GHh, H, K, plane, o.w0, o.wstride, o.b0));
+    if (c->wfuse) {
+      CK(fork_aux(c));
+      CK(wgrad_h(c, ffh, H, guph, F, 1, 0, o.out_w, 0, o.out_b));
+      CK(wgrad_h(c, x0h, F, GHh, H, K, plane, o.w0, o.wstride, o.b0));
+    }
     }
   } else {
   // g_ff = g_up . out_w^T, epilogue -> GH[z] (product rule + GeLU')
   CK(dgrad(c, g_up, F, 1, 0, wt(c) + o.out_w, 0, H, EpiBwdAct{b.H, GH, K, plane, H}));
+  // weight gradients on the side stream (after the branch dgrad in the fused
+  // weight-gradient/Adam mode, which updates W in place)
+  if (!c->wfuse) {
+    CK(fork_aux(c));
+    CK(wgrad(c, b.ff, H, g_up, F, 1, 0, o.out_w, 0, o.out_b));
+    CK(wgrad(c, b.x0, F, GH, H, K, plane, o.w0, o.wstride, o.b0));
+  }
   // g_x0 = sum_z GH[z] . W_z^T
   CK(dgrad(c, GH, H, K, plane, wt(c) + o.w0, o.wstride, F, EpiStore{c->gx0, F}));
-  // weight gradients on the side stream (after the last reads of these weights)
-  CK(fork_aux(c));
-  CK(wgrad(c, b.ff, H, g_up, F, 1, 0, o.out_w, 0, o.out_b));
-  CK(wgrad(c, b.x0, F, GH, H, K, plane, o.w0, o.wstride, o.b0));
+  if (c->wfuse) {
+    CK(fork_aux(c));
+    CK(wgrad(c, b.ff, H, g_up, F, 1, 0, o.out_w, 0, o.out_b));
+    CK(wgrad(c, b.x0, F, GH, H, K, plane, o.w0, o.wstride, o.b0));
+  }
   }
   // LN backward + residual, with the LN gain / bias gradient partials
   if (F <= kLnMaxF && c->g_count > 0) {
@@ -985,6 +1019,7 @@ static int mbrb_backward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, cons
 static int adam_range(edpc_ctx* c, int64_t off, int64_t len, cudaStream_t st, int nl = kNumGroups,
                       int64_t pstride = -1);
 static bool early_adam(const edpc_ctx* c);
+static int adam_span(edpc_ctx* c, int64_t lo, int64_t hi, cudaStream_t st);
 
 static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = false) {
   const Layout& L = c->lay;
@@ -1018,7 +1053,7 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
     EDPC_TRY(adam_range(c, L.glo.ln_g, 2 * (int64_t)F, wst(c)));
   } else if (early_adam(c)) {  // global MBRB (its LN backward included) + head: complete
     CK(fork_aux(c));
-    EDPC_TRY(adam_range(c, L.glo.ln_g, L.n_shared - L.glo.ln_g, c->st_aux));
+    EDPC_TRY(adam_span(c, L.glo.ln_g, L.n_shared, c->st_aux));
   }
   // LTE up
   {
@@ -1075,14 +1110,14 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
   }
   if (!c->wfuse && early_adam(c)) {  // LTE down + up
     CK(fork_aux(c));
-    EDPC_TRY(adam_range(c, L.down_w, L.glo.ln_g - L.down_w, c->st_aux));
+    EDPC_TRY(adam_span(c, L.down_w, L.glo.ln_g, c->st_aux));
   }
   // local MBRB: d(x_local) -> d(x_emb) (gradient w.r.t. the embedded context)
   MbrbBufs lb{c->x_emb, c->l_xhat, c->l_rstd, c->l_x0, c->l_H, c->l_ff, c->x_local};
   EDPC_TRY(mbrb_backward(c, L.loc, lb, c->g_loc, c->g_emb, c->GH_l, c->guph_l));
   if (!c->wfuse && early_adam(c)) {  // local MBRB: complete; overlaps the embedding scatter-add
     CK(fork_aux(c));
-    EDPC_TRY(adam_range(c, L.loc.ln_g, L.down_w - L.loc.ln_g, c->st_aux));
+    EDPC_TRY(adam_span(c, L.loc.ln_g, L.down_w, c->st_aux));
   }
   // embedding scatter-add as per-group partials
   if (c->n_chunks > 0) {
@@ -1202,6 +1237,29 @@ static int group_tree(edpc_ctx* c) {
   return EDPC_OK;
 }
 
+// Adam over [lo, hi) of the shared parameters with the right leaf count per
+// sub-range: the LN gains/biases and the embedding always have 8 lane-group
+// partials; the weight-gradient ranges have 2 subtree partials (slots 0, 4)
+// in subtree mode, else 8.
+static int adam_span(edpc_ctx* c, int64_t lo, int64_t hi, cudaStream_t st) {
+  const Layout& L = c->lay;
+  const int w = c->wsub ? 2 : kNumGroups;
+  const struct {
+    int64_t a, b;
+    int nl;
+  } seg[] = {{0, L.loc.w0, kNumGroups},       // embedding + local LN
+             {L.loc.w0, L.glo.ln_g, w},       // local MBRB weights, LTE
+             {L.glo.ln_g, L.glo.w0, kNumGroups},  // global LN
+             {L.glo.w0, L.n_shared, w}};      // global MBRB weights, head
+  for (const auto& s : seg) {
+    const int64_t a = std::max(lo, s.a), b = std::min(hi, s.b);
+    if (a < b)
+      EDPC_TRY(adam_range(c, a, b - a, st, s.nl,
+                          s.nl == 2 ? (int64_t)4 * L.n_shared : (int64_t)L.n_shared));
+  }
+  return EDPC_OK;
+}
+
 static int adam_shared(edpc_ctx* c) {
   const Layout& L = c->lay;
   const int G = shard_count(c);
@@ -1213,8 +1271,8 @@ static int adam_shared(edpc_ctx* c) {
   // fused weight gradients: only the embedding and the local LN (contiguous)
   // are left; the global LN went on the side stream after its backward
   if (c->wfuse) return adam_range(c, 0, L.loc.ln_g + 2 * (int64_t)L.F, c->st);
-  if (early_adam(c)) return adam_range(c, 0, L.loc.ln_g, c->st);  // the embedding
-  return adam_range(c, 0, L.n_shared, c->st);
+  if (early_adam(c)) return adam_span(c, 0, L.loc.ln_g, c->st);  // the embedding
+  return adam_span(c, 0, L.n_shared, c->st);
 }
 
 static int nccl_fail(const char* what, ncclResult_t r) {
@@ -1491,6 +1549,13 @@ int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t origina
                       L.down_w, L.up_w, L.head_w})
       ok = ok && o % 8 == 0;
     c->wfuse = ok;
+    // subtree weight gradients: the same geometry conditions (on by default;
+    // EDPC_WGRAD_SUBTREE=0 selects the per-group partial GEMMs for A/B runs)
+    const char* e2 = getenv("EDPC_WGRAD_SUBTREE");
+    bool sok = !(e2 && e2[0] == '0') && c->use_tc && c->g_count == kNumGroups &&
+               L.B % kNumGroups == 0 && (L.B / kNumGroups) % 64 == 0;
+    for (int n : {L.F, L.FP, L.HL, L.HG, 256}) sok = sok && n % 64 == 0;
+    c->wsub = sok && !c->wfuse;
   }
   auto fail = [&](int code) {
     delete c;
@@ -2130,6 +2195,7 @@ int edpc_ctx_set_comm(edpc_ctx* c, const uint8_t* id, int32_t nranks, int32_t ra
   c->nranks = nranks;
   c->rank = rank;
   c->wfuse = false;  // the slice exchange needs the group partials
+  c->wsub = false;
   for (auto& g : c->graph)  // captured steps must include the collective
     if (g) {
       cudaGraphExecDestroy(g);

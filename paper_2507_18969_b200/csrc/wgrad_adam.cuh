@@ -425,3 +425,335 @@ inline int wgrad_adam_launch(const void* X, int Mw, const void* G, int N, int nz
 }
 
 }  // namespace edpc
+
+namespace edpc {
+
+// ===================================================================
+// Subtree weight gradient: a CTA owns one output tile for HALF of the lane
+// groups -- 4 groups, one TMEM slot of BN columns each (4 x BN <= 512) --
+// and writes their subtree sum (g0+g1)+(g2+g3) (or the same over g4..g7)
+// as ONE partial plane, into partial slot 0 or 4.  The shared Adam then runs
+// the top level of the canonical tree over those two slots (NL = 2, stride
+// 4 planes): ((g0+g1)+(g2+g3)) + ((g4+g5)+(g6+g7)), bit for bit the 8-leaf
+// tree.  Against the per-group partial GEMM: 4x fewer partial planes written
+// and read (39 MB instead of 155 MB at paper dims), one wave of CTAs for the
+// big weights, each walking 4 groups through a deeper operand ring.
+namespace ws {
+constexpr int kGpc = 4;         // lane groups per CTA
+constexpr int kEW = 16;         // epilogue warps (4 per TMEM lane quadrant)
+constexpr int kBiasWarps = 2;
+constexpr int kThreads = 32 * (2 + kEW + kBiasWarps);
+template <int BN>
+struct Geo {
+  static constexpr int kCW = BN / (kEW / 4);              // columns per epilogue warp
+  static constexpr int kStage = (kTcBM + BN) * 128;       // A + B of one k-block
+  static constexpr int kEpi = kEW * 4096;                 // one 32x32 fp32 box per warp
+  static constexpr int kStages = (232448 - 2048 - kEpi) / kStage > 6 ? 6 : (232448 - 2048 - kEpi) / kStage;
+  static constexpr int kOffEpi = kStages * kStage;
+  static constexpr int kOffBar = kOffEpi + kEpi;
+  static constexpr int kSmemBytes = 1024 + kOffBar + 512;
+};
+}  // namespace ws
+
+template <bool H, int BN>
+__global__ void __launch_bounds__(ws::kThreads, 1)
+k_wgrad_subtree(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                const __grid_constant__ CUtensorMap tma_p, int Mw, int N, int nzb, int B_global,
+                int lane0, float* __restrict__ part, int64_t n_shared, int64_t bias_off,
+                int64_t bias_zstride, int with_bias) {
+  using namespace ws;
+  using G = Geo<BN>;
+  constexpr int BK = tc_bk<H>();
+  constexpr int kW = H ? 64 : 32;
+  constexpr int kCW = G::kCW;
+  static_assert(kCW == 32 || kCW == 16, "epilogue chunk");
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  constexpr int kStages = G::kStages;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + G::kOffBar);
+  uint64_t* empty = full + kStages;
+  uint64_t* gfull = empty + kStages;  // [kGpc]
+  uint64_t* gempty = gfull + kGpc;    // [kGpc]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gempty + kGpc);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_tn = N / BN, n_tm = (Mw + kTcBM - 1) / kTcBM;
+  const int n_units = n_tn * n_tm * nzb * 2;
+  auto coords = [&](int u, int& tn, int& tm, int& zb, int& sub) {
+    sub = u & 1;
+    const int v = u >> 1;
+    tn = v % n_tn;
+    tm = (v / n_tn) % n_tm;
+    zb = v / (n_tn * n_tm);
+  };
+  auto krange = [&](int g, int& k0, int& nkb) {
+    k0 = group_begin(g, B_global) - lane0;
+    nkb = (group_begin(g + 1, B_global) - lane0 - k0) / BK;
+  };
+
+  if (warp == 0 && lane == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_b) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tma_p) : "memory");
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], with_bias ? 2 : 1);
+    }
+    for (int g = 0; g < kGpc; ++g) {
+      mbar_init(&gfull[g], 1);
+      mbar_init(&gempty[g], kEW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_entry();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int tn, tm, zb, sub;
+        coords(u, tn, tm, zb, sub);
+        const int n0 = tn * BN, m0 = tm * kTcBM;
+        for (int gl = 0; gl < kGpc; ++gl) {
+          int k0, nkb;
+          krange(sub * kGpc + gl, k0, nkb);
+          for (int q = 0; q < nkb; ++q, ++it) {
+            const int st = it % kStages;
+            mbar_wait(&empty[st], ((uint32_t)(it / kStages) & 1u) ^ 1u);
+            uint8_t* sa = smem + st * G::kStage;
+            uint8_t* sb = sa + kTcBM * 128;
+            mbar_expect_tx(&full[st], G::kStage);
+            const int k = k0 + q * BK;
+#pragma unroll
+            for (int j = 0; j < kTcBM / kW; ++j) tma_load_3d(sa + j * kW * 128, &tma_a, &full[st], m0 + kW * j, k, 0);
+#pragma unroll
+            for (int j = 0; j < BN / kW; ++j) tma_load_3d(sb + j * kW * 128, &tma_b, &full[st], n0 + kW * j, k, zb);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = H ? idesc_f16(kTcBM, BN, 1, 1) : idesc_tf32(kTcBM, BN, 1, 1);
+      int it = 0, lu = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++lu) {
+        int tn, tm, zb, sub;
+        coords(u, tn, tm, zb, sub);
+        for (int gl = 0; gl < kGpc; ++gl) {
+          int k0, nkb;
+          krange(sub * kGpc + gl, k0, nkb);
+          mbar_wait_spin(&gempty[gl], ((uint32_t)lu & 1u) ^ 1u);
+          tc_fence_after();
+          const uint32_t d = tmem + (uint32_t)(gl * BN);
+          for (int q = 0; q < nkb; ++q, ++it) {
+            const int st = it % kStages;
+            mbar_wait(&full[st], (uint32_t)(it / kStages) & 1u);
+            tc_fence_after();
+            const uint32_t sa = smem_u32(smem + st * G::kStage), sb = sa + kTcBM * 128;
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              if constexpr (H) {
+                tc_mma_f16(d, sdesc(sa + kk * 2048, kMnH_LBO, kMnH_SBO, kLayoutSW128),
+                           sdesc(sb + kk * 2048, kMnH_LBO, kMnH_SBO, kLayoutSW128), idesc,
+                           (q > 0 || kk > 0) ? 1u : 0u);
+              } else {
+                tc_mma_tf32(d, sdesc(sa + kk * 1024, 4096, 512, kLayoutSW128Base32B),
+                            sdesc(sb + kk * 1024, 4096, 512, kLayoutSW128Base32B), idesc,
+                            (q > 0 || kk > 0) ? 1u : 0u);
+              }
+            }
+            tc_commit(&empty[st]);
+          }
+          tc_commit(&gfull[gl]);
+        }
+      }
+    }
+  } else if (warp < 2 + kEW) {
+    // ---------------- epilogue: (q0+q1)+(q2+q3) over the 4 slots -> one partial plane
+    const int ew = warp - 2, quad = warp & 3, cw = ew >> 2;
+    const int c0 = cw * kCW;
+    const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
+    float* box = reinterpret_cast<float*>(smem + G::kOffEpi) + ew * 1024;
+    int lu = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++lu) {
+      int tn, tm, zb, sub;
+      coords(u, tn, tm, zb, sub);
+      // 16-column passes keep the live set small; the last pass releases the slots
+      if (lane == 0) bulk_wait_read<0>();
+      __syncwarp();
+      // box: 32 rows x kCW fp32 -- 128-byte rows SWIZZLE_128B (kCW 32) or
+      // 64-byte rows SWIZZLE_64B (kCW 16)
+      float* row = box + lane * kCW;
+#pragma unroll
+      for (int h = 0; h < kCW / 16; ++h) {
+        const bool last = h == kCW / 16 - 1;
+        float acc[16], s1[16];
+#pragma unroll
+        for (int gl = 0; gl < kGpc; ++gl) {
+          mbar_wait_spin(&gfull[gl], (uint32_t)lu & 1u);
+          tc_fence_after();
+          float v[16];
+          tmem_ld16(tq + (uint32_t)(gl * BN + c0 + 16 * h), v);
+          if (last) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&gempty[gl]);
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (gl == 0) acc[j] = v[j];
+            else if (gl == 1) acc[j] = acc[j] + v[j];
+            else if (gl == 2) s1[j] = v[j];
+            else { s1[j] = s1[j] + v[j]; acc[j] = acc[j] + s1[j]; }
+          }
+        }
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) {
+          const int ch = kCW == 32 ? ((4 * h + j4) ^ (lane & 7)) : (j4 ^ ((lane >> 1) & 3));
+          *reinterpret_cast<float4*>(row + (ch << 2)) =
+              make_float4(acc[4 * j4], acc[4 * j4 + 1], acc[4 * j4 + 2], acc[4 * j4 + 3]);
+        }
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        tma_store_4d(&tma_p, box, tn * BN + c0, tm * kTcBM + quad * 32, zb, sub * kGpc);
+        bulk_commit();
+      }
+    }
+    if (lane == 0) bulk_wait_all();
+  } else if (with_bias) {
+    // ---------------- bias warps: the unfused path's per-group column sums, subtree of 4
+    const int bt = threadIdx.x - 32 * (2 + kEW);  // 0..63
+    int it = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+      int tn, tm, zb, sub;
+      coords(u, tn, tm, zb, sub);
+      const bool do_sum = tm == 0 && bias_off >= 0;
+      for (int cb = 0; cb < (H ? BN / 2 : BN); cb += 32 * kBiasWarps) {
+        (void)cb;
+      }
+      constexpr int kCols = (H ? BN / 2 : BN) / (32 * kBiasWarps) > 0 ? (H ? BN / 2 : BN) / (32 * kBiasWarps) : 1;
+      float gs[kGpc][kCols], gs2[kGpc][kCols];
+#pragma unroll
+      for (int gl = 0; gl < kGpc; ++gl) {
+        int k0, nkb;
+        krange(sub * kGpc + gl, k0, nkb);
+        float sum[kCols], sum2[kCols];
+#pragma unroll
+        for (int j = 0; j < kCols; ++j) sum[j] = sum2[j] = 0.f;
+        for (int q = 0; q < nkb; ++q, ++it) {
+          const int st = it % kStages;
+          mbar_wait(&full[st], (uint32_t)(it / kStages) & 1u);
+          if (do_sum) {
+            const uint8_t* sb = smem + st * G::kStage + kTcBM * 128;
+#pragma unroll
+            for (int j = 0; j < kCols; ++j) {
+              const int n = H ? 2 * (bt + j * 32 * kBiasWarps) : bt + j * 32 * kBiasWarps;
+              if (n < BN) {
+                if constexpr (H) {
+                  const int bx = n >> 6, nn = n & 63, chunk = nn >> 3;
+                  const uint8_t* base = sb + bx * 8192 + (nn & 7) * 2;
+                  float s0 = 0.f, t1 = 0.f;
+#pragma unroll 8
+                  for (int k = 0; k < BK; ++k) {
+                    const float2 f = __half22float2(*reinterpret_cast<const __half2*>(
+                        base + k * 128 + ((chunk ^ (k & 7)) << 4)));
+                    s0 += f.x;
+                    t1 += f.y;
+                  }
+                  sum[j] += s0;
+                  sum2[j] += t1;
+                } else {
+                  const int bx = n >> 5, nn = n & 31, chunk = nn >> 3;
+                  const float* base = reinterpret_cast<const float*>(sb + bx * 4096) + (nn & 7);
+#pragma unroll 8
+                  for (int k = 0; k < BK; ++k) sum[j] += base[(k * 128 + ((chunk ^ (k & 3)) << 5)) >> 2];
+                }
+              }
+            }
+          }
+          named_bar(1, 32 * kBiasWarps);
+          if (bt == 0) mbar_arrive(&empty[st]);
+        }
+#pragma unroll
+        for (int j = 0; j < kCols; ++j) {
+          gs[gl][j] = sum[j];
+          gs2[gl][j] = sum2[j];
+        }
+      }
+      if (do_sum) {
+#pragma unroll
+        for (int j = 0; j < kCols; ++j) {
+          const int n = H ? 2 * (bt + j * 32 * kBiasWarps) : bt + j * 32 * kBiasWarps;
+          float* dst = part + (int64_t)(sub * kGpc) * n_shared + bias_off + zb * bias_zstride + tn * BN + n;
+          if (n < BN && tn * BN + n < N) dst[0] = (gs[0][j] + gs[1][j]) + (gs[2][j] + gs[3][j]);
+          if (H && n + 1 < BN && tn * BN + n + 1 < N)
+            dst[1] = (gs2[0][j] + gs2[1][j]) + (gs2[2][j] + gs2[3][j]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+  }
+}
+
+// Launcher: partials of the weight at `off` (+ z * sOff), row stride N, into
+// slots 0 and 4 of part [8][n_shared]; bias (bias_off >= 0) likewise.
+template <bool H, int BN>
+inline int wgrad_subtree_launch(const void* X, int Mw, const void* G, int N, int nzb, int64_t sG,
+                                int B_global, int lane0, float* part, int64_t n_shared, int64_t off,
+                                int64_t sOff, int64_t bias_off, cudaStream_t st) {
+  using GG = ws::Geo<BN>;
+  TcShape s{Mw, N, B_global, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 1, 8, 0, B_global,
+            lane0};
+  TcOperand A{X, Mw, 0, 1}, B{G, N, sG, nzb};
+  CUtensorMap ta, tb, tp;
+  int r = tc_operand_maps<BN, true, true, H>(s, A, B, 1, ta, tb);
+  if (r != EDPC_OK) return r;
+  TcStoreMap pm{part + off, {(uint64_t)N, (uint64_t)Mw, (uint64_t)nzb, (uint64_t)kNumGroups},
+                {(uint64_t)N, (uint64_t)sOff, (uint64_t)n_shared}};
+  const bool ok = GG::kCW == 32 ? store_tmap_cache().get(&tp, pm)  // 32 x 32 boxes
+                                : wa_box_map(&tp, part + off, false, N, Mw, nzb, kNumGroups, sOff,
+                                             n_shared);            // 32 x 16 boxes
+  if (!ok) {
+    set_error("wgrad_subtree: partial map not encodable (alignment)");
+    return EDPC_ERR_INVALID;
+  }
+  static bool attr[16] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (!attr[dev & 15]) {
+    cudaFuncSetAttribute(k_wgrad_subtree<H, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         GG::kSmemBytes);
+    attr[dev & 15] = true;
+  }
+  const int units = (N / BN) * ((Mw + kTcBM - 1) / kTcBM) * nzb * 2;
+  const int grid = units < num_sms() ? units : num_sms();
+  cudaError_t e = pdl_launch(k_wgrad_subtree<H, BN>, grid, ws::kThreads, GG::kSmemBytes, st, ta, tb,
+                             tp, Mw, N, nzb, B_global, lane0, part, n_shared, bias_off, sOff,
+                             bias_off >= 0 ? 1 : 0);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string("k_wgrad_subtree launch: ") + cudaGetErrorString(e));
+    return EDPC_ERR_CUDA;
+  }
+  return EDPC_OK;
+}
+
+}  // namespace edpc

@@ -157,12 +157,13 @@ def test_tc_gemm_f16_unit(M, N, K, a_mn, b_mn):
     assert err < 1e-5, (err, C[:2, :4], ref[:2, :4])
 
 
-@pytest.mark.parametrize("switch", ["EDPC_MBRB_FUSED", "EDPC_WGRAD_FUSED"])
+@pytest.mark.parametrize("switch", ["EDPC_MBRB_FUSED", "EDPC_WGRAD_FUSED", "EDPC_WGRAD_SUBTREE"])
 def test_fused_kernels_are_bit_identical(switch):
-    """The fused MBRB forward / backward kernels (mbrb_fused.cuh) and the fused
-    weight-gradient + lane-group tree + Adam kernels (wgrad_adam.cuh) give
-    exactly the unfused paths' container (switch=0, run in a subprocess: the
-    switches are read once per process)."""
+    """The fused MBRB forward / backward kernels (mbrb_fused.cuh), the subtree
+    weight-gradient kernels and the fused weight-gradient + tree + Adam
+    kernels (wgrad_adam.cuh) give exactly the per-group partial path's
+    container (the switch flips the default, in a subprocess: the switches are
+    read once per process)."""
     import os
     import subprocess
     import sys
