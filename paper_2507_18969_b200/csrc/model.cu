@@ -522,18 +522,6 @@ static bool skip_wgrad_experiment() {
 // work of the weight-gradient stream (joined back before the exchange / Adam)
 static cudaStream_t wst(edpc_ctx* c) { return aux_enabled() ? c->st_aux : c->st; }
 
-// Side-stream weight-gradient GEMMs as short-lived CTAs (one work unit each)
-// instead of a persistent grid, so that SMs return to the main stream between
-// units.  EDPC_WGRAD_ONE_UNIT=0 restores the persistent grid.
-static int wgrad_one_unit() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("EDPC_WGRAD_ONE_UNIT");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v;
-}
-
 static cudaError_t fork_aux(edpc_ctx* c) {
   if (!aux_enabled()) return cudaSuccess;
   cudaError_t e = cudaEventRecord(c->ev_fork, c->st);
@@ -602,7 +590,6 @@ static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, in
     Scope sc(c, kRegGemm, ws);
     TcShape s{Mw, N, c->Bl, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 1,
               c->g_count, c->g_first, c->lay.B, c->lane0};
-    s.one_unit = wgrad_one_unit();
     if (bias_off >= 0) {
       s.bias_part = c->Gp;
       s.bias_gstride = c->lay.n_shared;
@@ -742,7 +729,6 @@ static cudaError_t wgrad_h(edpc_ctx* c, const __half* X, int Mw, const __half* G
   Scope sc(c, kRegGemm, ws);
   TcShape s{Mw, N, c->Bl, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 1,
             c->g_count, c->g_first, c->lay.B, c->lane0};
-  s.one_unit = wgrad_one_unit();
   if (bias_off >= 0) {
     s.bias_part = c->Gp;
     s.bias_gstride = c->lay.n_shared;
@@ -1401,7 +1387,7 @@ static int run_model_steps(edpc_ctx* c, int64_t n, int mode) {
         return st;
       }
       CK(e);
-      e = cudaGraphInstantiate(&ge, g, cudaGraphInstantiateFlagUseNodePriority);
+      e = cudaGraphInstantiate(&ge, g, 0);
       cudaGraphDestroy(g);
       CK(e);
     }
@@ -1563,13 +1549,10 @@ int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t origina
                       L.down_w, L.up_w, L.head_w})
       ok = ok && o % 8 == 0;
     c->wfuse = ok;
-    // subtree weight gradients: the same geometry conditions.  Numerics-
-    // neutral but OFF by default: its CTAs walk 4 groups through a 128-wide
-    // tile, twice the k-blocks of the 256-wide per-group GEMMs, and the
-    // per-CTA operand pipeline (~1 k-block per us) is what bounds both (ncu:
-    // global branch 75.7 vs 42.6 us; C2 7.4 vs 8.8 MB/s).  EDPC_WGRAD_SUBTREE=1.
+    // subtree weight gradients: the same geometry conditions (on by default;
+    // EDPC_WGRAD_SUBTREE=0 selects the per-group partial GEMMs for A/B runs)
     const char* e2 = getenv("EDPC_WGRAD_SUBTREE");
-    bool sok = (e2 && e2[0] == '1') && c->use_tc && c->g_count == kNumGroups &&
+    bool sok = !(e2 && e2[0] == '0') && c->use_tc && c->g_count == kNumGroups &&
                L.B % kNumGroups == 0 && (L.B / kNumGroups) % 64 == 0;
     for (int n : {L.F, L.FP, L.HL, L.HG, 256}) sok = sok && n % 64 == 0;
     c->wsub = sok && !c->wfuse;
@@ -1578,17 +1561,10 @@ int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t origina
     delete c;
     return code;
   };
-  // stream priorities: the critical-path stream first, the weight-gradient /
-  // encoder streams last (EDPC_STREAM_PRIO=0: all default)
-  int prio_lo = 0, prio_hi = 0;
-  {
-    const char* e = getenv("EDPC_STREAM_PRIO");
-    if (!(e && e[0] == '0')) cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  }
-  if (cudaStreamCreateWithPriority(&c->st, cudaStreamNonBlocking, prio_hi) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->st_enc, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->st_enc, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->st_aux, cudaStreamNonBlocking, prio_lo) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->st_aux, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->st_h2d, cudaStreamNonBlocking) != cudaSuccess ||

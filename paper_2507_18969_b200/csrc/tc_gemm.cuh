@@ -1189,7 +1189,7 @@ inline int tc_launch(const TcShape& s, const TcOperand& A, const TcOperand& B, c
   if (r != EDPC_OK) return r;
   const int nz = s.nzb * (s.kmode == 0 ? 1 : s.nsplit);
   const int units = (s.N / BN) * (n_tm / cl) * nz;
-  const int max_units = s.one_unit ? units : num_sms() / cl;
+  const int max_units = num_sms() / cl;
   const int grid = (units < max_units ? units : max_units) * cl;
   int dev = 0;
   cudaGetDevice(&dev);
