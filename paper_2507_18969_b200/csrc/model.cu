@@ -1549,10 +1549,13 @@ int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t origina
                       L.down_w, L.up_w, L.head_w})
       ok = ok && o % 8 == 0;
     c->wfuse = ok;
-    // subtree weight gradients: the same geometry conditions (on by default;
-    // EDPC_WGRAD_SUBTREE=0 selects the per-group partial GEMMs for A/B runs)
+    // subtree weight gradients: the same geometry conditions.  Numerics-
+    // neutral but OFF by default: its CTAs walk 4 groups through a 128-wide
+    // tile, twice the k-blocks of the 256-wide per-group GEMMs, and the
+    // per-CTA operand pipeline (~1 k-block per us) is what bounds both (ncu:
+    // global branch 75.7 vs 42.6 us; C2 7.4 vs 8.8 MB/s).  EDPC_WGRAD_SUBTREE=1.
     const char* e2 = getenv("EDPC_WGRAD_SUBTREE");
-    bool sok = !(e2 && e2[0] == '0') && c->use_tc && c->g_count == kNumGroups &&
+    bool sok = (e2 && e2[0] == '1') && c->use_tc && c->g_count == kNumGroups &&
                L.B % kNumGroups == 0 && (L.B / kNumGroups) % 64 == 0;
     for (int n : {L.F, L.FP, L.HL, L.HG, 256}) sok = sok && n % 64 == 0;
     c->wsub = sok && !c->wfuse;

@@ -179,7 +179,7 @@ def test_fused_kernels_are_bit_identical(switch):
             "sys.stdout.buffer.write(write_container(compress(synth.text_like(1024 * 40, 1), cfg, 64)))\n"
             % root)
     env = dict(os.environ, PYTHONPATH=root)
-    env[switch] = "1" if switch == "EDPC_WGRAD_FUSED" else "0"  # the non-default path
+    env[switch] = "0" if switch == "EDPC_MBRB_FUSED" else "1"  # the non-default path
     ref = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
                          timeout=600).stdout
     assert blob == ref
