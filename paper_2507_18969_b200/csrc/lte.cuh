@@ -64,6 +64,12 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_group 0;\n" ::: "memory");
 }
 
+__device__ __forceinline__ float tf32_round_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 __device__ __forceinline__ uint32_t tf32(float x) {
   uint32_t r;
   asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
@@ -149,12 +155,17 @@ struct Frag {
 
 // down = x_local W_d + b_d; mixed_b = down_b U_b; x_lte = mixed W_u + b_u.
 // Also stores down and mixed (operands of the FDM backward and of the
-// weight-gradient GEMMs).
+// weight-gradient GEMMs).  ln_gain != nullptr: also the global MBRB's layer
+// norm of x_lte (nn.py:103-113) -- the x_lte rows of the CTA are complete in
+// shared memory here -- with k_embed_ln's arithmetic and element order
+// (bit-identical), writing x_hat, rstd and x0 (fp16 x0h, or fp32 x0).
 __global__ void __launch_bounds__(lte::kThreads, 3)
 k_lte_fwd(const float* __restrict__ x_local, const float* __restrict__ Wd,
           const float* __restrict__ bd, const float* __restrict__ U, const float* __restrict__ Wu,
           const float* __restrict__ bu, float* __restrict__ down, float* __restrict__ mixed,
-          float* __restrict__ x_lte, int Bl) {
+          float* __restrict__ x_lte, int Bl, const float* __restrict__ ln_gain,
+          const float* __restrict__ ln_bias, float* __restrict__ xhat, float* __restrict__ rstd,
+          float* __restrict__ x0, __half* __restrict__ x0h, int rt) {
   using namespace lte;
   extern __shared__ float4 lte_smem4[];
   float* Xs = reinterpret_cast<float*>(lte_smem4);
@@ -225,12 +236,50 @@ k_lte_fwd(const float* __restrict__ x_local, const float* __restrict__ Wd,
     warp_tile<kFP, true>(acc, Ms, kLdS, Ws + (j >= 2 ? -(kF / 2) : 0), kLdWuF2, n0);
     const Frag f(n0);
     const float q0 = bu[f.c0], q1 = bu[f.c0 + 1];
-    if (b0 + f.r0 < Bl)
-      *reinterpret_cast<float2*>(x_lte + (int64_t)(b0 + f.r0) * kF + f.c0) =
-          make_float2(acc[0] + q0, acc[1] + q1);
+    const float2 lo = make_float2(acc[0] + q0, acc[1] + q1), hi = make_float2(acc[2] + q0, acc[3] + q1);
+    if (b0 + f.r0 < Bl) *reinterpret_cast<float2*>(x_lte + (int64_t)(b0 + f.r0) * kF + f.c0) = lo;
     if (b0 + f.r0 + 8 < Bl)
-      *reinterpret_cast<float2*>(x_lte + (int64_t)(b0 + f.r0 + 8) * kF + f.c0) =
-          make_float2(acc[2] + q0, acc[3] + q1);
+      *reinterpret_cast<float2*>(x_lte + (int64_t)(b0 + f.r0 + 8) * kF + f.c0) = hi;
+    if (ln_gain) {  // the rows for the layer norm below (Xs is free after the down projection)
+      *reinterpret_cast<float2*>(Xs + f.r0 * kLdX + f.c0) = lo;
+      *reinterpret_cast<float2*>(Xs + (f.r0 + 8) * kLdX + f.c0) = hi;
+    }
+  }
+  if (!ln_gain) return;
+  __syncthreads();
+  // global-MBRB layer norm: warp w -> rows 2w, 2w+1; lane -> elements lane + 32 j
+  const int lane = tid & 31;
+#pragma unroll 1
+  for (int rr = 0; rr < 2; ++rr) {
+    const int r = 2 * warp + rr, b = b0 + r;
+    if (b >= Bl) break;
+    float v[kF / 32];
+#pragma unroll
+    for (int j = 0; j < kF / 32; ++j) v[j] = Xs[r * kLdX + lane + 32 * j];
+    float sm = 0.f;
+#pragma unroll
+    for (int j = 0; j < kF / 32; ++j) sm += v[j];
+    const float mean = warp_sum(sm) / (float)kF;
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < kF / 32; ++j) {
+      const float d = v[j] - mean;
+      q += d * d;
+    }
+    const float var = warp_sum(q) / (float)kF;
+    const float rs = 1.0f / sqrtf(var + 1e-5f);
+#pragma unroll
+    for (int j = 0; j < kF / 32; ++j) {
+      const int fidx = lane + 32 * j;
+      const float h = (v[j] - mean) * rs;
+      xhat[(int64_t)b * kF + fidx] = h;
+      const float o = h * ln_gain[fidx] + ln_bias[fidx];
+      if (x0h)
+        x0h[(int64_t)b * kF + fidx] = __float2half_rn(o);
+      else
+        x0[(int64_t)b * kF + fidx] = rt ? tf32_round_rna(o) : o;
+    }
+    if (lane == 0) rstd[b] = rs;
   }
 }
 

@@ -767,11 +767,11 @@ struct MbrbBufs {
 };
 
 static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool gather,
-                        ByteCols src) {
+                        ByteCols src, bool ln_done = false) {
   const Layout& L = c->lay;
   const int Bl = c->Bl, F = L.F, H = o.H;
   dim3 g8((unsigned)cdiv(Bl, 8));
-  {
+  if (!ln_done) {
     Scope sc_ln(c, kRegElem, c->st);
     __half* x0h = c->h16 ? reinterpret_cast<__half*>(b.x0) : nullptr;
     if (gather)
@@ -842,6 +842,17 @@ static int mbrb_forward(edpc_ctx* c, const MbrbOffs& o, const MbrbBufs& b, bool 
 // tf32 rounds operands to nearest, tcgen05 tf32 truncates): numerics bit 2.
 static bool lte_fused(const edpc_ctx* c) { return c->lte_fwd; }
 
+// the global MBRB's layer norm inside k_lte_fwd (bit-identical to the
+// separate k_embed_ln; EDPC_LTE_LN_FUSED=0 selects the latter for A/B runs)
+static bool lte_ln_fused() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EDPC_LTE_LN_FUSED");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static bool lte_fused_possible(const edpc_ctx* c) {
   if (!(c->use_tc && c->lay.F == lte::kF && c->lay.FP == lte::kFP)) return false;
   static signed char attr[64] = {};  // per device: 0 unset, 1 ok, -1 failed
@@ -862,9 +873,13 @@ static int forward(edpc_ctx* c, ByteCols src) {
   EDPC_TRY(mbrb_forward(c, L.loc, lb, true, src));
   if (lte_fused(c)) {
     Scope sc_(c, kRegFdmFwd, c->st);
+    // + the global MBRB's layer norm (its k_embed_ln launch disappears)
+    const bool ln = lte_ln_fused();
     pdl_launch(k_lte_fwd, (unsigned)cdiv(Bl, lte::kRows), lte::kThreads, lte::kSmemBytesF, c->st,
                c->x_local, c->W + L.down_w, c->W + L.down_b, c->U, c->W + L.up_w, c->W + L.up_b,
-               c->down, c->mixed, c->x_lte, Bl);
+               c->down, c->mixed, c->x_lte, Bl, ln ? c->W + L.glo.ln_g : nullptr,
+               c->W + L.glo.ln_b, c->g_xhat, c->g_rstd, c->g_x0,
+               c->h16 ? reinterpret_cast<__half*>(c->g_x0) : nullptr, (int)c->rt);
     CK(cudaGetLastError());
   } else {
   CK(fwd_linear(c, c->x_local, L.F, L.F, wt(c) + L.down_w, L.FP, 1, 0, c->down, 0,
@@ -895,7 +910,7 @@ static int forward(edpc_ctx* c, ByteCols src) {
                 nullptr, Bl));
   }
   MbrbBufs gb{c->x_lte, c->g_xhat, c->g_rstd, c->g_x0, c->g_H, c->g_ff, c->x_global};
-  EDPC_TRY(mbrb_forward(c, L.glo, gb, false, src));
+  EDPC_TRY(mbrb_forward(c, L.glo, gb, false, src, lte_fused(c) && lte_ln_fused()));
   CK(fwd_linear(c, c->x_global, L.F, L.F, wt(c) + L.head_w, 256, 1, 0, c->logits, 0,
                 c->W + L.head_b, nullptr, Bl));
   return EDPC_OK;

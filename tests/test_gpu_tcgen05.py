@@ -157,7 +157,8 @@ def test_tc_gemm_f16_unit(M, N, K, a_mn, b_mn):
     assert err < 1e-5, (err, C[:2, :4], ref[:2, :4])
 
 
-@pytest.mark.parametrize("switch", ["EDPC_MBRB_FUSED", "EDPC_WGRAD_FUSED", "EDPC_WGRAD_SUBTREE"])
+@pytest.mark.parametrize("switch", ["EDPC_MBRB_FUSED", "EDPC_LTE_LN_FUSED", "EDPC_WGRAD_FUSED",
+                                    "EDPC_WGRAD_SUBTREE"])
 def test_fused_kernels_are_bit_identical(switch):
     """The fused MBRB forward / backward kernels (mbrb_fused.cuh), the subtree
     weight-gradient kernels and the fused weight-gradient + tree + Adam
@@ -179,7 +180,8 @@ def test_fused_kernels_are_bit_identical(switch):
             "sys.stdout.buffer.write(write_container(compress(synth.text_like(1024 * 40, 1), cfg, 64)))\n"
             % root)
     env = dict(os.environ, PYTHONPATH=root)
-    env[switch] = "0" if switch == "EDPC_MBRB_FUSED" else "1"  # the non-default path
+    # the non-default path: fused kernels switched off, experimental ones on
+    env[switch] = "0" if switch in ("EDPC_MBRB_FUSED", "EDPC_LTE_LN_FUSED") else "1"
     ref = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
                          timeout=600).stdout
     assert blob == ref
