@@ -519,19 +519,6 @@ static bool skip_wgrad_experiment() {
   return v == 1;
 }
 
-// Weight-gradient GEMMs walk their m-tiles fastest: the units that share a
-// gradient (B) tile run on neighbouring CTAs at the same time, so the second
-// read of that tile hits L2 (ncu: the global branch weight gradient read its
-// 64 MB g_H twice from DRAM).  EDPC_WGRAD_MFAST=0 restores n-fastest.
-static int wgrad_m_fast() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("EDPC_WGRAD_MFAST");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v;
-}
-
 // work of the weight-gradient stream (joined back before the exchange / Adam)
 static cudaStream_t wst(edpc_ctx* c) { return aux_enabled() ? c->st_aux : c->st; }
 
@@ -603,7 +590,6 @@ static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, in
     Scope sc(c, kRegGemm, ws);
     TcShape s{Mw, N, c->Bl, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 1,
               c->g_count, c->g_first, c->lay.B, c->lane0};
-    s.m_fast = wgrad_m_fast();
     if (bias_off >= 0) {
       s.bias_part = c->Gp;
       s.bias_gstride = c->lay.n_shared;
@@ -743,7 +729,6 @@ static cudaError_t wgrad_h(edpc_ctx* c, const __half* X, int Mw, const __half* G
   Scope sc(c, kRegGemm, ws);
   TcShape s{Mw, N, c->Bl, nzb, 1, kBatchNone, nzb > 1 ? kBatchZ : kBatchNone, 1,
             c->g_count, c->g_first, c->lay.B, c->lane0};
-  s.m_fast = wgrad_m_fast();
   if (bias_off >= 0) {
     s.bias_part = c->Gp;
     s.bias_gstride = c->lay.n_shared;

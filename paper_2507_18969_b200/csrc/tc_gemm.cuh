@@ -539,18 +539,10 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
   constexpr uint16_t kMask = (uint16_t)((1u << CL) - 1u);
 
   auto tile_coords = [&](int t, int& tn, int& tm, int& zb, int& zg, int& kb0, int& nkb) {
-    int z;
-    if (s.m_fast) {  // m-tiles of one (n-tile, batch) adjacent: their shared B tile is read once from DRAM
-      tm = (t % n_tmu) * CL + crank;
-      const int r = t / n_tmu;
-      tn = r % n_tn;
-      z = r / n_tn;
-    } else {
-      tn = t % n_tn;
-      const int r = t / n_tn;
-      tm = (r % n_tmu) * CL + crank;
-      z = r / n_tmu;
-    }
+    tn = t % n_tn;
+    const int r = t / n_tn;
+    tm = (r % n_tmu) * CL + crank;
+    const int z = r / n_tmu;
     const int nzb = ZIN > 1 ? 1 : s.nzb;
     zb = z % nzb;
     zg = z / nzb;

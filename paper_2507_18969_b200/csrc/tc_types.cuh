@@ -20,7 +20,6 @@ struct TcShape {
   int kmode, nsplit, g0, B_global, lane0;
   int dbg = 0;  // tests only: 1 = epilogue writes m*1000+n; 2/3 = ablations
   int ts = 0;   // set by the launcher: the output tensor map is valid (TMA-store epilogue)
-  int m_fast = 0;  // work units walk m-tiles fastest (units sharing a B tile run together)
   int mn_lbo = 0, mn_sbo = 0;  // tests only: fp16 MN-major descriptor strides (0 = default)
   // fused column sums of B over K (weight-gradient GEMMs: the bias gradient
   // of lane group g0+zg); needs MN-major B
