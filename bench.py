@@ -31,7 +31,7 @@ of predict -> quantize -> encode -> backward -> Adam.
                 runs (kind::f16 MBRB GEMMs at the measured dense bf16/fp16
                 rate, kind::tf32 LTE/head GEMMs at half of it); ``traffic`` is
                 the GEMMs' DRAM bytes per model step from the committed ncu
-                capture (profiles/r01_gemm_traffic.json).
+                capture (profiles/r02_gemm_traffic.json).
 * ``cpu_baseline`` the CPU oracle (numpy fp64 + C coder, restating the
                 reference) step-sampled at the same B and dims on this host.
 
@@ -383,7 +383,9 @@ def run_ours(args, wl):
     else:
         peak_t, gemm_kind, dtype = peak_16 / 2, "SIMT fp32", "fp32"
     traffic, traffic_src = None, None
-    tp = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "r02_gemm_traffic.json")
+    if not os.path.exists(tp):
+        tp = os.path.join(ROOT, "profiles", "r01_gemm_traffic.json")
     if os.path.exists(tp):
         tj = json.load(open(tp))
         traffic, traffic_src = tj["gemm_dram_bytes_per_step"], tj.get("source", tp)

@@ -56,13 +56,14 @@ def main(path, title):
             print(f"| {name} (encoder stream, not in the total) | {e['grid']} | {t:.1f} | | | | |")
             continue
         tot += t
-        if "k_tc_gemm" in name:
+        if "k_tc_gemm" in name or "k_mbrb_" in name or "k_wgrad_" in name:
             gt += t
             gb += rb + wb
         print(f"| {name} | {e['grid']} | {t:.1f} | {rb:.1f} | {wb:.1f} | "
               f"{e.get(M_TC, 0):.1f} | {e.get(M_L2, 0):.1f} |")
     print(f"| **total** | | {tot:.1f} | | | | |")
-    print(f"\ntcgen05 GEMMs: {gt:.1f} us of {tot:.1f} us; GEMM DRAM traffic {gb:.1f} MB per step.")
+    print(f"\ntcgen05 GEMM kernels (k_tc_gemm, fused k_mbrb_*, k_wgrad_*): {gt:.1f} us of {tot:.1f} us;"
+          f" their DRAM traffic {gb:.1f} MB per step.")
     return dict(gemm_dram_bytes_per_step=gb * 1e6, gemm_us_per_step_serialized=gt,
                 step_us_serialized=tot, source=path)
 
