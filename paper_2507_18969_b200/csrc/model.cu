@@ -507,18 +507,6 @@ static bool aux_enabled() {
   return v == 1;
 }
 
-// Timing experiments only (never set in tests or the bench): skips the
-// weight-gradient GEMMs and the shared Adam to measure what the side stream
-// costs the main stream.  The trajectory is then wrong; nothing is decoded.
-static bool skip_wgrad_experiment() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("EDPC_EXPERIMENT_SKIP_WGRAD");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 // work of the weight-gradient stream (joined back before the exchange / Adam)
 static cudaStream_t wst(edpc_ctx* c) { return aux_enabled() ? c->st_aux : c->st; }
 
@@ -574,7 +562,6 @@ static cudaError_t wgrad_sub(edpc_ctx* c, const void* X, int Mw, const void* G, 
 
 static cudaError_t wgrad(edpc_ctx* c, const float* X, int Mw, const float* G, int N, int nzb,
                          int64_t sG, int64_t off, int64_t sOff, int64_t bias_off) {
-  if (skip_wgrad_experiment()) return cudaSuccess;
   if (c->wsub) return wgrad_sub<false>(c, X, Mw, G, N, nzb, sG, off, sOff, bias_off);
   if (c->wfuse) {  // gradient + tree + Adam in one kernel (no partials, no Adam launch)
     Scope sc(c, kRegGemm, wst(c));
@@ -716,7 +703,6 @@ static cudaError_t dgrad_h(edpc_ctx* c, const __half* G, int Kd, int nsum, int64
 // lanes, by the GEMM's bias warps from its own fp16 B tiles in shared memory
 static cudaError_t wgrad_h(edpc_ctx* c, const __half* X, int Mw, const __half* G, int N, int nzb,
                            int64_t sG, int64_t off, int64_t sOff, int64_t bias_off) {
-  if (skip_wgrad_experiment()) return cudaSuccess;
   if (c->wsub) return wgrad_sub<true>(c, X, Mw, G, N, nzb, sG, off, sOff, bias_off);
   if (c->wfuse) {
     Scope sc(c, kRegGemm, wst(c));
@@ -1205,7 +1191,7 @@ static void adam_launch(edpc_ctx* c, int blocks, cudaStream_t st, int64_t off, i
 // pstride (8 lane groups, or G subtree sums)
 static int adam_range(edpc_ctx* c, int64_t off, int64_t len, cudaStream_t st, int nl,
                       int64_t pstride) {
-  if (len <= 0 || skip_wgrad_experiment()) return EDPC_OK;
+  if (len <= 0) return EDPC_OK;
   if (pstride < 0) pstride = c->lay.n_shared;
   const int blocks = (int)std::min<int64_t>(cdiv(len, 256), 148 * 8);
   {
