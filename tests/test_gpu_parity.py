@@ -93,11 +93,12 @@ def test_trained_probs_match_oracle(name, dims, lanes, segs, kind, nbytes, steps
 
 
 GRAD_CASES = [
-    # (cfg, relative tolerance per tensor): fp32 SIMT path / tcgen05 + fp16 path
-    (TINY, 1e-4),
-    (ModelConfig(**DESK, lanes=16), 1e-4),
-    (ModelConfig(**PAPER, lanes=64), 1e-4),
-    (ModelConfig(**PAPER, lanes=4096), 2e-2),
+    # (cfg, relative Frobenius tolerance per tensor): fp32 SIMT path (measured
+    # <= 2.3e-6) / tcgen05 + fp16 MBRB + tf32 path at paper dims (measured <= 1.6e-3)
+    (TINY, 1e-5),
+    (ModelConfig(**DESK, lanes=16), 1e-5),
+    (ModelConfig(**PAPER, lanes=64), 1e-5),
+    (ModelConfig(**PAPER, lanes=4096), 5e-3),
 ]
 
 
