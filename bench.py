@@ -323,8 +323,9 @@ def run_ours(args, wl):
         from paper_2507_18969_b200 import compress, decompress, read_container, write_container
         e_n = min(n, args.e2e_bytes) if args.e2e_bytes else n
         stream = bytes(data[:e_n])
+        cstats: dict = {}
         t0 = time.perf_counter()
-        blob = write_container(compress(stream, cfg, S))
+        blob = write_container(compress(stream, cfg, S, stats=cstats))
         ce_s = time.perf_counter() - t0
         t0 = time.perf_counter()
         back = decompress(read_container(blob))
@@ -339,7 +340,10 @@ def run_ours(args, wl):
         full = dict(full_stream_bytes=e_n, full_stream_compress_MBps=e_n / ce_s / 1e6,
                     full_stream_decompress_MBps=e_n / de_s / 1e6, full_stream_lossless=ok,
                     full_stream_bits_per_byte=8.0 * len(blob) / e_n,
-                    full_stream_compress_s=ce_s, full_stream_decompress_s=de_s)
+                    full_stream_compress_s=ce_s, full_stream_decompress_s=de_s,
+                    full_stream_compress_breakdown_s={k: round(cstats[k], 4) for k in
+                                                      ("setup_s", "device_loop_s", "encode_s")
+                                                      if k in cstats})
 
     # ---- bits/byte vs the reference's own run of the C2-mini stream
     ratio = {}
