@@ -76,6 +76,14 @@ WORKLOADS = {
 METRIC = "compress/decompress MB/s at 1/2/4/8 B200 + bits/byte vs CPU ref"
 
 
+_T0 = time.perf_counter()
+
+
+def note(msg: str) -> None:
+    """Progress on stderr (stdout carries only the JSON line)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def gemm_flops_per_lane(m) -> float:
     F = m["context_len"] * m["embed_dim"]
     Fp = F // m["lte_ratio"]
@@ -264,6 +272,7 @@ def run_ours(args, wl):
         return ms.value, regions, c.value
 
     # ---- compress (device-resident input)
+    note("compress loop")
     ctx = DeviceContext(cfg, S, n, 0)
     ctx.load_flat(params)
     numerics = ctx.numerics()
@@ -294,6 +303,7 @@ def run_ours(args, wl):
     region_bpb = 8.0 * tot.value / (B * C)
 
     # ---- decompress the same columns
+    note("decompress loop")
     dctx = DeviceContext(cfg, S, n, 0)
     dctx.load_flat(params)
     _lib.check(lib.edpc_set_payloads(dctx.h, pay.ctypes.data, bits.ctypes.data))
@@ -315,6 +325,7 @@ def run_ours(args, wl):
     dctx.close()
 
     # ---- e2e: the whole stream through the public API (host bytes in,
+    note("full-stream e2e")
     # container bytes out): context setup, parameter upload, streaming column
     # H2D, graph-replayed model steps, device payload assembly + D2H, container
     # write; then the full decompress, checked lossless
@@ -342,10 +353,12 @@ def run_ours(args, wl):
                     full_stream_bits_per_byte=8.0 * len(blob) / e_n,
                     full_stream_compress_s=ce_s, full_stream_decompress_s=de_s,
                     full_stream_compress_breakdown_s={k: round(cstats[k], 4) for k in
-                                                      ("setup_s", "device_loop_s", "encode_s")
+                                                      ("setup_s", "device_loop_s", "encode_s",
+                                                       "finish_s", "payload_d2h_s", "close_s")
                                                       if k in cstats})
 
     # ---- bits/byte vs the reference's own run of the C2-mini stream
+    note("ratio")
     ratio = {}
     if not args.no_ratio and wl is WORKLOADS["c2"]:
         from paper_2507_18969_b200 import compress, write_container
@@ -361,6 +374,7 @@ def run_ours(args, wl):
             ratio["ratio_delta_vs_ref"] = (len(mini) / len(blob)) / ref["ratio"] - 1.0
 
     # ---- CPU baseline (bounded sample, rank 0, N=1)
+    note("cpu baseline")
     cpu = None
     if not args.no_cpu:
         r = cpu_sample(wl, min_seconds=args.cpu_seconds, max_steps=20)

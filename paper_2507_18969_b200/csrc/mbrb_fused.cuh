@@ -609,7 +609,7 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
   uint64_t* dfull = tempty1 + 2;   // [2] D tiles of a chunk loaded into staging buffer u
   uint64_t* staged = dfull + 2;    // g_H of a chunk written (one arrive per epilogue warp)
   uint64_t* a2empty = staged + 1;  // MMA2 done with a chunk's staging buffer
-  uint64_t* sdone = a2empty + 1;   // the store warp has consumed a chunk's `staged` phase
+  uint64_t* sdone = a2empty + 1;   // the store warp has finished a chunk (all its waits for it)
   uint64_t* t2full = sdone + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t2full + 1);
 
@@ -706,7 +706,6 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
       for (int c = 0; c < nc; ++c) {
         const int u = c & 1, h0 = h_begin + c * kHC;
         mbar_wait(staged, (uint32_t)c & 1u);
-        mbar_arrive(sdone);
         for (int z = 0; z < 2; ++z) tma_store_3d(&tm_gh, sS + (2 * u + z) * kTile, h0, m0, z);
         bulk_commit();
         if (c + 2 < nc) {  // buffer u takes chunk c+2 once the stores and MMA2(c) have read it
@@ -714,6 +713,7 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
           mbar_wait(a2empty, (uint32_t)c & 1u);
           load_d(c + 2);
         }
+        mbar_arrive(sdone);  // iteration c done: both of its parity waits are behind it
       }
       bulk_wait_all();
     }
@@ -803,11 +803,13 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
         }
       }
       fence_async_smem();
-      // `staged` must not run two phases ahead of its two consumers (the
-      // store warp and the MMA2 issuer wait on its parity): chunk c-1's phase
-      // consumed by both -- MMA2(c-1) complete, the store warp past it --
-      // before chunk c's arrivals.  (Without this the epilogue, which needs
-      // neither of them to proceed, could lap them and deadlock the CTA.)
+      // Parity waits alias when a barrier completes two phases before its
+      // waiter looks: chunk c's `staged` arrivals wait until MMA2(c-1) has
+      // completed (the MMA2 issuer is past staged(c-1)) and the store warp has
+      // finished iteration c-1 (past its staged(c-1) and a2empty(c-1) waits),
+      // so neither `staged` nor `a2empty` can lap the thread waiting on it.
+      // (Without this the epilogue, which needs neither of them to proceed,
+      // could run two chunks ahead and deadlock the CTA.)
       if (c > 0) {
         mbar_wait(a2empty, (uint32_t)(c - 1) & 1u);
         mbar_wait(sdone, (uint32_t)(c - 1) & 1u);

@@ -114,10 +114,14 @@ def compress(data: bytes, cfg: ModelConfig, segments: int = 4, *,
         bits = np.zeros(segments, dtype=np.int64)
         total = ctypes.c_int64(0)
         _lib.check(lib.edpc_compress_finish(ctx.h, bits.ctypes.data, ctypes.addressof(total)))
+        finish_s = time.perf_counter() - te
         pay = np.zeros(max(total.value, 1), dtype=np.uint8)
         _lib.check(lib.edpc_get_payloads(ctx.h, pay.ctypes.data, pay.size))
+        d2h_s = time.perf_counter() - te - finish_s
     finally:
+        tc = time.perf_counter()
         ctx.close()
+        close_s = time.perf_counter() - tc
     payloads, pos = [], 0
     for b in bits.tolist():
         nb = (b + 7) // 8
@@ -125,7 +129,8 @@ def compress(data: bytes, cfg: ModelConfig, segments: int = 4, *,
         pos += nb
     _stats(stats, steps=max(0, L - T), predict_s=loop_s, train_s=0.0,
            encode_s=time.perf_counter() - te, wall_s=time.perf_counter() - t0,
-           peak_queue_depth=0, setup_s=setup_s, device_loop_s=loop_s,
+           peak_queue_depth=0, setup_s=setup_s, device_loop_s=loop_s, finish_s=finish_s,
+           payload_d2h_s=d2h_s, close_s=close_s,
            note="predict, quantize, encode and train run as one device schedule: "
                 "predict_s is the whole device loop, train_s is inside it")
     return EdpcContainer(header=Header.from_config(cfg, n, bits.tolist(), numerics),
