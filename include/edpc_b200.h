@@ -190,6 +190,12 @@ int edpc_ctx_set_comm(edpc_ctx* ctx, const uint8_t* id, int32_t nranks, int32_t 
 
 int edpc_sync(edpc_ctx* ctx);
 
+/* Context buffers come from the device's stream-ordered memory pool and stay
+ * cached there after edpc_ctx_destroy (the next context reuses them; no
+ * reference counterpart -- the reference allocates host arrays per call).
+ * Returns the cached, unused memory of `device` to the driver. */
+int edpc_trim_pool(int32_t device);
+
 /* test/debug read-back of internal fp32 buffers after a step:
  * 0 gradient partials [8][n_shared], 1 probs, 2 x_local, 3 x_lte, 4 x_global,
  * 5 local branch outputs [k][B][h_l], 6 global branch outputs, 7 d(embedded

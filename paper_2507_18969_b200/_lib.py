@@ -93,6 +93,7 @@ _SIGS = {
     "edpc_nccl_unique_id": ([_P, _I32], ctypes.c_int),
     "edpc_ctx_set_comm": ([_P, _P, _I32, _I32], ctypes.c_int),
     "edpc_sync": ([_P], ctypes.c_int),
+    "edpc_trim_pool": ([ctypes.c_int32], ctypes.c_int),
     "edpc_debug_read": ([_P, _I32, _P, _I64], ctypes.c_int),
     "edpc_ctx_numerics": ([_P, _P], ctypes.c_int),
     "edpc_ksg_counts": ([_P, _I32, _P, _I32, _I64, _I32, _I32, _P, _P, _P], ctypes.c_int),

@@ -15,6 +15,7 @@
 #include <type_traits>
 #include <cmath>
 #include <string>
+#include <mutex>
 #include <vector>
 
 #include <dlfcn.h>
@@ -299,7 +300,9 @@ struct edpc_ctx {
     for (auto& g : graph)
       if (g) cudaGraphExecDestroy(g);
     if (comm) nccl().commDestroy(comm);
-    for (void* p : allocs) cudaFree(p);
+    // back to the device's stream-ordered pool (kept resident: the next
+    // context's allocations reuse it instead of cudaMalloc/cudaFree round trips)
+    for (void* p : allocs) cudaFreeAsync(p, st);
     if (ev) cudaEventDestroy(ev);
     if (t0) cudaEventDestroy(t0);
     if (t1) cudaEventDestroy(t1);
@@ -318,9 +321,11 @@ struct edpc_ctx {
     size_t bytes = (size_t)std::max<int64_t>(count, 1) * sizeof(T);
     bytes = (bytes + 255) & ~(size_t)255;
     void* q = nullptr;
-    cudaError_t e = cudaMalloc(&q, bytes);
+    // stream-ordered pool allocation, complete before any other stream uses it
+    cudaError_t e = cudaMallocAsync(&q, bytes, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) {
-      set_error("cudaMalloc(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+      set_error("cudaMallocAsync(" + std::to_string(bytes) + "): " + cudaGetErrorString(e));
       return EDPC_ERR_NOMEM;
     }
     allocs.push_back(q);
@@ -1408,6 +1413,38 @@ static int set_step(edpc_ctx* c, int64_t i, int64_t t) {
   return EDPC_OK;
 }
 
+// Context buffers come from the device's default stream-ordered pool, with the
+// release threshold lifted so freed contexts keep their memory for the next
+// one (back-to-back compress/decompress calls skip cudaMalloc/cudaFree, whose
+// first-touch mapping and implicit device syncs cost 0.1-1.3 s per context at
+// C2/C3 sizes); `edpc_trim_pool` hands it back.  Peers that can reach the
+// device get pool access (the sharded optimizer's peer pulls).
+static void pool_setup(int device) {
+  static std::mutex mu;
+  static std::vector<bool> done;
+  std::lock_guard<std::mutex> g(mu);
+  if (device < 0) return;
+  if ((int)done.size() <= device) done.resize(device + 1, false);
+  if (done[device]) return;
+  done[device] = true;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) return;
+  uint64_t keep = UINT64_MAX;
+  cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  int n = 0;
+  cudaGetDeviceCount(&n);
+  for (int p = 0; p < n; ++p) {
+    int ok = 0;
+    if (p == device || cudaDeviceCanAccessPeer(&ok, p, device) != cudaSuccess || !ok) continue;
+    cudaMemAccessDesc d{};
+    d.location.type = cudaMemLocationTypeDevice;
+    d.location.id = p;
+    d.flags = cudaMemAccessFlagsProtReadWrite;
+    cudaMemPoolSetAccess(pool, &d, 1);
+  }
+  cudaGetLastError();
+}
+
 static int launch_encoder(edpc_ctx* c, int64_t upto) {
   if (upto <= c->enc_upto) return EDPC_OK;
   CK(cudaEventRecord(c->ev, c->st));
@@ -1565,6 +1602,7 @@ int edpc_ctx_create_ex(const edpc_config* cfg, int32_t segments, int64_t origina
     delete c;
     return code;
   };
+  pool_setup(c->device);
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
       cudaStreamCreateWithFlags(&c->st_enc, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming) != cudaSuccess ||
@@ -2503,6 +2541,15 @@ int edpc_debug_keep_grads(edpc_ctx* c, int32_t keep) {
       cudaGraphExecDestroy(g);
       g = nullptr;
     }
+  return EDPC_OK;
+}
+
+int edpc_trim_pool(int32_t device) {
+  EDPC_CUDA_TRY(cudaSetDevice(device));
+  cudaMemPool_t pool;
+  EDPC_CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, device));
+  EDPC_CUDA_TRY(cudaDeviceSynchronize());
+  EDPC_CUDA_TRY(cudaMemPoolTrimTo(pool, 0));
   return EDPC_OK;
 }
 
