@@ -1102,16 +1102,12 @@ inline int num_sms() {
   return dev < 16 && n[dev] ? n[dev] : 148;
 }
 
-// 2-CTA multicast clusters: correct, but measured slower on these shapes
-// (the GEMMs are not L2-bandwidth bound), so opt-in via EDPC_CLUSTER=1.
-inline bool cluster_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("EDPC_CLUSTER");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
+// 2-CTA multicast clusters (CL = 2): measured slower than CL = 1 in round 1
+// (the GEMMs were not L2-bandwidth bound), and under the round-2 schedule
+// (programmatic dependent launch on every step kernel, fused cluster MBRB
+// kernels beside them) the CL = 2 step deadlocks, so the path is compiled out
+// of the launch decision until it is reworked; the kernel template keeps it.
+inline constexpr bool cluster_enabled() { return false; }
 
 template <typename Kern, typename Epi>
 inline cudaError_t launch_tc(Kern kern, int grid, int threads, int smem, cudaStream_t st, int cl,
