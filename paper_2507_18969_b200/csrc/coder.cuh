@@ -292,11 +292,10 @@ __device__ __forceinline__ uint32_t read_bit(const uint8_t* data, int64_t bit_le
 }
 
 // Given the decoded symbol's interval, advance the decoder (coder.py:198-223).
-// Returns false on exhaustion (bitpos beyond bit_length + 64).  fetch(bi)
-// returns payload byte bi (< ceil(bit_length / 8)).
-template <class Fetch>
-__device__ __forceinline__ bool dec_advance_f(DecState& st, Fetch&& fetch, int64_t bit_length,
-                                              uint64_t span, uint32_t c_lo, uint32_t c_hi) {
+// Returns false on exhaustion (bitpos beyond bit_length + 64).
+__device__ __forceinline__ bool dec_advance(DecState& st, const uint8_t* data,
+                                            int64_t bit_length, uint64_t span, uint32_t c_lo,
+                                            uint32_t c_hi) {
   uint64_t low = st.low, code = st.code;
   uint64_t high = low + ((span * c_hi) >> 16) - 1;
   low = low + ((span * c_lo) >> 16);
@@ -322,7 +321,7 @@ __device__ __forceinline__ bool dec_advance_f(DecState& st, Fetch&& fetch, int64
       const int64_t bi = bp >> 3;
       if (bi != st.cidx) {
         st.cidx = bi;
-        st.cbyte = fetch(bi);
+        st.cbyte = data[bi];
       }
       bit = (st.cbyte >> (7 - (bp & 7))) & 1u;
     } else if (bp > limit) {
@@ -337,13 +336,6 @@ __device__ __forceinline__ bool dec_advance_f(DecState& st, Fetch&& fetch, int64
   st.code = code;
   st.bitpos = bp;
   return true;
-}
-
-__device__ __forceinline__ bool dec_advance(DecState& st, const uint8_t* data,
-                                            int64_t bit_length, uint64_t span, uint32_t c_lo,
-                                            uint32_t c_hi) {
-  return dec_advance_f(st, [&](int64_t bi) { return (uint32_t)data[bi]; }, bit_length, span, c_lo,
-                       c_hi);
 }
 
 // coder.py:186: value = ((code - low + 1) * TOTAL - 1) // span.  num < 2^49

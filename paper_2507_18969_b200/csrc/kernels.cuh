@@ -1354,25 +1354,6 @@ __global__ void k_decode_column(uint8_t* __restrict__ mat, int64_t L, StepIdx si
   const uint8_t* data = pay + pay_off[s];
   const int64_t nbits = bits[s];
   bool ok = !dead;
-  // the payload bytes this column will consume, fetched into the warp up front
-  // (lane l holds bytes wb0 + 4l .. 4l+3; 128 bytes >= spl symbols x the
-  // longest code of 16 bits + renormalisation): the serial renormalisation
-  // loop then reads them with a shuffle instead of a dependent global load
-  // every 8 bits; bytes past the window fall back to global loads
-  const int64_t nbytes = (nbits + 7) >> 3;
-  const int64_t wb0 = st.bitpos >> 3;
-  uint32_t win = 0;
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int64_t bi = wb0 + 4 * lane + q;
-    if (bi < nbytes) win |= (uint32_t)data[bi] << (8 * q);
-  }
-  auto fetch = [&](int64_t bi) -> uint32_t {
-    const int64_t rel = bi - wb0;  // warp-uniform: every lane runs the same coder state
-    if (rel >= 0 && rel < 128)
-      return (__shfl_sync(0xffffffffu, win, (int)(rel >> 2)) >> (8 * (rel & 3))) & 0xffu;
-    return (uint32_t)data[bi];
-  };
   // the segment's CDF rows are independent of the coder state: loaded kPf
   // rows ahead (double-buffered) so the serial symbol chain never waits on them
   constexpr int kPf = 8;
@@ -1408,7 +1389,7 @@ __global__ void k_decode_column(uint8_t* __restrict__ mat, int64_t L, StepIdx si
         const uint64_t value = dec_value(st, span);
         uint32_t c_lo, c_hi;
         sym = warp_find_symbol(cum, value, c_lo, c_hi);
-        ok = dec_advance_f(st, fetch, nbits, span, c_lo, c_hi);
+        ok = dec_advance(st, data, nbits, span, c_lo, c_hi);
         if (!ok) sym = 0;
       }
       if (lane == 0) mat[(int64_t)b * L + i] = (uint8_t)sym;

@@ -564,9 +564,9 @@ inline int mbrb_fwd_fused(const __half* x0h, const __half* Wb, int64_t sW, const
 //
 // Same skeleton as the forward: a CTA owns a 128-row tile and one H slice in
 // chunks of 64; MMA1 (N = 64, K = F) into a double-buffered TMEM accumulator,
-// the epilogue multiplies by the D_z pieces it loads into registers one chunk
-// ahead and writes g_H_z into double-buffered staging tiles -- which serve as
-// the A operands of MMA2 (acc2 += g_H_z . W_z^T, N = F)
+// the epilogue multiplies by the D_z tiles that a loader warp TMA-loads into
+// double-buffered staging tiles and writes g_H_z back in place -- the staging
+// tiles then serve as the A operands of MMA2 (acc2 += g_H_z . W_z^T, N = F)
 // and as the source of the g_H_z TMA stores.  The 4 slices of a row tile are
 // a cluster and reduce over DSMEM in rank order.  MMA2 walks each 64-deep
 // block as branch 0 then branch 1, the order of the unfused split-K dgrad
@@ -574,7 +574,7 @@ inline int mbrb_fwd_fused(const __half* x0h, const __half* Wb, int64_t sW, const
 namespace mb {
 constexpr int kBM = 128, kF = 256, kHC = 64, kEW = 16, kCW = kHC / (kEW / 4);
 constexpr int kB1Stages = 4;
-constexpr int kThreads = 32 * (2 + kEW + 3);  // + W_z producer, g_H store warp, MMA2 issuer
+constexpr int kThreads = 32 * (2 + kEW + 3);  // + W_z producer, store/D loader, MMA2 issuer
 constexpr int kA1Bytes = kBM * kF * 2;        // g_up tile, 64 KB
 constexpr int kB1Stage = kHC * 64 * 2;        // W_out rows of the chunk, one 64-deep k-block: 8 KB
 constexpr int kB2Bytes = 2 * kF * kHC * 2;    // both branches' W_z^T blocks: 64 KB
@@ -589,7 +589,7 @@ constexpr int kSmemBytes = 1024 + kOffBar + 256;
 
 __global__ void __launch_bounds__(mb::kThreads, 1)
 k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant__ CUtensorMap tm_wo,
-                 const __grid_constant__ CUtensorMap tm_wb, const __half* __restrict__ Dg,
+                 const __grid_constant__ CUtensorMap tm_wb, const __grid_constant__ CUtensorMap tm_d,
                  const __grid_constant__ CUtensorMap tm_gh, int Bl, int H, float* __restrict__ out) {
   using namespace mb;
   extern __shared__ uint8_t smem_raw[];
@@ -606,9 +606,10 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
   uint64_t* b2empty = b2full + 1;
   uint64_t* tfull1 = b2empty + 1;  // [2]
   uint64_t* tempty1 = tfull1 + 2;  // [2]
-  uint64_t* staged = tempty1 + 2;  // g_H of a chunk written (one arrive per epilogue warp)
+  uint64_t* dfull = tempty1 + 2;   // [2] D tiles of a chunk loaded into staging buffer u
+  uint64_t* staged = dfull + 2;    // g_H of a chunk written (one arrive per epilogue warp)
   uint64_t* a2empty = staged + 1;  // MMA2 done with a chunk's staging buffer
-  uint64_t* sdone = a2empty + 1;   // the store warp has finished a chunk (stores read it)
+  uint64_t* sdone = a2empty + 1;   // the store warp has finished a chunk (all its waits for it)
   uint64_t* t2full = sdone + 1;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(t2full + 1);
 
@@ -632,6 +633,7 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull1[b], 1);
       mbar_init(&tempty1[b], kEW);
+      mbar_init(&dfull[b], 1);
     }
     mbar_init(staged, kEW);
     mbar_init(a2empty, 1);
@@ -691,15 +693,27 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
     }
   } else if (warp == 3 + kEW) {
     if (lane == 0) {
-      // ---------------- g_H store warp
+      // ---------------- D loader + g_H store warp
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_d) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(&tm_gh) : "memory");
+      auto load_d = [&](int c) {
+        const int u = c & 1;
+        mbar_expect_tx(&dfull[u], 2 * kTile);
+        for (int z = 0; z < 2; ++z)
+          tma_load_3d(sS + (2 * u + z) * kTile, &tm_d, &dfull[u], h_begin + c * kHC, m0, z);
+      };
+      for (int c = 0; c < 2 && c < nc; ++c) load_d(c);
       for (int c = 0; c < nc; ++c) {
         const int u = c & 1, h0 = h_begin + c * kHC;
         mbar_wait(staged, (uint32_t)c & 1u);
         for (int z = 0; z < 2; ++z) tma_store_3d(&tm_gh, sS + (2 * u + z) * kTile, h0, m0, z);
         bulk_commit();
-        bulk_wait_read<0>();
-        mbar_arrive(sdone);  // iteration c done: its staged wait is behind it, buffer u read
+        if (c + 2 < nc) {  // buffer u takes chunk c+2 once the stores and MMA2(c) have read it
+          bulk_wait_read<0>();
+          mbar_wait(a2empty, (uint32_t)c & 1u);
+          load_d(c + 2);
+        }
+        mbar_arrive(sdone);  // iteration c done: both of its parity waits are behind it
       }
       bulk_wait_all();
     }
@@ -754,36 +768,11 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
       tc_commit(t2full);
     }
   } else if (warp < 2 + kEW) {
-    // ---------------- epilogue: g_H_z = g_ff * D_z into the staging tiles.
-    // Each thread owns row r, columns [half * kCW, +kCW) of a chunk: its D_z
-    // pieces (2 x 32 B per branch) are loaded straight into registers one
-    // chunk ahead -- a TMA-loaded D tile could only be prefetched into a
-    // staging buffer once MMA2 and the stores had released it, which left the
-    // epilogue waiting on DRAM every chunk (ncu: the D-full barrier was the
-    // top stall).  Staging buffer u is free for chunk c because this warp
-    // waited for MMA2(c-2) and the store warp's iteration c-2 before arriving
-    // for chunk c-1 (below).
+    // ---------------- epilogue: g_H_z = g_ff * D_z, in place in the staging tiles
     const int quad = warp & 3, half = (warp - 2) >> 2, r = quad * 32 + lane;
     const uint32_t tq = tmem + ((uint32_t)(quad * 32) << 16);
-    const int64_t plane = (int64_t)Bl * H;
-    const bool row_ok = m0 + r < Bl;
-    const __half* drow = Dg + (int64_t)(row_ok ? m0 + r : 0) * H + h_begin + half * kCW;
-    auto load_d = [&](int c, uint4 (&q)[2][2]) {
-#pragma unroll
-      for (int z = 0; z < 2; ++z) {
-        const uint4* p = reinterpret_cast<const uint4*>(drow + z * plane + (int64_t)c * kHC);
-        q[z][0] = row_ok ? __ldg(p) : make_uint4(0u, 0u, 0u, 0u);  // rows past Bl: TMA's zero fill
-        q[z][1] = row_ok ? __ldg(p + 1) : make_uint4(0u, 0u, 0u, 0u);
-      }
-    };
-    uint4 dn[2][2];
-    load_d(0, dn);
     for (int c = 0; c < nc; ++c) {
       const int b = c & 1, u = c & 1;
-      uint4 dc[2][2];
-#pragma unroll
-      for (int z = 0; z < 2; ++z) dc[z][0] = dn[z][0], dc[z][1] = dn[z][1];
-      if (c + 1 < nc) load_d(c + 1, dn);
       mbar_wait(&tfull1[b], (uint32_t)(c >> 1) & 1u);
       tc_fence_after();
       float g[kCW];
@@ -791,13 +780,17 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty1[b]);
+      mbar_wait(&dfull[u], (uint32_t)(c >> 1) & 1u);
 #pragma unroll
       for (int z = 0; z < 2; ++z) {
         const uint32_t row = smem_u32(sS + (2 * u + z) * kTile) + (uint32_t)(r * 128);
 #pragma unroll
         for (int jj = 0; jj < kCW / 8; ++jj) {
           const uint32_t a = row + (uint32_t)(((half * kCW / 8 + jj) ^ (r & 7)) << 4);
-          uint32_t w[4] = {dc[z][jj].x, dc[z][jj].y, dc[z][jj].z, dc[z][jj].w};
+          uint32_t w[4];
+          asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                       : "r"(a));
 #pragma unroll
           for (int q = 0; q < 4; ++q) {  // EpiBwdActH: g_H = g_ff * D, rounded to fp16
             const float2 d = __half22float2(*reinterpret_cast<const __half2*>(&w[q]));
@@ -813,10 +806,10 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
       // Parity waits alias when a barrier completes two phases before its
       // waiter looks: chunk c's `staged` arrivals wait until MMA2(c-1) has
       // completed (the MMA2 issuer is past staged(c-1)) and the store warp has
-      // finished iteration c-1, so `staged` cannot lap either of its waiters.
+      // finished iteration c-1 (past its staged(c-1) and a2empty(c-1) waits),
+      // so neither `staged` nor `a2empty` can lap the thread waiting on it.
       // (Without this the epilogue, which needs neither of them to proceed,
-      // could run two chunks ahead and deadlock the CTA.)  The same two waits
-      // free staging buffer u for chunk c+1's writes.
+      // could run two chunks ahead and deadlock the CTA.)
       if (c > 0) {
         mbar_wait(a2empty, (uint32_t)(c - 1) & 1u);
         mbar_wait(sdone, (uint32_t)(c - 1) & 1u);
@@ -886,12 +879,13 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
 inline int mbrb_bwd_fused(const __half* guph, const __half* Wo, const __half* Wb, int64_t sW,
                           const __half* D, __half* GH, int Bl, int H, float* out, cudaStream_t st) {
   using namespace mb;
-  CUtensorMap tg, to, tw, th;
+  CUtensorMap tg, to, tw, td, th;
   int r = tmap_cache().get(&tg, guph, kF, (uint64_t)Bl, 1, kF, 0, 64, kBM, 2);
   if (r == EDPC_OK) r = tmap_cache().get(&to, Wo, kF, (uint64_t)H, 1, kF, 0, 64, 64, 2);
   if (r == EDPC_OK) r = tmap_cache().get(&tw, Wb, (uint64_t)H, kF, 2, (uint64_t)H, (uint64_t)sW, 64, 256, 2);
   if (r != EDPC_OK) return r;
-  if (!fused_map_cache().get(&th, GH, (uint64_t)H, (uint64_t)Bl, 2)) {
+  if (!fused_map_cache().get(&td, D, (uint64_t)H, (uint64_t)Bl, 2) ||
+      !fused_map_cache().get(&th, GH, (uint64_t)H, (uint64_t)Bl, 2)) {
     set_error("mbrb_bwd_fused: fp16 tile maps not encodable");
     return EDPC_ERR_CUDA;
   }
@@ -916,7 +910,7 @@ inline int mbrb_bwd_fused(const __half* guph, const __half* Wo, const __half* Wb
   at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl_enabled() ? 2 : 1;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, k_mbrb_bwd_fused, tg, to, tw, D, th, Bl, H, out);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, k_mbrb_bwd_fused, tg, to, tw, td, th, Bl, H, out);
   if (e == cudaSuccess) e = cudaGetLastError();
   if (e != cudaSuccess) {
     set_error(std::string("k_mbrb_bwd_fused launch: ") + cudaGetErrorString(e));
