@@ -154,9 +154,9 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
   uint64_t* a1full = bar;
   uint64_t* b1full = bar + 1;
   uint64_t* b1empty = b1full + kB1Stages;
-  uint64_t* b2full = b1empty + kB1Stages;
-  uint64_t* b2empty = b2full + 1;
-  uint64_t* tfull1 = b2empty + 1;   // [2]
+  uint64_t* b2full = b1empty + kB1Stages;  // [2] out-projection weight halves (n 0-127, 128-255)
+  uint64_t* b2empty = b2full + 2;          // [2]
+  uint64_t* tfull1 = b2empty + 2;   // [2]
   uint64_t* tempty1 = tfull1 + 2;   // [2]
   uint64_t* staged = tempty1 + 2;   // ff / D_z of a chunk written (one arrive per epilogue warp)
   uint64_t* a2empty = staged + 1;   // MMA2 done reading ff
@@ -179,8 +179,10 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
       mbar_init(&b1full[s], 1);
       mbar_init(&b1empty[s], 1);
     }
-    mbar_init(b2full, 1);
-    mbar_init(b2empty, 1);
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&b2full[q], 1);
+      mbar_init(&b2empty[q], 1);
+    }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull1[b], 1);
       mbar_init(&tempty1[b], kEW);
@@ -240,10 +242,15 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
         const int h0 = h_begin + c * kHC;
         if (c + 1 < nc)
           for (int j = 0; j < kF / 64; ++j) tma_prefetch_3d(&tm_wo, j * 64, h0 + kHC, 0);
-        mbar_wait(b2empty, ((uint32_t)c & 1u) ^ 1u);
-        mbar_expect_tx(b2full, kB2Bytes);
-#pragma unroll
-        for (int j = 0; j < kF / 64; ++j) tma_load_3d(sB2 + j * 8192, &tm_wo, b2full, j * 64, h0, 0);
+        // in n-halves: half 0 of chunk c refills while MMA2(c-1) still works on
+        // half 1 (a single 32 KB buffer put the weight load between every two
+        // chunks' MMA2s)
+        for (int q = 0; q < 2; ++q) {
+          mbar_wait(&b2empty[q], ((uint32_t)c & 1u) ^ 1u);
+          mbar_expect_tx(&b2full[q], kB2Bytes / 2);
+          for (int j = 2 * q; j < 2 * q + 2; ++j)
+            tma_load_3d(sB2 + j * 8192, &tm_wo, &b2full[q], j * 64, h0, 0);
+        }
       }
     }
   } else if (warp == 3 + kEW) {
@@ -307,18 +314,24 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
     if (lane == 0) {
       // ---------------- MMA2 issuer (its own thread: MMA1 never waits behind
       // an epilogue hand-off; the two write disjoint TMEM accumulators)
-      constexpr uint32_t id2 = idesc_f16(kBM, kF, 0, 1);
+      // two N = 128 halves per chunk (columns 0-127, 128-255 of acc2): every
+      // output column still accumulates the same 16-deep steps in the same order
+      constexpr uint32_t id2 = idesc_f16(kBM, kF / 2, 0, 1);
       const uint64_t d_a2 = sdesc(smem_u32(sA2), 16, 1024, kLayoutSW128);
       const uint64_t d_b2 = sdesc(smem_u32(sB2), 8192, 1024, kLayoutSW128);
       for (int p = 0; p < nc; ++p) {  // acc2 += ff(p) . W_out[chunk p]
         mbar_wait(staged, (uint32_t)p & 1u);
-        mbar_wait(b2full, (uint32_t)p & 1u);
-        tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          tc_mma_f16(tmem + 256u, d_a2 + (uint64_t)((kk * 32) >> 4),
-                     d_b2 + (uint64_t)((kk * 2048) >> 4), id2, (p > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(b2empty);
+        for (int q = 0; q < 2; ++q) {
+          mbar_wait(&b2full[q], (uint32_t)p & 1u);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma_f16(tmem + 256u + (uint32_t)(q * kF / 2), d_a2 + (uint64_t)((kk * 32) >> 4),
+                       d_b2 + (uint64_t)((q * 16384 + kk * 2048) >> 4), id2,
+                       (p > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(&b2empty[q]);
+        }
         tc_commit(a2empty);
       }
       tc_commit(t2full);
@@ -602,9 +615,9 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
   uint64_t* a1full = bar;
   uint64_t* b1full = bar + 1;
   uint64_t* b1empty = b1full + kB1Stages;
-  uint64_t* b2full = b1empty + kB1Stages;
-  uint64_t* b2empty = b2full + 1;
-  uint64_t* tfull1 = b2empty + 1;  // [2]
+  uint64_t* b2full = b1empty + kB1Stages;  // [2] W_0^T / W_1^T blocks of a chunk
+  uint64_t* b2empty = b2full + 2;          // [2]
+  uint64_t* tfull1 = b2empty + 2;  // [2]
   uint64_t* tempty1 = tfull1 + 2;  // [2]
   uint64_t* dfull = tempty1 + 2;   // [2] D tiles of a chunk loaded into staging buffer u
   uint64_t* staged = dfull + 2;    // g_H of a chunk written (one arrive per epilogue warp)
@@ -628,8 +641,10 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
       mbar_init(&b1full[s], 1);
       mbar_init(&b1empty[s], 1);
     }
-    mbar_init(b2full, 1);
-    mbar_init(b2empty, 1);
+    for (int q = 0; q < 2; ++q) {
+      mbar_init(&b2full[q], 1);
+      mbar_init(&b2empty[q], 1);
+    }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull1[b], 1);
       mbar_init(&tempty1[b], kEW);
@@ -686,9 +701,13 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
         const int h0 = h_begin + c * kHC;
         if (c + 1 < nc)
           for (int z = 0; z < 2; ++z) tma_prefetch_3d(&tm_wb, h0 + kHC, 0, z);
-        mbar_wait(b2empty, ((uint32_t)c & 1u) ^ 1u);
-        mbar_expect_tx(b2full, kB2Bytes);
-        for (int z = 0; z < 2; ++z) tma_load_3d(sB2 + z * (kF * 128), &tm_wb, b2full, h0, 0, z);
+        // per branch: W_0^T of chunk c refills while MMA2(c-1) still works on
+        // branch 1 (one 64 KB buffer put the load between every two chunks)
+        for (int z = 0; z < 2; ++z) {
+          mbar_wait(&b2empty[z], ((uint32_t)c & 1u) ^ 1u);
+          mbar_expect_tx(&b2full[z], kB2Bytes / 2);
+          tma_load_3d(sB2 + z * (kF * 128), &tm_wb, &b2full[z], h0, 0, z);
+        }
       }
     }
   } else if (warp == 3 + kEW) {
@@ -753,16 +772,17 @@ k_mbrb_bwd_fused(const __grid_constant__ CUtensorMap tm_g, const __grid_constant
       for (int c = 0; c < nc; ++c) {
         const int u = c & 1;
         mbar_wait(staged, (uint32_t)c & 1u);
-        mbar_wait(b2full, (uint32_t)c & 1u);
-        tc_fence_after();
 #pragma unroll
-        for (int z = 0; z < 2; ++z)
+        for (int z = 0; z < 2; ++z) {
+          mbar_wait(&b2full[z], (uint32_t)c & 1u);
+          tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             tc_mma_f16(tmem + 256u, d_s + (uint64_t)(((2 * u + z) * kTile + kk * 32) >> 4),
                        d_b2 + (uint64_t)((z * (kF * 128) + kk * 32) >> 4), id2,
                        (c > 0 || z > 0 || kk > 0) ? 1u : 0u);
-        tc_commit(b2empty);
+          tc_commit(&b2empty[z]);
+        }
         tc_commit(a2empty);
       }
       tc_commit(t2full);
