@@ -52,6 +52,21 @@ def test_random_geometry_roundtrips():
         assert roundtrip(data, cfg, segments) == data, (lanes, segments, n)
 
 
+def test_pooled_context_memory_reuse_and_trim():
+    """Context buffers come from the device's stream-ordered pool and are reused
+    by the next context; reused (non-zeroed) memory and a trimmed pool give the
+    same container bytes (every buffer a step reads is written first)."""
+    from paper_2507_18969_b200 import _lib
+    cfg = ModelConfig(**PAPER, lanes=1024)  # the benchmark's numerics (tcgen05, fused MBRB)
+    data = synth.text_like(1024 * 40, 2)
+    first = write_container(compress(data, cfg, 64))
+    again = write_container(compress(data, cfg, 64))
+    _lib.check(_lib.load().edpc_trim_pool(0))
+    trimmed = write_container(compress(data, cfg, 64))
+    assert first == again == trimmed
+    assert decompress(read_container(first)) == data
+
+
 def test_repeated_byte_compresses_hard():
     data = b"a" * 65536
     cfg = tiny_cfg(lanes=16, context_len=8)

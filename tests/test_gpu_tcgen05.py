@@ -158,13 +158,14 @@ def test_tc_gemm_f16_unit(M, N, K, a_mn, b_mn):
 
 
 @pytest.mark.parametrize("switch", ["EDPC_MBRB_FUSED", "EDPC_LTE_LN_FUSED", "EDPC_WGRAD_FUSED",
-                                    "EDPC_WGRAD_SUBTREE"])
+                                    "EDPC_WGRAD_SUBTREE", "EDPC_L2_PERSIST"])
 def test_fused_kernels_are_bit_identical(switch):
     """The fused MBRB forward / backward kernels (mbrb_fused.cuh), the subtree
     weight-gradient kernels and the fused weight-gradient + tree + Adam
     kernels (wgrad_adam.cuh) give exactly the per-group partial path's
-    container (the switch flips the default, in a subprocess: the switches are
-    read once per process)."""
+    container, and so does the run without the persisting-L2 window over U
+    (the switch flips the default, in a subprocess: the switches are read
+    once per process)."""
     import os
     import subprocess
     import sys
@@ -181,7 +182,7 @@ def test_fused_kernels_are_bit_identical(switch):
             % root)
     env = dict(os.environ, PYTHONPATH=root)
     # the non-default path: fused kernels switched off, experimental ones on
-    env[switch] = "0" if switch in ("EDPC_MBRB_FUSED", "EDPC_LTE_LN_FUSED") else "1"
+    env[switch] = "0" if switch in ("EDPC_MBRB_FUSED", "EDPC_LTE_LN_FUSED", "EDPC_L2_PERSIST") else "1"
     ref = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
                          timeout=600).stdout
     assert blob == ref
