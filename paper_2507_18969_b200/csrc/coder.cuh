@@ -296,26 +296,31 @@ __device__ __forceinline__ uint32_t read_bit(const uint8_t* data, int64_t bit_le
 __device__ __forceinline__ bool dec_advance(DecState& st, const uint8_t* data,
                                             int64_t bit_length, uint64_t span, uint32_t c_lo,
                                             uint32_t c_hi) {
-  uint64_t low = st.low, code = st.code;
-  uint64_t high = low + ((span * c_hi) >> 16) - 1;
-  low = low + ((span * c_lo) >> 16);
+  // low <= code <= high < 2^32 throughout (the coder's 32-bit registers), and
+  // every shift below starts from a value < 2^31, so the renormalisation runs
+  // in 32-bit registers (half the instructions of the 64-bit form on this
+  // serial decode chain); only the interval update needs the 64-bit product
+  uint32_t code = (uint32_t)st.code;
+  uint32_t high = (uint32_t)(st.low + ((span * c_hi) >> 16) - 1);
+  uint32_t low = (uint32_t)(st.low + ((span * c_lo) >> 16));
+  constexpr uint32_t kH = (uint32_t)kHalf, kQ = (uint32_t)kQuarter, kTQ = (uint32_t)kThreeQ;
   int64_t bp = st.bitpos;
   const int64_t limit = bit_length + 64;
   for (;;) {
-    if (high < kHalf) {
-    } else if (low >= kHalf) {
-      low -= kHalf;
-      high -= kHalf;
-      code -= kHalf;
-    } else if (low >= kQuarter && high < kThreeQ) {
-      low -= kQuarter;
-      high -= kQuarter;
-      code -= kQuarter;
+    if (high < kH) {
+    } else if (low >= kH) {
+      low -= kH;
+      high -= kH;
+      code -= kH;
+    } else if (low >= kQ && high < kTQ) {
+      low -= kQ;
+      high -= kQ;
+      code -= kQ;
     } else {
       break;
     }
     low <<= 1;
-    high = (high << 1) | 1;
+    high = (high << 1) | 1u;
     uint32_t bit = 0;
     if (bp < bit_length) {
       const int64_t bi = bp >> 3;
