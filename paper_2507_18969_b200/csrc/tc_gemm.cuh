@@ -883,13 +883,18 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
                 // fp16 MN-major: 64-wide boxes of 64 K-rows, 16-byte chunk c of
                 // row k at c ^ (k & 7) (SWIZZLE_128B); this thread's column
                 // pair (n, n + 1) is one half2 per row
+                // (32-bit shared addresses: LDS with immediate offsets, not
+                // generic 64-bit loads -- these warps gate every stage's release)
                 const int box = n >> 6, nn = n & 63, chunk = nn >> 3;
-                const uint8_t* base = sb + box * 8192 + (nn & 7) * 2;
+                const uint32_t base = smem_u32(sb + box * 8192 + (nn & 7) * 2);
                 float s0 = 0.f, s1 = 0.f;
 #pragma unroll 8
                 for (int k = 0; k < BK; ++k) {
-                  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(
-                      base + k * 128 + ((chunk ^ (k & 7)) << 4)));
+                  uint32_t w;
+                  asm volatile("ld.shared.b32 %0, [%1];"
+                               : "=r"(w)
+                               : "r"(base + (uint32_t)(k * 128 + ((chunk ^ (k & 7)) << 4))));
+                  const float2 f = __half22float2(*reinterpret_cast<const __half2*>(&w));
                   s0 += f.x;
                   s1 += f.y;
                 }
@@ -897,10 +902,15 @@ k_tc_gemm(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUt
                 sum2[j] += s1;
               } else {
                 const int box = n >> 5, nn = n & 31, chunk = nn >> 3;
-                const float* base = reinterpret_cast<const float*>(sb + box * 4096) + (nn & 7);
+                const uint32_t base = smem_u32(sb + box * 4096) + (uint32_t)(nn & 7) * 4u;
 #pragma unroll 8
-                for (int k = 0; k < kTcBK; ++k)
-                  sum[j] += base[(k * 128 + ((chunk ^ (k & 3)) << 5)) >> 2];
+                for (int k = 0; k < kTcBK; ++k) {
+                  float v;
+                  asm volatile("ld.shared.f32 %0, [%1];"
+                               : "=f"(v)
+                               : "r"(base + (uint32_t)(k * 128 + ((chunk ^ (k & 3)) << 5))));
+                  sum[j] += v;
+                }
               }
             }
           }
