@@ -372,22 +372,26 @@ struct TsIo {
   int* next;     // ring position (persists across blocks)
   int ib;        // first slot of this block's input boxes (in / put_at)
   // row `lane` of box `slot`: 16-byte chunk j at j ^ (lane & 7) (SWIZZLE_128B)
+  // (32-bit shared-window addresses: STS/LDS, not generic 64-bit accesses)
   __device__ __forceinline__ void write_row(int slot, const float (&v)[32]) const {
     const int lane = threadIdx.x & 31;
-    float* box = slots + slot * SF + lane * 32;
+    const uint32_t box = smem_u32(slots + slot * SF + lane * 32);
 #pragma unroll
     for (int j = 0; j < 8; ++j)
-      *reinterpret_cast<float4*>(box + ((j ^ (lane & 7)) << 2)) =
-          make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(
+                       box + (uint32_t)((j ^ (lane & 7)) << 4)),
+                   "f"(v[4 * j]), "f"(v[4 * j + 1]), "f"(v[4 * j + 2]), "f"(v[4 * j + 3])
+                   : "memory");
   }
   __device__ __forceinline__ void in(int slot, float (&v)[32]) const {
     const int lane = threadIdx.x & 31;
-    const float* box = slots + (ib + slot) * SF + lane * 32;
+    const uint32_t box = smem_u32(slots + (ib + slot) * SF + lane * 32);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const float4 q = *reinterpret_cast<const float4*>(box + ((j ^ (lane & 7)) << 2));
-      v[4 * j] = q.x; v[4 * j + 1] = q.y; v[4 * j + 2] = q.z; v[4 * j + 3] = q.w;
-    }
+    for (int j = 0; j < 8; ++j)
+      asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                   : "=f"(v[4 * j]), "=f"(v[4 * j + 1]), "=f"(v[4 * j + 2]), "=f"(v[4 * j + 3])
+                   : "r"(box + (uint32_t)((j ^ (lane & 7)) << 4))
+                   : "memory");
   }
   __device__ __forceinline__ void issue(int slot, int map, int c2, int c3) const {
     fence_async_smem();
