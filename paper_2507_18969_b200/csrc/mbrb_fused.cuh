@@ -351,13 +351,17 @@ k_mbrb_fwd_fused(const __grid_constant__ CUtensorMap tm_x0, const __grid_constan
       const int b = c & 1;
       const int h0 = h_begin + c * kHC;
       float4 bc0[kCW / 4], bc1[kCW / 4];
-      {
-        const float4* q0 = reinterpret_cast<const float4*>(sBiasT + c * kHC + half * kCW);
-        const float4* q1 = reinterpret_cast<const float4*>(sBiasT + hs + c * kHC + half * kCW);
+      {  // LDS.128 through the shared window (generic loads cost 64-bit address math)
+        const uint32_t q0 = smem_u32(sBiasT + c * kHC + half * kCW);
+        const uint32_t q1 = smem_u32(sBiasT + hs + c * kHC + half * kCW);
 #pragma unroll
         for (int j = 0; j < kCW / 4; ++j) {
-          bc0[j] = q0[j];
-          bc1[j] = q1[j];
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(bc0[j].x), "=f"(bc0[j].y), "=f"(bc0[j].z), "=f"(bc0[j].w)
+                       : "r"(q0 + 16u * j));
+          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                       : "=f"(bc1[j].x), "=f"(bc1[j].y), "=f"(bc1[j].z), "=f"(bc1[j].w)
+                       : "r"(q1 + 16u * j));
         }
       }
       mbar_wait(&tfull1[b], (uint32_t)(c >> 1) & 1u);
