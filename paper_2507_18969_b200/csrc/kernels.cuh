@@ -1117,7 +1117,50 @@ __global__ void k_adam_shared(float* __restrict__ W, float* __restrict__ M, floa
   pdl_entry();
   float bc1, bc2;
   adam_bc(c, b1d, b2d, si.T(), bc1, bc2);
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+  int64_t head = 0;
+  // 16-byte vectors when every stream is aligned (same per-element
+  // arithmetic, so bit-identical); the scalar loop takes the tail
+  const bool vec = ((((uintptr_t)W | (uintptr_t)M | (uintptr_t)V | (uintptr_t)P |
+                      (uintptr_t)Wt) & 15) == 0) &&
+                   (pstride & 3) == 0 && ((uintptr_t)Wh & 7) == 0;
+  if (vec) {
+    const int64_t n4 = n >> 2;
+    for (int64_t e4 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e4 < n4;
+         e4 += (int64_t)gridDim.x * blockDim.x) {
+      float4 q4[NL];
+#pragma unroll
+      for (int g = 0; g < NL; ++g) q4[g] = reinterpret_cast<const float4*>(P + g * pstride)[e4];
+      float4 w4 = reinterpret_cast<const float4*>(W)[e4];
+      float4 m4 = reinterpret_cast<const float4*>(M)[e4];
+      float4 v4 = reinterpret_cast<const float4*>(V)[e4];
+      float* wv = &w4.x;
+      float* mv = &m4.x;
+      float* vv = &v4.x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float q[NL];
+#pragma unroll
+        for (int g = 0; g < NL; ++g) q[g] = (&q4[g].x)[j];
+        const float grad = tree_sum<NL>(q) * ginv;
+        adam_elem(wv[j], mv[j], vv[j], grad, c, bc1, bc2);
+      }
+      reinterpret_cast<float4*>(W)[e4] = w4;
+      reinterpret_cast<float4*>(M)[e4] = m4;
+      reinterpret_cast<float4*>(V)[e4] = v4;
+      if (Wh) {
+        __half2 h0 = __floats2half2_rn(w4.x, w4.y), h1 = __floats2half2_rn(w4.z, w4.w);
+        uint2 hh;
+        hh.x = *reinterpret_cast<uint32_t*>(&h0);
+        hh.y = *reinterpret_cast<uint32_t*>(&h1);
+        reinterpret_cast<uint2*>(Wh)[e4] = hh;
+      }
+      if (Wt)
+        reinterpret_cast<float4*>(Wt)[e4] =
+            make_float4(tf32_rna(w4.x), tf32_rna(w4.y), tf32_rna(w4.z), tf32_rna(w4.w));
+    }
+    head = n4 << 2;
+  }
+  for (int64_t e = head + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     float q[NL];
 #pragma unroll
