@@ -1086,8 +1086,9 @@ static int backward(edpc_ctx* c, ByteCols src, float* nll, bool have_dlogits = f
                      ldexpf(1.0f, -c->gs_log2));
         };
         // (a split variant -- FDM backward on the main stream, U's Adam pass on
-        // the side stream -- measured 3% slower at C2: the passes compete for
-        // HBM and U is read twice)
+        // the side stream -- measured 3% slower at C2 in round 1 and 6% slower
+        // in round 2 (9.44 -> 8.89 MB/s A/B): the passes compete for HBM and U
+        // is read twice)
         if (FP == 64)
           run(k_fdm_bwd_adam_v<64>, c->st);
         else if (FP == 128)
