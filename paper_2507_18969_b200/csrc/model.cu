@@ -1366,7 +1366,7 @@ static int model_step(edpc_ctx* c, int mode, int advance = 1) {
 // CUDA graphs: kGraphSteps consecutive model steps are captured once per
 // mode and replayed; the step index lives in device memory (d_i / d_t) and is
 // advanced by the last kernel of each step, so replays need no host input.
-constexpr int kGraphSteps = 8;
+constexpr int kGraphSteps = 16;
 
 static bool graphs_enabled() {
   static int v = -1;
